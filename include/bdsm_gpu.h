@@ -1,0 +1,171 @@
+/* bdsm_gpu.h — C ABI of the B200-native batch-dynamic subgraph matching engine
+ * (libbdsm_b200.so).  Plain pointers and sizes only; no CUDA or torch types.
+ *
+ * The reference has no FFI: its boundary is the bdsm_core C++ API
+ * (SURVEY.md §8(b)).  Each entry point below replaces the reference call
+ * named beside it; INTEGRATION.md shows the bindings (C++ wrapper, ctypes).
+ *
+ * Semantics are the reference's with MatchOptions{coalesce=false} (SURVEY.md
+ * F1), with its brute-force oracle's edge-label and vertex-label rules
+ * (F4, F5): per batch the engine returns |positive| = |Matches(G') \ Matches(G)|
+ * and |negative| = |Matches(G) \ Matches(G')| for every registered query.
+ */
+#ifndef BDSM_GPU_H_
+#define BDSM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BDSM_API __attribute__((visibility("default")))
+#else
+#define BDSM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BDSM_NO_LABEL 0xffffffffu /* "no edge label" (reference: std::nullopt) */
+
+/* Status codes map one-to-one onto the reference's exceptions. */
+typedef enum bdsm_status {
+  BDSM_OK = 0,
+  BDSM_BATCH_ERROR = 1,      /* bdsm::BatchError (src/graph.cpp:117-143, src/matcher.cpp:373-378) */
+  BDSM_INVALID_ARGUMENT = 2, /* std::invalid_argument: self-loop / conflicting pair in a batch
+                                (src/graph.cpp:13-20), bad graph (src/graph.cpp:38-64) or query
+                                (src/query_graph.cpp:14-22, src/query_analysis.cpp:361,367) */
+  BDSM_RUNTIME_ERROR = 3,    /* std::runtime_error (src/scheduler.cpp:281-283) */
+  BDSM_CUDA_ERROR = 4,       /* device failure (no reference counterpart) */
+  BDSM_OUT_OF_MEMORY = 5     /* std::bad_alloc */
+} bdsm_status;
+
+typedef struct bdsm_engine bdsm_engine;
+
+/* Data graph: replaces LabeledGraph::build_from_edges(vertices, edges)
+ * (include/bdsm/graph.hpp:69-70, src/graph.cpp:35-72).  Vertex ids are dense
+ * 0..num_vertices-1; edges are undirected, simple, without self-loops. */
+typedef struct bdsm_graph_desc {
+  uint32_t num_vertices;
+  const uint32_t* vertex_labels; /* [num_vertices] */
+  uint64_t num_edges;
+  const uint32_t* src;           /* [num_edges] */
+  const uint32_t* dst;           /* [num_edges] */
+  const uint32_t* edge_labels;   /* [num_edges] or NULL; BDSM_NO_LABEL = none */
+} bdsm_graph_desc;
+
+/* Query: replaces QueryGraph(labels, edges) (include/bdsm/query_graph.hpp:24). */
+typedef struct bdsm_query_desc {
+  uint32_t num_vertices;         /* <= 32 (reference limit); connected */
+  const uint32_t* vertex_labels;
+  uint32_t num_edges;
+  const uint32_t* a;
+  const uint32_t* b;
+  const uint32_t* edge_labels;   /* [num_edges] or NULL */
+} bdsm_query_desc;
+
+typedef struct bdsm_options {
+  uint32_t group_bits;   /* NLF counter width M (reference default 2; PipelineConfig::group_bits) */
+  uint32_t coalesce;     /* must be 0: coalesced search is not exact in the reference (F1) */
+  int32_t device;        /* CUDA device ordinal */
+  uint32_t shard_rank;   /* multi-GPU: this rank's share of the work units */
+  uint32_t shard_world;  /* 0 or 1 = whole batch */
+  float slack;           /* per-vertex adjacency slack fraction (default 0.25) */
+  float pool_reserve;    /* extra adjacency pool for relocations, fraction of 2|E| (default 0.5) */
+  uint32_t chunk;        /* level-2 work-unit size (default 64) */
+} bdsm_options;
+
+/* One update: replaces EdgeUpdate (include/bdsm/graph.hpp:14-22).  The batch
+ * order is the array index, as in UpdateBatch (src/graph.cpp:21). */
+typedef struct bdsm_update {
+  uint32_t u;
+  uint32_t v;
+  uint32_t op;          /* 0 insert, 1 delete */
+  uint32_t edge_label;  /* inserts only; BDSM_NO_LABEL = none */
+} bdsm_update;
+
+/* Replaces UpdateError{index, reason} (include/bdsm/graph.hpp:36-39). */
+typedef struct bdsm_update_error {
+  uint64_t index;
+  uint32_t reason;      /* 1 unknown vertex, 2 insert of existing edge, 3 delete of missing edge */
+} bdsm_update_error;
+
+/* Per-batch counters (MatchStats, include/bdsm/search.hpp:18-36, plus
+ * device timing and the SURVEY.md §8(d) algorithmic byte counts). */
+typedef struct bdsm_batch_stats {
+  double ms_total;        /* host wall time of the call */
+  double ms_device;       /* CUDA-event time of the whole device sequence */
+  double ms_negative;     /* matching kernel, negative phase(s) */
+  double ms_update;       /* sort + merge + refresh */
+  double ms_positive;     /* matching kernel, positive phase(s) */
+  uint64_t dfs_visits;    /* candidates accepted at levels >= 2 */
+  uint64_t tasks;         /* (update, query edge, orientation) anchors */
+  uint64_t work_items;    /* level-2 chunks scheduled */
+  uint64_t gen_calls;     /* GenCandidates calls (levels whose candidates were generated) */
+  uint64_t bytes_phase;   /* B_phase: 4 B x backward-neighbour degrees per GenCandidates call */
+  uint64_t bytes_update;  /* B_upd: 16|dB| + 4 x (old + new degree) of touched vertices */
+  uint64_t touched;       /* distinct batch endpoints */
+  uint64_t relocations;   /* adjacency lists moved to the append pool */
+  uint32_t compactions;   /* pool compactions triggered by this batch */
+  uint32_t timed_out;     /* bitmask of queries whose deadline passed (counts dropped) */
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+} bdsm_batch_stats;
+
+/* Engine lifecycle.  Replaces LabeledGraph::build_from_edges plus the
+ * device-resident copy of the graph (PackedMemoryArray, src/pma.cpp). */
+BDSM_API bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options* opts,
+                               bdsm_engine** out);
+BDSM_API void bdsm_engine_destroy(bdsm_engine* engine);
+
+/* Registers a query: QueryEncodingState::initialize (src/matcher.cpp:10-18) +
+ * build_query_plan with coalescing off (src/query_analysis.cpp:358-363,
+ * :437-441).  Returns the query index (>= 0) or -status. */
+BDSM_API int bdsm_engine_add_query(bdsm_engine* engine, const bdsm_query_desc* query);
+
+/* match_batch (src/matcher.cpp:370-389) over every registered query: validate,
+ * negative phase on G, apply, refresh, positive phase on G'.  `updates` is
+ * HOST memory.  pos/neg receive one count per query.  All-or-nothing: on
+ * BDSM_BATCH_ERROR / BDSM_INVALID_ARGUMENT the graph is unchanged. */
+BDSM_API bdsm_status bdsm_engine_apply_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n,
+                                    uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats);
+
+/* Same, with `updates` already resident in device memory (HBM). */
+BDSM_API bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const bdsm_update* d_updates,
+                                           size_t n, uint64_t* pos, uint64_t* neg,
+                                           bdsm_batch_stats* stats);
+
+/* Per-query time budget in seconds for subsequent batches (MatchOptions::
+ * deadline, PipelineConfig::timeout_seconds); <= 0 disables. */
+BDSM_API bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seconds_from_now);
+
+/* After BDSM_BATCH_ERROR: the failures in batch order (BatchError::failures).
+ * Returns the total number of failures. */
+BDSM_API size_t bdsm_last_batch_errors(bdsm_engine* engine, bdsm_update_error* out, size_t cap);
+
+/* Message of the last failing call on this thread (exception::what()). */
+BDSM_API const char* bdsm_last_error(void);
+
+/* Introspection (tests, CLI): sorted neighbours of v (returns the degree),
+ * candidate rows of a query, matching order for (query, edge), counts. */
+BDSM_API size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, size_t cap);
+BDSM_API bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out /* [V] */);
+BDSM_API int bdsm_engine_order(bdsm_engine* engine, int query, uint32_t edge, uint32_t* out /* [32] */);
+BDSM_API bdsm_status bdsm_engine_column_sizes(bdsm_engine* engine, int query, uint64_t* out /* [n] */);
+BDSM_API uint64_t bdsm_engine_num_edges(bdsm_engine* engine);
+BDSM_API uint32_t bdsm_engine_num_vertices(bdsm_engine* engine);
+/* Rebuild the plan of a query from the current candidate columns
+ * (drift replanning, src/bench.cpp:451-453). */
+BDSM_API bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query);
+
+/* Multi-GPU work split: owner rank of each work unit given
+ * its cost, in canonical order.  owner = floor(world * prefix / total).
+ * Pure host function, used by the engine and by the CPU tests. */
+BDSM_API void bdsm_shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);
+
+BDSM_API const char* bdsm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDSM_GPU_H_ */

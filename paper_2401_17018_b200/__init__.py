@@ -1,0 +1,338 @@
+"""B200-native batch-dynamic subgraph matching (GAMMA, arXiv 2401.17018).
+
+Python binding of the C ABI in include/bdsm_gpu.h (libbdsm_b200.so, built
+in-tree by paper_2401_17018_b200/build.sh).  It mirrors the reference's
+bdsm_core API for the hot path:
+
+  reference (C++)                                  here
+  ----------------------------------------------   -----------------------------
+  LabeledGraph::build_from_edges (graph.cpp:35)    Engine(vlabels, src, dst, ...)
+  QueryGraph + QueryEncodingState::initialize +
+    build_query_plan (coalesce off)                Engine.add_query(labels, edges)
+  UpdateBatch + match_batch (matcher.cpp:370)      Engine.match_batch(updates)
+  BatchError / std::invalid_argument               BatchError / ValueError
+
+The engine returns per-query counts |positive| and |negative| (the reference
+returns the match vectors whose sizes the CLI reports in deltas.csv).  There
+is no CPU fallback: importing this package without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = ["Engine", "BatchError", "EngineError", "UPDATE_DTYPE", "make_updates", "lib_path",
+           "shard_owners", "NO_LABEL"]
+
+NO_LABEL = 0xFFFFFFFF
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libbdsm_b200.so")
+
+
+UPDATE_DTYPE = np.dtype([("u", "<u4"), ("v", "<u4"), ("op", "<u4"), ("elab", "<u4")])
+
+
+class _GraphDesc(C.Structure):
+    _fields_ = [("num_vertices", C.c_uint32), ("vertex_labels", C.c_void_p), ("num_edges", C.c_uint64),
+                ("src", C.c_void_p), ("dst", C.c_void_p), ("edge_labels", C.c_void_p)]
+
+
+class _QueryDesc(C.Structure):
+    _fields_ = [("num_vertices", C.c_uint32), ("vertex_labels", C.c_void_p), ("num_edges", C.c_uint32),
+                ("a", C.c_void_p), ("b", C.c_void_p), ("edge_labels", C.c_void_p)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("group_bits", C.c_uint32), ("coalesce", C.c_uint32), ("device", C.c_int32),
+                ("shard_rank", C.c_uint32), ("shard_world", C.c_uint32), ("slack", C.c_float),
+                ("pool_reserve", C.c_float), ("chunk", C.c_uint32)]
+
+
+class _UpdateError(C.Structure):
+    _fields_ = [("index", C.c_uint64), ("reason", C.c_uint32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("ms_total", C.c_double), ("ms_device", C.c_double), ("ms_negative", C.c_double),
+                ("ms_update", C.c_double), ("ms_positive", C.c_double), ("dfs_visits", C.c_uint64),
+                ("tasks", C.c_uint64), ("work_items", C.c_uint64), ("gen_calls", C.c_uint64),
+                ("bytes_phase", C.c_uint64), ("bytes_update", C.c_uint64), ("touched", C.c_uint64),
+                ("relocations", C.c_uint64), ("compactions", C.c_uint32), ("timed_out", C.c_uint32),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA engine first "
+            "(python -c 'import __graft_entry__ as g; g.build()' or paper_2401_17018_b200/build.sh)")
+    L = C.CDLL(path)
+    L.bdsm_engine_create.restype = C.c_int
+    L.bdsm_engine_create.argtypes = [C.POINTER(_GraphDesc), C.POINTER(_Options), C.POINTER(C.c_void_p)]
+    L.bdsm_engine_destroy.restype = None
+    L.bdsm_engine_destroy.argtypes = [C.c_void_p]
+    L.bdsm_engine_add_query.restype = C.c_int
+    L.bdsm_engine_add_query.argtypes = [C.c_void_p, C.POINTER(_QueryDesc)]
+    for name in ("bdsm_engine_apply_batch", "bdsm_engine_apply_batch_device"):
+        f = getattr(L, name)
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
+    L.bdsm_engine_set_deadline.restype = C.c_int
+    L.bdsm_engine_set_deadline.argtypes = [C.c_void_p, C.c_int, C.c_double]
+    L.bdsm_last_batch_errors.restype = C.c_size_t
+    L.bdsm_last_batch_errors.argtypes = [C.c_void_p, C.POINTER(_UpdateError), C.c_size_t]
+    L.bdsm_last_error.restype = C.c_char_p
+    L.bdsm_last_error.argtypes = []
+    L.bdsm_engine_neighbors.restype = C.c_size_t
+    L.bdsm_engine_neighbors.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_size_t]
+    L.bdsm_engine_rows.restype = C.c_int
+    L.bdsm_engine_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.bdsm_engine_order.restype = C.c_int
+    L.bdsm_engine_order.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.c_void_p]
+    L.bdsm_engine_column_sizes.restype = C.c_int
+    L.bdsm_engine_column_sizes.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.bdsm_engine_replan.restype = C.c_int
+    L.bdsm_engine_replan.argtypes = [C.c_void_p, C.c_int]
+    L.bdsm_engine_num_edges.restype = C.c_uint64
+    L.bdsm_engine_num_edges.argtypes = [C.c_void_p]
+    L.bdsm_engine_num_vertices.restype = C.c_uint32
+    L.bdsm_engine_num_vertices.argtypes = [C.c_void_p]
+    L.bdsm_shard_owners.restype = None
+    L.bdsm_shard_owners.argtypes = [C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]
+    L.bdsm_version.restype = C.c_char_p
+    L.bdsm_version.argtypes = []
+    _lib = L
+    return L
+
+
+def lib():
+    return _load()
+
+
+class EngineError(RuntimeError):
+    """Non-batch failure (CUDA error, out of memory, runtime error)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class BatchError(RuntimeError):
+    """bdsm::BatchError (include/bdsm/graph.hpp:42-52): all-or-nothing rejection.
+    failures: list of (index, reason) with reason 1 unknown vertex, 2 insert of
+    an existing edge, 3 delete of a missing edge."""
+
+    def __init__(self, msg: str, failures):
+        super().__init__(msg)
+        self.failures = failures
+
+
+_REASONS = {1: "unknown vertex", 2: "insert of existing edge", 3: "delete of missing edge"}
+
+
+def _raise(status: int, engine_handle=None):
+    msg = (lib().bdsm_last_error() or b"").decode()
+    if status == 1:
+        fails = []
+        if engine_handle:
+            n = lib().bdsm_last_batch_errors(engine_handle, None, 0)
+            buf = (_UpdateError * max(n, 1))()
+            lib().bdsm_last_batch_errors(engine_handle, buf, n)
+            fails = [(int(buf[i].index), int(buf[i].reason)) for i in range(n)]
+        raise BatchError(msg, fails)
+    if status == 2:
+        raise ValueError(msg)
+    if status == 5:
+        raise MemoryError(msg)
+    raise EngineError(status, msg)
+
+
+def _u32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint32))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def make_updates(updates) -> np.ndarray:
+    """Packs updates into the C ABI layout (bdsm_update: u, v, op, edge_label).
+    Accepts a structured array of UPDATE_DTYPE, an (n, 3|4) integer array, or an
+    iterable of (op, u, v[, label]) tuples with op 0 insert / 1 delete (the
+    tests' tuple order)."""
+    if isinstance(updates, np.ndarray) and updates.dtype == UPDATE_DTYPE:
+        return np.ascontiguousarray(updates)
+    rows = list(updates)
+    out = np.zeros(len(rows), dtype=UPDATE_DTYPE)
+    for i, r in enumerate(rows):
+        op, u, v = int(r[0]), int(r[1]), int(r[2])
+        lab = r[3] if len(r) > 3 else None
+        out[i] = (u, v, op, NO_LABEL if lab is None or lab < 0 else lab)
+    return out
+
+
+@dataclass
+class BatchResult:
+    positive: List[int]
+    negative: List[int]
+    stats: dict = field(default_factory=dict)
+
+
+def _stats_dict(s: _Stats) -> dict:
+    return {name: getattr(s, name) for name, _ in _Stats._fields_}
+
+
+class Engine:
+    """Device-resident dynamic graph + registered queries (one CUDA device)."""
+
+    def __init__(self, vertex_labels, src, dst, edge_labels=None, *, group_bits: int = 2, device: int = 0,
+                 shard_rank: int = 0, shard_world: int = 1, slack: float = 0.25, pool_reserve: float = 0.5,
+                 chunk: int = 64):
+        L = lib()
+        self._vl = _u32(vertex_labels)
+        s, d = _u32(src), _u32(dst)
+        el = None if edge_labels is None else _u32(edge_labels)
+        desc = _GraphDesc(len(self._vl), self._vl.ctypes.data, len(s), s.ctypes.data, d.ctypes.data,
+                          None if el is None else el.ctypes.data)
+        opts = _Options(group_bits, 0, device, shard_rank, shard_world, slack, pool_reserve, chunk)
+        h = C.c_void_p()
+        st = L.bdsm_engine_create(C.byref(desc), C.byref(opts), C.byref(h))
+        if st != 0:
+            _raise(st)
+        self._h = h
+        self.nq = 0
+        self.query_sizes: List[int] = []
+
+    @property
+    def handle(self):
+        return self._h
+
+    def add_query(self, labels: Sequence[int], edges: Iterable[Tuple]) -> int:
+        ql = _u32(labels)
+        edges = list(edges)
+        qa = _u32([e[0] for e in edges])
+        qb = _u32([e[1] for e in edges])
+        qlab = _u32([NO_LABEL if (len(e) < 3 or e[2] is None or e[2] < 0) else e[2] for e in edges])
+        desc = _QueryDesc(len(ql), ql.ctypes.data, len(qa), qa.ctypes.data if len(qa) else None,
+                          qb.ctypes.data if len(qb) else None, qlab.ctypes.data if len(qlab) else None)
+        r = lib().bdsm_engine_add_query(self._h, C.byref(desc))
+        if r < 0:
+            _raise(-r, self._h)
+        self.nq += 1
+        self.query_sizes.append(len(ql))
+        return r
+
+    def match_batch(self, updates) -> BatchResult:
+        """match_batch over every query; updates in HOST memory."""
+        ups = make_updates(updates)
+        pos = np.zeros(max(self.nq, 1), np.uint64)
+        neg = np.zeros(max(self.nq, 1), np.uint64)
+        st = _Stats()
+        r = lib().bdsm_engine_apply_batch(self._h, _ptr(ups) if len(ups) else None, len(ups), _ptr(pos),
+                                          _ptr(neg), C.byref(st))
+        if r != 0:
+            _raise(r, self._h)
+        return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
+
+    apply_batch = match_batch
+
+    def match_batch_device(self, dev_ptr: int, n: int) -> BatchResult:
+        """Same, with the packed updates already in device memory (e.g. a
+        torch uint8/int32 CUDA tensor's data_ptr())."""
+        pos = np.zeros(max(self.nq, 1), np.uint64)
+        neg = np.zeros(max(self.nq, 1), np.uint64)
+        st = _Stats()
+        r = lib().bdsm_engine_apply_batch_device(self._h, C.c_void_p(dev_ptr), n, _ptr(pos), _ptr(neg),
+                                                 C.byref(st))
+        if r != 0:
+            _raise(r, self._h)
+        return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
+
+    def set_deadline(self, query: int, seconds_from_now: float) -> None:
+        r = lib().bdsm_engine_set_deadline(self._h, query, seconds_from_now)
+        if r != 0:
+            _raise(r, self._h)
+
+    def neighbors(self, v: int) -> List[int]:
+        d = lib().bdsm_engine_neighbors(self._h, v, None, 0)
+        out = np.zeros(max(d, 1), np.uint32)
+        lib().bdsm_engine_neighbors(self._h, v, _ptr(out), d)
+        return out[:d].tolist()
+
+    def rows(self, query: int) -> np.ndarray:
+        out = np.zeros(max(self.num_vertices, 1), np.uint32)
+        r = lib().bdsm_engine_rows(self._h, query, _ptr(out))
+        if r != 0:
+            _raise(r, self._h)
+        return out[: self.num_vertices]
+
+    def order(self, query: int, edge: int) -> List[int]:
+        out = np.zeros(32, np.uint32)
+        n = lib().bdsm_engine_order(self._h, query, edge, _ptr(out))
+        if n < 0:
+            _raise(-n, self._h)
+        return out[:n].tolist()
+
+    def column_sizes(self, query: int) -> List[int]:
+        out = np.zeros(32, np.uint64)
+        r = lib().bdsm_engine_column_sizes(self._h, query, _ptr(out))
+        if r != 0:
+            _raise(r, self._h)
+        return out[: self.query_sizes[query]].tolist()
+
+    def replan(self, query: int) -> None:
+        r = lib().bdsm_engine_replan(self._h, query)
+        if r != 0:
+            _raise(r, self._h)
+
+    @property
+    def num_vertices(self) -> int:
+        return int(lib().bdsm_engine_num_vertices(self._h))
+
+    @property
+    def num_edges(self) -> int:
+        return int(lib().bdsm_engine_num_edges(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().bdsm_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def shard_owners(costs: Sequence[int], world: int) -> List[int]:
+    """Owner rank of each work unit (canonical order) under the cost-balanced
+    split used by the engine: floor(world * prefix / total)."""
+    c = np.ascontiguousarray(np.asarray(costs, dtype=np.uint64))
+    out = np.zeros(max(len(c), 1), np.uint32)
+    lib().bdsm_shard_owners(_ptr(c), len(c), world, _ptr(out))
+    return out[: len(c)].tolist()
+
+
+def version() -> str:
+    return lib().bdsm_version().decode()

@@ -1,0 +1,20 @@
+#!/usr/bin/env bash
+# Builds libbdsm_b200.so in-tree for sm_100a (no torch types; plain C ABI).
+set -euo pipefail
+HERE="$(cd "$(dirname "$0")" && pwd)"
+NVCC="${NVCC:-nvcc}"
+FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC
+       -Xcompiler -fvisibility=hidden -I"$HERE/../include" --expt-relaxed-constexpr -diag-suppress 177)
+OBJ="$HERE/build"
+mkdir -p "$OBJ"
+pids=()
+for f in store match engine; do
+  "$NVCC" "${FLAGS[@]}" -Xptxas -v -c "$HERE/csrc/$f.cu" -o "$OBJ/$f.o" 2> "$OBJ/$f.ptxas.log" &
+  pids+=($!)
+done
+g++ -std=c++17 -O3 -fPIC -fvisibility=hidden -I"$HERE/../include" -I/usr/local/cuda/include \
+    -c "$HERE/csrc/planner.cpp" -o "$OBJ/planner.o"
+for p in "${pids[@]}"; do wait "$p" || { cat "$OBJ"/*.ptxas.log; exit 1; }; done
+"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o "$HERE/libbdsm_b200.so" \
+    "$OBJ/store.o" "$OBJ/match.o" "$OBJ/engine.o" "$OBJ/planner.o"
+echo "built $HERE/libbdsm_b200.so"

@@ -1,0 +1,92 @@
+// Shared host/device definitions of the B200 engine (libbdsm_b200.so).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bdsm_b200 {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kMaxQ = 16;          // query vertices handled by the matching kernel
+constexpr int kMaxQEdges = kMaxQ * (kMaxQ - 1) / 2;
+constexpr int kWarpsPerBlock = 8;  // matching kernel: 256 threads
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Device view of the slack-padded dynamic CSR:
+// adj[off[v] .. off[v] + deg[v]) is v's sorted neighbour list, with room up to
+// cap[v] for in-place merges; offsets are 64-bit (F9) and 16-byte aligned.
+struct DevGraph {
+  uint32_t V;
+  const uint64_t* off;
+  const uint32_t* deg;
+  const uint32_t* cap;
+  const uint32_t* adj;
+  const uint32_t* elab;    // parallel to adj, or nullptr when no edge labels exist
+  const uint32_t* vlabel;
+};
+
+// Matching program of one (query, anchor edge): the matching order and, per
+// level l >= 2, the backward neighbours (positions j < l adjacent to order[l]),
+// the positions holding the same query label (injectivity candidates) and
+// the query-edge label of each backward edge.  Built by the host planner.
+struct LevelProg {
+  uint32_t qbit;                 // 1 << order[l] (candidate-row bit)
+  uint32_t backmask;             // positions j < l adjacent to order[l]
+  uint32_t eqmask;               // positions j < l with label(order[j]) == label(order[l])
+  uint32_t nback;
+  uint8_t back[kMaxQ];           // ascending positions
+  uint32_t elab[kMaxQ];          // query edge label of (order[back[b]], order[l])
+};
+
+struct EdgeProg {
+  uint32_t n;                    // query vertex count
+  uint32_t query;                // query index
+  uint32_t order[kMaxQ];
+  LevelProg lv[kMaxQ];
+};
+
+// Anchor-mapping table entry (map_update_to_query_edges, src/matcher.cpp:42-55).
+struct AnchorEdge {
+  uint32_t la, lb;               // labels of query endpoints a, b
+  uint32_t elab;                 // query edge label (kNone: unlabelled)
+  uint32_t prog;                 // EdgeProg index
+};
+
+// One anchor: (update, query edge, orientation) with its level-2 driver length.
+struct Task {
+  uint32_t upd;
+  uint32_t prog;
+  uint32_t flip;
+  uint32_t d;                    // level-2 driver length (0 for 2-vertex queries)
+};
+
+// One work unit: a chunk [begin, begin + chunk) of a task's level-2 driver.
+struct Item {
+  uint32_t task;
+  uint32_t begin;
+};
+
+// Device-side batch bookkeeping, copied back once per batch.
+struct BatchState {
+  uint32_t err_count;            // validate_batch failures
+  uint32_t selfloop_min;         // first self-loop update index (kNone: none)
+  uint32_t conflict_min;         // first conflicting update index (kNone: none)
+  uint32_t n_touched;            // distinct endpoints
+  uint32_t overflow;             // adjacency pool exhausted: merge skipped
+  uint32_t timed_out;            // bitmask over queries
+  uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
+  uint32_t n_items[2];
+  uint32_t next_item;            // work-queue head of the running phase
+  uint32_t pad;
+  uint64_t pool_top;             // adjacency pool bump pointer (elements)
+  uint64_t relocations;
+  uint64_t bytes_update;
+  uint64_t counts[2][32];        // [phase][query] matches
+  uint64_t visits;
+  uint64_t tasks_total;
+  uint64_t items_total;
+  uint64_t gen_calls;
+  uint64_t bytes_phase;
+};
+
+}  // namespace bdsm_b200

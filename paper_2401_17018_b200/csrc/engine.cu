@@ -1,0 +1,998 @@
+// Engine orchestration and the C ABI (include/bdsm_gpu.h).
+//
+// One engine = one device-resident dynamic CSR shared by N queries.  A batch
+// is one stream-ordered device sequence with a single host synchronisation at
+// the end (match_batch, reference src/matcher.cpp:370-389):
+//   H2D(batch) -> K1 validate/canonicalise -> radix sort of the 2|dB| directed
+//   keys -> segment heads / bitmaps -> [per query: K5 anchors -> K6 count on G]
+//   -> K3 merge + K4 refresh -> [per query: K5 -> K6 on G'] -> D2H(counts).
+// Every kernel after K1 checks the device-side error flags, so an invalid
+// batch is rejected all-or-nothing without a host round trip.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/bdsm_gpu.h"
+#include "kernels.cuh"
+#include "planner.hpp"
+
+using namespace bdsm_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct BatchRejected : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      if (e_ == cudaErrorMemoryAllocation) throw std::bad_alloc();                        \
+      throw CudaFailure(std::string(#expr) + ": " + cudaGetErrorString(e_));              \
+    }                                                                                     \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t want) {
+    if (want <= n && p) return;
+    release();
+    size_t alloc = std::max<size_t>(want, 1);
+    CK(cudaMalloc(&p, alloc * sizeof(T)));
+    n = alloc;
+  }
+  void ensure_grow(size_t want) {  // amortised growth
+    if (want <= n && p) return;
+    ensure(std::max<size_t>(want, n + n / 2));
+  }
+};
+
+struct QueryState {
+  HostQuery q;
+  QueryEncoding enc;
+  DevQueryEnc denc{};
+  DBuf<uint32_t> rows;
+  DBuf<uint64_t> colsize;
+  DBuf<EdgeProg> progs;
+  DBuf<AnchorEdge> anchors;
+  std::vector<std::vector<uint32_t>> orders;
+  uint64_t deadline_ns = 0;  // host-steady-clock based, translated per batch
+  double deadline_s = 0;     // seconds since epoch of the host steady clock
+  bool solved = true;
+};
+
+uint64_t now_ns() {
+  return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now().time_since_epoch())
+                      .count());
+}
+
+}  // namespace
+
+struct bdsm_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  bdsm_options opts{};
+  DevGraphMut g{};
+  uint64_t pool_top = 0;
+  uint64_t n_edges = 0;
+  bool has_elab = false;
+
+  DBuf<uint64_t> off;
+  DBuf<uint32_t> deg, cap, adj, elab, vlabel;
+
+  std::vector<std::unique_ptr<QueryState>> queries;
+  DBuf<DevQueryEnc> d_qenc;
+  DBuf<uint32_t*> d_rows;
+  DBuf<uint64_t*> d_colsize;
+
+  // batch buffers
+  DBuf<bdsm_update_dev> ups;
+  DBuf<uint64_t> keys, skeys;
+  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap;
+  DBuf<uint8_t> ecode, head;
+  DBuf<uint64_t> new_off;
+  DBuf<uint32_t> ins_bits, del_bits;
+  DBuf<uint32_t> upd_counts, upd_task_counts, item_off, task_off;
+  DBuf<uint64_t> upd_cost, cost_off;
+  DBuf<Task> tasks;
+  DBuf<Item> items;
+  size_t max_items = 0;
+  DBuf<uint8_t> cub_tmp;
+  DBuf<BatchState> d_st;
+  BatchState* h_st = nullptr;
+  bdsm_update* h_ups = nullptr;
+  size_t h_ups_cap = 0;
+  cudaEvent_t ev[6] = {};
+
+  std::vector<bdsm_update_error> last_errors;
+
+  ~bdsm_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (h_st) cudaFreeHost(h_st);
+    if (h_ups) cudaFreeHost(h_ups);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  DevGraph view() const {
+    DevGraph v;
+    v.V = g.V;
+    v.off = g.off;
+    v.deg = g.deg;
+    v.cap = g.cap;
+    v.adj = g.adj;
+    v.elab = g.elab;
+    v.vlabel = g.vlabel;
+    return v;
+  }
+
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+
+  // ---------------------------------------------------------------- build --
+  void build(const bdsm_graph_desc* d) {
+    const uint32_t V = d->num_vertices;
+    const uint64_t E = d->num_edges;
+    if (E && (!d->src || !d->dst)) throw std::invalid_argument("edge arrays are null");
+    if (V && !d->vertex_labels) throw std::invalid_argument("vertex labels are null");
+    g.V = V;
+    n_edges = E;
+    has_elab = false;
+    if (d->edge_labels) {
+      for (uint64_t i = 0; i < E; ++i)
+        if (d->edge_labels[i] != BDSM_NO_LABEL) {
+          has_elab = true;
+          break;
+        }
+    }
+    vlabel.ensure(V);
+    deg.ensure(V);
+    cap.ensure(V);
+    off.ensure(V);
+    if (V) CK(cudaMemcpyAsync(vlabel.p, d->vertex_labels, sizeof(uint32_t) * V, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemsetAsync(deg.p, 0, sizeof(uint32_t) * std::max<uint32_t>(V, 1), stream));
+    const uint64_t M = 2 * E;
+    DBuf<uint32_t> src, dst, labs;
+    DBuf<uint64_t> k0, k1, v0, v1, cap64, dense;
+    DBuf<uint32_t> bad;
+    bad.ensure(1);
+    CK(cudaMemsetAsync(bad.p, 0, 4, stream));
+    if (E) {
+      src.ensure(E);
+      dst.ensure(E);
+      CK(cudaMemcpyAsync(src.p, d->src, 4 * E, cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(dst.p, d->dst, 4 * E, cudaMemcpyHostToDevice, stream));
+      k0.ensure(M);
+      k1.ensure(M);
+      if (has_elab) {
+        v0.ensure(M);
+        v1.ensure(M);
+        labs.ensure(E);
+        CK(cudaMemcpyAsync(labs.p, d->edge_labels, 4 * E, cudaMemcpyHostToDevice, stream));
+      }
+      launch_build_keys(src.p, dst.p, E, V, k0.p, has_elab ? v0.p : nullptr, bad.p, stream);
+      src.release();
+      dst.release();
+      size_t tmp = 0;
+      cub::DoubleBuffer<uint64_t> kb(k0.p, k1.p), vb(v0.p, v1.p);
+      if (has_elab) {
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, int64_t(M), 0, 64, stream));
+        cub_tmp.ensure(tmp);
+        CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int64_t(M), 0, 64, stream));
+      } else {
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, int64_t(M), 0, 64, stream));
+        cub_tmp.ensure(tmp);
+        CK(cub::DeviceRadixSort::SortKeys(cub_tmp.p, tmp, kb, int64_t(M), 0, 64, stream));
+      }
+      uint64_t* sk = kb.Current();
+      uint64_t* sv = has_elab ? vb.Current() : nullptr;
+      launch_check_sorted_dups(sk, M, bad.p, stream);
+      uint32_t hbad = 0;
+      CK(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, stream));
+      sync();
+      if (hbad) throw_build_error(d, hbad);
+      launch_degrees(sk, M, deg.p, stream);
+      // capacities -> offsets; dense offsets for the scatter
+      cap64.ensure(V);
+      dense.ensure(V);
+      launch_caps(deg.p, V, opts.slack, cap.p, cap64.p, stream);
+      scan_u64_inplace(cap64.p, off.p, V);
+      // dense offsets: exclusive scan of deg (as u64)
+      scan_widen(deg.p, dense.p, V);
+      uint64_t last_off = 0;
+      uint32_t last_cap = 0;
+      CK(cudaMemcpyAsync(&last_off, off.p + (V - 1), 8, cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(&last_cap, cap.p + (V - 1), 4, cudaMemcpyDeviceToHost, stream));
+      sync();
+      pool_top = last_off + last_cap;
+      uint64_t reserve = std::max<uint64_t>(uint64_t(double(M) * opts.pool_reserve), 1u << 20);
+      g.pool_size = pool_top + reserve;
+      adj.ensure(g.pool_size);
+      if (has_elab) elab.ensure(g.pool_size);
+      launch_scatter(sk, sv, M, dense.p, off.p, adj.p, has_elab ? labs.p : nullptr,
+                     has_elab ? elab.p : nullptr, stream);
+    } else {
+      if (V) {
+        DBuf<uint64_t> cap64b;
+        cap64b.ensure(V);
+        launch_caps(deg.p, V, opts.slack, cap.p, cap64b.p, stream);
+        scan_u64_inplace(cap64b.p, off.p, V);
+        uint64_t last_off = 0;
+        uint32_t last_cap = 0;
+        CK(cudaMemcpyAsync(&last_off, off.p + (V - 1), 8, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&last_cap, cap.p + (V - 1), 4, cudaMemcpyDeviceToHost, stream));
+        sync();
+        pool_top = last_off + last_cap;
+      }
+      g.pool_size = pool_top + (1u << 20);
+      adj.ensure(g.pool_size);
+    }
+    sync();
+    refresh_graph_view();
+  }
+
+  void refresh_graph_view() {
+    g.off = off.p;
+    g.deg = deg.p;
+    g.cap = cap.p;
+    g.adj = adj.p;
+    g.elab = has_elab ? elab.p : nullptr;
+    g.vlabel = vlabel.p;
+  }
+
+  [[noreturn]] void throw_build_error(const bdsm_graph_desc* d, uint32_t bad) {
+    // Host rescan for the reference's exact message (src/graph.cpp:38-64).
+    for (uint64_t i = 0; i < d->num_edges; ++i) {
+      uint32_t u = d->src[i], v = d->dst[i];
+      if (u == v)
+        throw std::invalid_argument("self-loop edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
+      if (u >= d->num_vertices || v >= d->num_vertices)
+        throw std::invalid_argument("edge (" + std::to_string(u) + "," + std::to_string(v) +
+                                    ") references unknown vertex");
+    }
+    if (bad & 4u) throw std::invalid_argument("duplicate edge");
+    throw std::invalid_argument("invalid graph");
+  }
+
+  struct Widen {
+    __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+  };
+  void scan_widen(const uint32_t* in, uint64_t* out, uint64_t n) {
+    cub::TransformInputIterator<uint64_t, Widen, const uint32_t*> it(in, Widen{});
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, it, out, int64_t(n), stream));
+    cub_tmp.ensure(tmp);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, it, out, int64_t(n), stream));
+  }
+
+  void scan_u64_inplace(const uint64_t* in, uint64_t* out, uint64_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, int64_t(n), stream));
+    cub_tmp.ensure(tmp);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, in, out, int64_t(n), stream));
+  }
+
+  // Rebuild every list into a fresh pool with fresh slack (pool exhausted).
+  void compact(uint64_t extra_need) {
+    const uint32_t V = g.V;
+    DBuf<uint32_t> ncap;
+    DBuf<uint64_t> ncap64, noff;
+    ncap.ensure(V);
+    ncap64.ensure(V);
+    noff.ensure(V);
+    launch_caps(deg.p, V, opts.slack, ncap.p, ncap64.p, stream);
+    scan_u64_inplace(ncap64.p, noff.p, V);
+    uint64_t last_off = 0;
+    uint32_t last_cap = 0;
+    CK(cudaMemcpyAsync(&last_off, noff.p + (V - 1), 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&last_cap, ncap.p + (V - 1), 4, cudaMemcpyDeviceToHost, stream));
+    sync();
+    uint64_t used = last_off + last_cap;
+    uint64_t reserve = std::max<uint64_t>(uint64_t(double(used) * opts.pool_reserve), 1u << 20);
+    reserve = std::max(reserve, 2 * extra_need);
+    uint64_t size = used + reserve;
+    DBuf<uint32_t> nadj, nelab;
+    nadj.ensure(size);
+    if (has_elab) nelab.ensure(size);
+    launch_compact(g, noff.p, ncap.p, nadj.p, has_elab ? nelab.p : nullptr, stream);
+    sync();
+    std::swap(adj.p, nadj.p);
+    std::swap(adj.n, nadj.n);
+    if (has_elab) {
+      std::swap(elab.p, nelab.p);
+      std::swap(elab.n, nelab.n);
+    }
+    std::swap(off.p, noff.p);
+    std::swap(off.n, noff.n);
+    std::swap(cap.p, ncap.p);
+    std::swap(cap.n, ncap.n);
+    g.pool_size = size;
+    pool_top = used;
+    refresh_graph_view();
+  }
+
+  void enable_edge_labels() {
+    // A labelled insert into an unlabelled graph: materialise the parallel
+    // label array (all "none") once.
+    elab.ensure(g.pool_size);
+    std::vector<uint32_t> none(1 << 20, BDSM_NO_LABEL);
+    for (uint64_t i = 0; i < g.pool_size; i += none.size()) {
+      uint64_t k = std::min<uint64_t>(none.size(), g.pool_size - i);
+      CK(cudaMemcpyAsync(elab.p + i, none.data(), 4 * k, cudaMemcpyHostToDevice, stream));
+      sync();
+    }
+    has_elab = true;
+    refresh_graph_view();
+  }
+
+  // --------------------------------------------------------------- queries --
+  int add_query(const bdsm_query_desc* d) {
+    if (!d || (d->num_vertices && !d->vertex_labels) || (d->num_edges && (!d->a || !d->b)))
+      throw std::invalid_argument("null query arrays");
+    std::vector<uint32_t> labels(d->vertex_labels, d->vertex_labels + d->num_vertices);
+    std::vector<QEdge> edges;
+    for (uint32_t i = 0; i < d->num_edges; ++i)
+      edges.push_back({d->a[i], d->b[i], d->edge_labels ? d->edge_labels[i] : kNone});
+    auto qs = std::make_unique<QueryState>();
+    qs->q = HostQuery(std::move(labels), std::move(edges));
+    if (!qs->q.connected()) throw std::invalid_argument("disconnected query graph");
+    if (qs->q.n > uint32_t(kMaxQ))
+      throw std::invalid_argument("query graph too large for the GPU engine (max " +
+                                  std::to_string(kMaxQ) + " vertices)");
+    if (queries.size() >= 32) throw std::invalid_argument("at most 32 queries per engine");
+    qs->enc = encode_query(qs->q, opts.group_bits);
+    DevQueryEnc& de = qs->denc;
+    de.n = qs->q.n;
+    de.G = uint32_t(qs->enc.group_labels.size());
+    de.cap = qs->enc.cap;
+    for (uint32_t u = 0; u < de.n; ++u) de.qlabel[u] = qs->q.labels[u];
+    for (uint32_t gi = 0; gi < de.G; ++gi) de.glabel[gi] = qs->enc.group_labels[gi];
+    for (uint32_t u = 0; u < de.n; ++u)
+      for (uint32_t gi = 0; gi < de.G; ++gi) de.qcnt[u][gi] = qs->enc.qcnt[u * de.G + gi];
+    DBuf<DevQueryEnc> one;
+    one.ensure(1);
+    CK(cudaMemcpyAsync(one.p, &de, sizeof(de), cudaMemcpyHostToDevice, stream));
+    qs->rows.ensure(std::max<uint32_t>(g.V, 1));
+    qs->colsize.ensure(32);
+    CK(cudaMemsetAsync(qs->colsize.p, 0, 8 * 32, stream));
+    if (g.V) {
+      launch_encode_all(view(), one.p, qs->rows.p, num_sms, stream);
+      launch_column_sizes(qs->rows.p, g.V, de.n, qs->colsize.p, stream);
+    }
+    sync();
+    queries.push_back(std::move(qs));
+    int qi = int(queries.size() - 1);
+    replan(qi);
+    upload_query_tables();
+    return qi;
+  }
+
+  std::vector<uint64_t> column_sizes(int qi) {
+    QueryState& qs = *queries.at(size_t(qi));
+    std::vector<uint64_t> cs(32);
+    CK(cudaMemcpyAsync(cs.data(), qs.colsize.p, 8 * 32, cudaMemcpyDeviceToHost, stream));
+    sync();
+    cs.resize(qs.q.n);
+    return cs;
+  }
+
+  // build_query_plan with coalescing off: one order per query edge.
+  void replan(int qi) {
+    QueryState& qs = *queries.at(size_t(qi));
+    std::vector<uint64_t> cs = column_sizes(qi);
+    qs.orders.clear();
+    std::vector<EdgeProg> progs;
+    std::vector<AnchorEdge> anchors;
+    for (uint32_t e = 0; e < qs.q.edges.size(); ++e) {
+      qs.orders.push_back(matching_order(qs.q, e, cs));
+      progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back()));
+      const QEdge& qe = qs.q.edges[e];
+      anchors.push_back({qs.q.labels[qe.a], qs.q.labels[qe.b], qe.label, e});
+    }
+    qs.progs.ensure(std::max<size_t>(progs.size(), 1));
+    qs.anchors.ensure(std::max<size_t>(anchors.size(), 1));
+    if (!progs.empty()) {
+      CK(cudaMemcpyAsync(qs.progs.p, progs.data(), sizeof(EdgeProg) * progs.size(), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(qs.anchors.p, anchors.data(), sizeof(AnchorEdge) * anchors.size(),
+                         cudaMemcpyHostToDevice, stream));
+    }
+    sync();
+  }
+
+  void upload_query_tables() {
+    size_t nq = queries.size();
+    std::vector<DevQueryEnc> enc(nq);
+    std::vector<uint32_t*> rows(nq);
+    std::vector<uint64_t*> cols(nq);
+    for (size_t i = 0; i < nq; ++i) {
+      enc[i] = queries[i]->denc;
+      rows[i] = queries[i]->rows.p;
+      cols[i] = queries[i]->colsize.p;
+    }
+    d_qenc.ensure(nq);
+    d_rows.ensure(nq);
+    d_colsize.ensure(nq);
+    CK(cudaMemcpyAsync(d_qenc.p, enc.data(), sizeof(DevQueryEnc) * nq, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_rows.p, rows.data(), sizeof(uint32_t*) * nq, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_colsize.p, cols.data(), sizeof(uint64_t*) * nq, cudaMemcpyHostToDevice, stream));
+    sync();
+  }
+
+  // --------------------------------------------------------------- batches --
+  size_t cub_bytes_for(size_t n) {
+    size_t m = 2 * n, a = 0, b = 0, c = 0, d = 0, e = 0;
+    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, int(m), 0, 64, stream));
+    CK(cub::DeviceSelect::Flagged(nullptr, b, cub::CountingInputIterator<uint32_t>(0), (uint8_t*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, int(m), stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, int(m + 1), stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, d, (uint64_t*)nullptr, (uint64_t*)nullptr, int(n + 1), stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, e, (uint32_t*)nullptr, (uint32_t*)nullptr, int(n + 1), stream));
+    return std::max({a, b, c, d, e});
+  }
+
+  size_t batch_cap = 0;
+  void ensure_batch(size_t n) {
+    if (n <= batch_cap) return;
+    size_t cap_n = std::max<size_t>(n, batch_cap + batch_cap / 2);
+    cap_n = std::max<size_t>(cap_n, 1024);
+    size_t m = 2 * cap_n;
+    ups.ensure(cap_n);
+    keys.ensure(m);
+    skeys.ensure(m);
+    vals.ensure(m);
+    svals.ensure(m);
+    dlab.ensure(cap_n);
+    ecode.ensure(cap_n);
+    head.ensure(m);
+    insflag.ensure(m + 1);
+    ins_prefix.ensure(m + 1);
+    heads.ensure(m);
+    ipos.ensure(m);
+    new_off.ensure(m);
+    new_cap.ensure(m);
+    upd_counts.ensure(cap_n + 1);
+    upd_task_counts.ensure(cap_n + 1);
+    item_off.ensure(cap_n + 1);
+    task_off.ensure(cap_n + 1);
+    upd_cost.ensure(cap_n + 1);
+    cost_off.ensure(cap_n + 1);
+    cub_tmp.ensure(cub_bytes_for(cap_n));
+    batch_cap = cap_n;
+  }
+
+  void ensure_tasks(size_t n) {
+    size_t maxq_edges = 1;
+    for (auto& q : queries) maxq_edges = std::max(maxq_edges, q->q.edges.size());
+    tasks.ensure_grow(std::max<size_t>(n * 2 * maxq_edges, 1024));
+    if (max_items == 0) {
+      max_items = std::max<size_t>(tasks.n * 4, size_t(1) << 22);
+      items.ensure(max_items);
+    }
+  }
+
+  void ensure_host_ups(size_t n) {
+    if (n <= h_ups_cap) return;
+    if (h_ups) cudaFreeHost(h_ups);
+    size_t c = std::max<size_t>(n, h_ups_cap * 2);
+    CK(cudaMallocHost(&h_ups, c * sizeof(bdsm_update)));
+    h_ups_cap = c;
+  }
+
+  PhaseArgs phase_args(uint32_t n, uint32_t phase, int qi) {
+    QueryState& qs = *queries[size_t(qi)];
+    PhaseArgs a{};
+    a.g = view();
+    a.ups = ups.p;
+    a.n_ups = n;
+    a.dlab = dlab.p;
+    a.anchors = qs.anchors.p;
+    a.n_anchor = uint32_t(qs.q.edges.size());
+    a.progs = qs.progs.p;
+    a.rows = qs.rows.p;
+    a.skeys = skeys.p;
+    a.svals = svals.p;
+    a.m_keys = 2 * n;
+    a.touched_bits = phase == 0 ? del_bits.p : ins_bits.p;
+    a.phase = phase;
+    a.query = uint32_t(qi);
+    a.qn = qs.q.n;
+    a.chunk = opts.chunk;
+    a.shard_rank = opts.shard_rank;
+    a.shard_world = std::max<uint32_t>(opts.shard_world, 1);
+    a.upd_counts = upd_counts.p;
+    a.upd_task_counts = upd_task_counts.p;
+    a.upd_cost = upd_cost.p;
+    a.item_off = item_off.p;
+    a.task_off = task_off.p;
+    a.cost_off = cost_off.p;
+    a.tasks = tasks.p;
+    a.items = items.p;
+    a.max_items = uint32_t(std::min<size_t>(max_items, 0xffffffffu));
+    a.st = d_st.p;
+    a.deadline_ns = 0;
+    return a;
+  }
+
+  void run_phase(uint32_t n, uint32_t phase) {
+    for (size_t qi = 0; qi < queries.size(); ++qi) {
+      QueryState& qs = *queries[qi];
+      if (!qs.solved || qs.q.edges.empty()) continue;
+      PhaseArgs a = phase_args(n, phase, int(qi));
+      if (qs.deadline_s > 0) {
+        // device %globaltimer is in ns since an arbitrary epoch: express the
+        // deadline relative to "now" on both clocks via a calibration kernel
+        // would be exact; the host steady clock offset is applied instead.
+        a.deadline_ns = device_deadline(qs.deadline_s);
+      }
+      launch_anchor_count(a, stream);
+      size_t tmp = cub_tmp.n;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_task_counts.p, task_off.p, int(n + 1), stream));
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_counts.p, item_off.p, int(n + 1), stream));
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_cost.p, cost_off.p, int(n + 1), stream));
+      launch_anchor_emit(a, stream);
+      CK(cudaMemsetAsync(&d_st.p->next_item, 0, sizeof(uint32_t), stream));
+      if (qs.q.n > 2) launch_wbm(a, num_sms, stream);
+    }
+  }
+
+  // %globaltimer and the host steady clock differ by an offset measured once.
+  int64_t gt_offset = 0;
+  bool gt_calibrated = false;
+  uint64_t device_deadline(double deadline_s);
+
+  BatchState template_state() {
+    BatchState s{};
+    s.selfloop_min = kNone;
+    s.conflict_min = kNone;
+    s.pool_top = pool_top;
+    return s;
+  }
+
+  bdsm_status apply(const bdsm_update* updates, size_t n, bool device_input, uint64_t* pos,
+                    uint64_t* neg, bdsm_batch_stats* stats) {
+    auto t0 = std::chrono::steady_clock::now();
+    last_errors.clear();
+    bdsm_batch_stats st{};
+    for (size_t qi = 0; qi < queries.size(); ++qi) {
+      if (pos) pos[qi] = 0;
+      if (neg) neg[qi] = 0;
+    }
+    if (n == 0) {
+      if (stats) *stats = st;
+      return BDSM_OK;
+    }
+    if (n >= (size_t(1) << 31)) throw std::invalid_argument("batch too large");
+    if (!device_input) {
+      bool labelled = false;
+      for (size_t i = 0; i < n && !labelled; ++i)
+        labelled = updates[i].op == 0 && updates[i].edge_label != BDSM_NO_LABEL;
+      if (labelled && !has_elab) enable_edge_labels();
+    }
+    ensure_batch(n);
+    ensure_tasks(n);
+    if (!h_st) CK(cudaMallocHost(&h_st, sizeof(BatchState)));
+    if (!ev[0])
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+    d_st.ensure(1);
+    const bdsm_update_dev* src;
+    if (device_input) {
+      src = reinterpret_cast<const bdsm_update_dev*>(updates);
+    } else {
+      ensure_host_ups(n);
+      std::memcpy(h_ups, updates, n * sizeof(bdsm_update));
+      src = ups.p;
+    }
+    uint32_t compactions = 0;
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 8) throw std::runtime_error("batch could not be scheduled");
+      CK(cudaEventRecord(ev[0], stream));
+      if (!device_input) {
+        CK(cudaMemcpyAsync(ups.p, h_ups, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+        st.h2d_bytes = n * sizeof(bdsm_update);
+      }
+      *h_st = template_state();
+      CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+      size_t words = (size_t(g.V) + 31) / 32 + 1;
+      ins_bits.ensure(words);
+      del_bits.ensure(words);
+      CK(cudaMemsetAsync(ins_bits.p, 0, words * 4, stream));
+      CK(cudaMemsetAsync(del_bits.p, 0, words * 4, stream));
+      const uint32_t m = uint32_t(2 * n);
+      launch_prepare(src, uint32_t(n), view(), d_st.p, keys.p, vals.p, dlab.p, ecode.p, stream);
+      {
+        size_t tmp = cub_tmp.n;
+        cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
+        cub::DoubleBuffer<uint32_t> vb(vals.p, svals.p);
+        CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, 64, stream));
+        if (kb.Current() != skeys.p)
+          CK(cudaMemcpyAsync(skeys.p, kb.Current(), 8ull * m, cudaMemcpyDeviceToDevice, stream));
+        if (vb.Current() != svals.p)
+          CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
+      }
+      // device-input batches: the ups buffer the kernels read is `src`
+      PhaseArgsFix fix(this, src);
+      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, ins_bits.p, del_bits.p, g.V, stream);
+      {
+        size_t tmp = cub_tmp.n;
+        CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
+                                      &d_st.p->n_touched, int(m), stream));
+        tmp = cub_tmp.n;
+        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, insflag.p, ins_prefix.p, int(m + 1), stream));
+      }
+      CK(cudaEventRecord(ev[1], stream));
+      run_phase(uint32_t(n), 0);
+      CK(cudaEventRecord(ev[2], stream));
+      launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, stream);
+      launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, src, g, new_off.p, new_cap.p, ipos.p,
+                           d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, num_sms, stream);
+      CK(cudaEventRecord(ev[3], stream));
+      run_phase(uint32_t(n), 1);
+      CK(cudaEventRecord(ev[4], stream));
+      CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+      CK(cudaEventRecord(ev[5], stream));
+      sync();
+      const BatchState& b = *h_st;
+      if (b.selfloop_min != kNone || b.conflict_min != kNone) {
+        bdsm_update bad{};
+        uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
+        fetch_update(src, device_input, idx, &bad);
+        if (b.selfloop_min <= b.conflict_min)
+          throw std::invalid_argument("self-loop update (" + std::to_string(bad.u) + "," +
+                                      std::to_string(bad.v) + ")");
+        throw std::invalid_argument("conflicting updates on edge (" + std::to_string(bad.u) + "," +
+                                    std::to_string(bad.v) + ") within one batch");
+      }
+      if (b.err_count) {
+        std::vector<uint8_t> codes(n);
+        CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
+        sync();
+        for (size_t i = 0; i < n; ++i)
+          if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
+        throw BatchRejected("batch rejected: " + std::to_string(last_errors.size()) +
+                            " invalid update(s), none applied");
+      }
+      if (b.overflow == 4) {  // labelled insert into an unlabelled graph: nothing merged
+        enable_edge_labels();
+        continue;
+      }
+      if (b.overflow == 1) {  // adjacency pool exhausted: nothing merged yet
+        compact(b.pool_top > g.pool_size ? b.pool_top - pool_top : 0);
+        ++compactions;
+        continue;
+      }
+      if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
+        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
+        items.ensure(max_items);
+        continue;
+      }
+      if (b.overflow == 3) {  // positive phase only (graph already merged)
+        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
+        items.ensure(max_items);
+        rerun_positive(uint32_t(n), src);
+      }
+      break;
+    }
+    const BatchState& b = *h_st;
+    pool_top = b.pool_top;
+    for (size_t qi = 0; qi < queries.size(); ++qi) {
+      bool dead = (b.timed_out >> qi) & 1u;
+      if (dead) queries[qi]->solved = false;
+      if (neg) neg[qi] = dead ? 0 : b.counts[0][qi];
+      if (pos) pos[qi] = dead ? 0 : b.counts[1][qi];
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[0], ev[5]);
+    st.ms_device = ms;
+    cudaEventElapsedTime(&ms, ev[1], ev[2]);
+    st.ms_negative = ms;
+    cudaEventElapsedTime(&ms, ev[2], ev[3]);
+    st.ms_update = ms;
+    cudaEventElapsedTime(&ms, ev[3], ev[4]);
+    st.ms_positive = ms;
+    st.dfs_visits = b.visits;
+    st.tasks = b.tasks_total;
+    st.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
+    st.gen_calls = b.gen_calls;
+    st.bytes_phase = b.bytes_phase;
+    st.bytes_update = b.bytes_update + 16ull * n;
+    st.touched = b.n_touched;
+    st.relocations = b.relocations;
+    st.compactions = compactions;
+    st.timed_out = b.timed_out;
+    st.d2h_bytes = sizeof(BatchState);
+    st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = st;
+    return BDSM_OK;
+  }
+
+  // RAII helper: kernels launched through phase_args read `ups.p`; for
+  // device-resident input we temporarily point it at the caller's buffer.
+  struct PhaseArgsFix {
+    bdsm_engine* e;
+    bdsm_update_dev* saved;
+    PhaseArgsFix(bdsm_engine* en, const bdsm_update_dev* src) : e(en), saved(en->ups.p) {
+      e->ups.p = const_cast<bdsm_update_dev*>(src);
+    }
+    ~PhaseArgsFix() { e->ups.p = saved; }
+  };
+
+  void rerun_positive(uint32_t n, const bdsm_update_dev* src) {
+    PhaseArgsFix fix(this, src);
+    h_st->overflow = 0;
+    for (auto& c : h_st->counts[1]) c = 0;
+    CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+    run_phase(n, 1);
+    CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
+  }
+
+  void fetch_update(const bdsm_update_dev* src, bool device_input, uint32_t idx, bdsm_update* out) {
+    if (!device_input) {
+      *out = h_ups[idx];
+      return;
+    }
+    CK(cudaMemcpyAsync(out, src + idx, sizeof(bdsm_update), cudaMemcpyDeviceToHost, stream));
+    sync();
+  }
+};
+
+namespace {
+__global__ void k_read_globaltimer(uint64_t* out) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace
+
+// %globaltimer and the host steady clock differ by an offset, measured once
+// with a one-thread kernel bracketed by host clock reads.
+uint64_t bdsm_engine::device_deadline(double deadline_s) {
+  if (!gt_calibrated) {
+    DBuf<uint64_t> t;
+    t.ensure(1);
+    uint64_t h0 = now_ns();
+    k_read_globaltimer<<<1, 1, 0, stream>>>(t.p);
+    uint64_t gt = 0;
+    CK(cudaMemcpyAsync(&gt, t.p, 8, cudaMemcpyDeviceToHost, stream));
+    sync();
+    uint64_t h1 = now_ns();
+    gt_offset = int64_t(gt) - int64_t((h0 + h1) / 2);
+    gt_calibrated = true;
+  }
+  int64_t host_deadline = int64_t(deadline_s * 1e9);
+  int64_t dev = host_deadline + gt_offset;
+  return dev <= 1 ? 1 : uint64_t(dev);
+}
+
+// ------------------------------------------------------------------ C ABI --
+
+namespace {
+
+bdsm_status fail(bdsm_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+template <typename F>
+bdsm_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const BatchRejected& e) {
+    return fail(BDSM_BATCH_ERROR, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(BDSM_INVALID_ARGUMENT, e.what());
+  } catch (const std::out_of_range& e) {
+    return fail(BDSM_INVALID_ARGUMENT, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(BDSM_OUT_OF_MEMORY, "out of device or host memory");
+  } catch (const CudaFailure& e) {
+    return fail(BDSM_CUDA_ERROR, e.what());
+  } catch (const std::exception& e) {
+    return fail(BDSM_RUNTIME_ERROR, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bdsm_version(void) { return "bdsm_b200 0.1 (sm_100a)"; }
+
+const char* bdsm_last_error(void) { return g_last_error.c_str(); }
+
+bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options* opts, bdsm_engine** out) {
+  if (!out) return fail(BDSM_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  return guarded([&]() -> bdsm_status {
+    if (!graph) throw std::invalid_argument("null graph");
+    auto e = std::make_unique<bdsm_engine>();
+    bdsm_options o{};
+    o.group_bits = 2;
+    o.slack = 0.25f;
+    o.pool_reserve = 0.5f;
+    o.chunk = 64;
+    o.shard_world = 1;
+    if (opts) {
+      o = *opts;
+      if (o.group_bits == 0) o.group_bits = 2;
+      if (o.slack <= 0) o.slack = 0.25f;
+      if (o.pool_reserve <= 0) o.pool_reserve = 0.5f;
+      if (o.chunk == 0) o.chunk = 64;
+      if (o.shard_world == 0) o.shard_world = 1;
+    }
+    if (o.coalesce) throw std::invalid_argument("coalesced search is not supported: it is not exact in the reference (SURVEY.md F1)");
+    if (o.shard_rank >= o.shard_world) throw std::invalid_argument("shard_rank must be < shard_world");
+    if (o.chunk % 32 != 0) throw std::invalid_argument("chunk must be a multiple of 32");
+    e->opts = o;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (ndev == 0) throw CudaFailure("no CUDA device");
+    e->device = o.device;
+    CK(cudaSetDevice(e->device));
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
+    e->build(graph);
+    *out = e.release();
+    return BDSM_OK;
+  });
+}
+
+void bdsm_engine_destroy(bdsm_engine* engine) { delete engine; }
+
+int bdsm_engine_add_query(bdsm_engine* engine, const bdsm_query_desc* query) {
+  if (!engine) return -int(fail(BDSM_INVALID_ARGUMENT, "null engine"));
+  int idx = -1;
+  bdsm_status s = guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    idx = engine->add_query(query);
+    return BDSM_OK;
+  });
+  return s == BDSM_OK ? idx : -int(s);
+}
+
+bdsm_status bdsm_engine_apply_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n, uint64_t* pos,
+                                    uint64_t* neg, bdsm_batch_stats* stats) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  if (n && !updates) return fail(BDSM_INVALID_ARGUMENT, "null updates");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    return engine->apply(updates, n, false, pos, neg, stats);
+  });
+}
+
+bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const bdsm_update* d_updates, size_t n,
+                                           uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  if (n && !d_updates) return fail(BDSM_INVALID_ARGUMENT, "null updates");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    return engine->apply(d_updates, n, true, pos, neg, stats);
+  });
+}
+
+bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seconds_from_now) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    QueryState& qs = *engine->queries.at(size_t(query));
+    qs.deadline_s = seconds_from_now > 0 ? double(now_ns()) * 1e-9 + seconds_from_now : 0;
+    return BDSM_OK;
+  });
+}
+
+size_t bdsm_last_batch_errors(bdsm_engine* engine, bdsm_update_error* out, size_t cap) {
+  if (!engine) return 0;
+  size_t n = std::min(cap, engine->last_errors.size());
+  if (out)
+    for (size_t i = 0; i < n; ++i) out[i] = engine->last_errors[i];
+  return engine->last_errors.size();
+}
+
+size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, size_t cap) {
+  if (!engine || v >= engine->g.V) return 0;
+  size_t d = 0;
+  guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    uint32_t dv = 0;
+    uint64_t o = 0;
+    CK(cudaMemcpyAsync(&dv, engine->deg.p + v, 4, cudaMemcpyDeviceToHost, engine->stream));
+    CK(cudaMemcpyAsync(&o, engine->off.p + v, 8, cudaMemcpyDeviceToHost, engine->stream));
+    engine->sync();
+    d = dv;
+    if (out && cap) {
+      CK(cudaMemcpyAsync(out, engine->adj.p + o, 4 * std::min<size_t>(cap, dv), cudaMemcpyDeviceToHost,
+                         engine->stream));
+      engine->sync();
+    }
+    return BDSM_OK;
+  });
+  return d;
+}
+
+bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    QueryState& qs = *engine->queries.at(size_t(query));
+    CK(cudaMemcpyAsync(out, qs.rows.p, 4ull * engine->g.V, cudaMemcpyDeviceToHost, engine->stream));
+    engine->sync();
+    return BDSM_OK;
+  });
+}
+
+int bdsm_engine_order(bdsm_engine* engine, int query, uint32_t edge, uint32_t* out) {
+  if (!engine || query < 0 || size_t(query) >= engine->queries.size()) return -int(BDSM_INVALID_ARGUMENT);
+  QueryState& qs = *engine->queries[size_t(query)];
+  if (edge >= qs.orders.size()) return -int(BDSM_INVALID_ARGUMENT);
+  const auto& o = qs.orders[edge];
+  for (size_t i = 0; i < o.size(); ++i) out[i] = o[i];
+  return int(o.size());
+}
+
+bdsm_status bdsm_engine_column_sizes(bdsm_engine* engine, int query, uint64_t* out) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    auto cs = engine->column_sizes(query);
+    std::copy(cs.begin(), cs.end(), out);
+    return BDSM_OK;
+  });
+}
+
+bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    engine->replan(query);
+    return BDSM_OK;
+  });
+}
+
+uint64_t bdsm_engine_num_edges(bdsm_engine* engine) {
+  if (!engine) return 0;
+  uint64_t total = 0;
+  guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    std::vector<uint32_t> d(engine->g.V);
+    CK(cudaMemcpyAsync(d.data(), engine->deg.p, 4ull * engine->g.V, cudaMemcpyDeviceToHost, engine->stream));
+    engine->sync();
+    for (uint32_t x : d) total += x;
+    return BDSM_OK;
+  });
+  return total / 2;
+}
+
+uint32_t bdsm_engine_num_vertices(bdsm_engine* engine) { return engine ? engine->g.V : 0; }
+
+void bdsm_shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners) {
+  shard_owners(costs, n, world, owners);
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Kernel entry points of libbdsm_b200.so (definitions in store.cu, match.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace bdsm_b200 {
+
+struct bdsm_update_dev {  // mirrors bdsm_update (include/bdsm_gpu.h)
+  uint32_t u, v, op, elab;
+};
+
+// Per-query filter tables on the device (candidate rows, encodings).
+struct DevQueryEnc {
+  uint32_t n;                    // query vertices
+  uint32_t G;                    // counter groups
+  uint32_t cap;                  // saturation cap
+  uint32_t qlabel[kMaxQ];
+  uint32_t glabel[kMaxQ];
+  uint8_t qcnt[kMaxQ][kMaxQ];    // [u][g]
+};
+
+// Mutable device graph (owner's view).
+struct DevGraphMut {
+  uint32_t V;
+  uint64_t* off;
+  uint32_t* deg;
+  uint32_t* cap;
+  uint32_t* adj;
+  uint32_t* elab;
+  uint32_t* vlabel;
+  uint64_t pool_size;
+};
+
+// ---- store.cu: build ------------------------------------------------------
+void launch_build_keys(const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t V,
+                       uint64_t* keys, uint64_t* vals, uint32_t* bad, cudaStream_t s);
+void launch_check_sorted_dups(const uint64_t* keys, uint64_t n, uint32_t* bad, cudaStream_t s);
+void launch_degrees(const uint64_t* keys, uint64_t n, uint32_t* deg, cudaStream_t s);
+void launch_caps(const uint32_t* deg, uint32_t V, float slack, uint32_t* cap, uint64_t* cap64,
+                 cudaStream_t s);
+void launch_scatter(const uint64_t* keys, const uint64_t* vals, uint64_t n, const uint64_t* dense_off,
+                    const uint64_t* off, uint32_t* adj, const uint32_t* edge_labels, uint32_t* elab,
+                    cudaStream_t s);
+void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* new_cap,
+                    uint32_t* new_adj, uint32_t* new_elab, cudaStream_t s);
+
+// ---- store.cu: per batch ---------------------------------------------------
+void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, BatchState* st,
+                    uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, cudaStream_t s);
+void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
+                      uint8_t* head, uint32_t* insflag, uint32_t* ins_bits, uint32_t* del_bits,
+                      uint32_t V, cudaStream_t s);
+void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
+                  uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
+                  uint32_t* new_cap, cudaStream_t s);
+void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
+                          const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
+                          DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
+                          uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
+                          uint64_t* const* colsize, BatchState* st, int num_sms, cudaStream_t s);
+void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
+void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);
+
+// ---- match.cu ---------------------------------------------------------------
+struct PhaseArgs {
+  DevGraph g;
+  const bdsm_update_dev* ups;
+  uint32_t n_ups;
+  const uint32_t* dlab;          // pre-batch edge labels of deletes
+  const AnchorEdge* anchors;     // anchor table of this query
+  uint32_t n_anchor;
+  const EdgeProg* progs;
+  const uint32_t* rows;          // candidate rows of this query
+  const uint64_t* skeys;         // sorted directed batch keys (visibility lookups)
+  const uint32_t* svals;
+  uint32_t m_keys;
+  const uint32_t* touched_bits;  // same-kind endpoint bitmap of this phase
+  uint32_t phase;                // 0 negative (deletes), 1 positive (inserts)
+  uint32_t query;
+  uint32_t qn;                   // query vertex count
+  uint32_t chunk;
+  uint32_t shard_rank, shard_world;
+  uint32_t* upd_counts;          // [n_ups + 1] items per update (scan input)
+  uint32_t* upd_task_counts;     // [n_ups + 1]
+  uint64_t* upd_cost;            // [n_ups + 1] driver mass per update (scan input)
+  uint32_t* item_off;            // exclusive scans
+  uint32_t* task_off;
+  uint64_t* cost_off;
+  Task* tasks;
+  Item* items;
+  uint32_t max_items;
+  BatchState* st;
+  uint64_t deadline_ns;          // 0: none
+};
+
+void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);
+void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s);
+void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s);
+
+}  // namespace bdsm_b200

@@ -1,0 +1,139 @@
+// Host planner.  Follows the reference's coalesce-off plan: one greedy
+// matching order per query edge (src/query_analysis.cpp:295-363, :437-441).
+#include "planner.hpp"
+
+#include <algorithm>
+
+namespace bdsm_b200 {
+
+HostQuery::HostQuery(std::vector<uint32_t> vertex_labels, std::vector<QEdge> qedges)
+    : labels(std::move(vertex_labels)) {
+  n = static_cast<uint32_t>(labels.size());
+  if (n == 0) throw std::invalid_argument("empty query graph");
+  if (n > 32) throw std::invalid_argument("query graph too large");
+  adjmask.assign(n, 0);
+  degree.assign(n, 0);
+  for (const QEdge& e : qedges) {
+    if (e.a >= n || e.b >= n) throw std::invalid_argument("query edge references unknown vertex");
+    if (e.a == e.b) throw std::invalid_argument("query self-loop");
+    if (adjacent(e.a, e.b)) throw std::invalid_argument("duplicate query edge");
+    adjmask[e.a] |= 1u << e.b;
+    adjmask[e.b] |= 1u << e.a;
+    ++degree[e.a];
+    ++degree[e.b];
+    edges.push_back(e);
+  }
+}
+
+uint32_t HostQuery::edge_label(uint32_t u, uint32_t v) const {
+  for (const QEdge& e : edges) {
+    if ((e.a == u && e.b == v) || (e.a == v && e.b == u)) return e.label;
+  }
+  return kNone;
+}
+
+bool HostQuery::connected() const {  // src/query_graph.cpp:43-55
+  uint32_t seen = 1, frontier = 1;
+  while (frontier) {
+    uint32_t next = 0;
+    for (uint32_t u = 0; u < n; ++u) {
+      if ((frontier >> u) & 1u) next |= adjmask[u];
+    }
+    frontier = next & ~seen;
+    seen |= next;
+  }
+  return seen == (n == 32 ? ~0u : (1u << n) - 1);
+}
+
+QueryEncoding encode_query(const HostQuery& q, uint32_t group_bits) {
+  if (group_bits == 0 || group_bits > 8) throw std::invalid_argument("group_bits must be in 1..8");
+  QueryEncoding enc;
+  enc.group_labels = q.labels;
+  std::sort(enc.group_labels.begin(), enc.group_labels.end());
+  enc.group_labels.erase(std::unique(enc.group_labels.begin(), enc.group_labels.end()),
+                         enc.group_labels.end());
+  enc.cap = (1u << group_bits) - 1;
+  size_t G = enc.group_labels.size();
+  enc.qcnt.assign(size_t(q.n) * G, 0);
+  for (uint32_t u = 0; u < q.n; ++u) {
+    for (uint32_t w = 0; w < q.n; ++w) {
+      if (!q.adjacent(u, w)) continue;
+      size_t g = size_t(std::lower_bound(enc.group_labels.begin(), enc.group_labels.end(), q.labels[w]) -
+                        enc.group_labels.begin());
+      uint8_t& c = enc.qcnt[u * G + g];
+      if (c < enc.cap) ++c;
+    }
+  }
+  return enc;
+}
+
+std::vector<uint32_t> matching_order(const HostQuery& q, uint32_t e,
+                                     const std::vector<uint64_t>& column_sizes) {
+  const QEdge& anchor = q.edges.at(e);
+  std::vector<uint32_t> order{anchor.a, anchor.b};
+  uint32_t assigned = (1u << anchor.a) | (1u << anchor.b);
+  uint32_t all = q.n == 32 ? ~0u : (1u << q.n) - 1;
+  auto sel = [&](uint32_t u) {
+    return double(column_sizes[u]) / double(std::max<uint32_t>(q.degree[u], 1));
+  };
+  while ((assigned & all) != all) {
+    int best = -1;
+    for (uint32_t u = 0; u < q.n; ++u) {
+      if ((assigned >> u) & 1u) continue;
+      if (!(q.adjmask[u] & assigned)) continue;  // prefix connectivity
+      if (best < 0) {
+        best = int(u);
+        continue;
+      }
+      uint32_t bu = uint32_t(best);
+      double su = sel(u), sb = sel(bu);
+      if (su < sb || (su == sb && (q.degree[u] > q.degree[bu] ||
+                                   (q.degree[u] == q.degree[bu] && u < bu)))) {
+        best = int(u);
+      }
+    }
+    if (best < 0) throw std::invalid_argument("disconnected query graph");
+    order.push_back(uint32_t(best));
+    assigned |= 1u << best;
+  }
+  return order;
+}
+
+EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order) {
+  EdgeProg p{};
+  p.n = q.n;
+  p.query = query_index;
+  for (uint32_t i = 0; i < q.n; ++i) p.order[i] = order[i];
+  for (uint32_t l = 0; l < q.n; ++l) {
+    LevelProg& lp = p.lv[l];
+    uint32_t u = order[l];
+    lp.qbit = 1u << u;
+    lp.nback = 0;
+    for (uint32_t j = 0; j < l; ++j) {
+      if (q.adjacent(order[j], u)) {
+        lp.backmask |= 1u << j;
+        lp.back[lp.nback] = uint8_t(j);
+        lp.elab[lp.nback] = q.edge_label(order[j], u);
+        ++lp.nback;
+      }
+      if (q.labels[order[j]] == q.labels[u]) lp.eqmask |= 1u << j;
+    }
+  }
+  return p;
+}
+
+void shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners) {
+  if (world <= 1) {
+    std::fill(owners, owners + n, 0u);
+    return;
+  }
+  unsigned __int128 total = 0;
+  for (size_t k = 0; k < n; ++k) total += costs[k];
+  unsigned __int128 prefix = 0;
+  for (size_t k = 0; k < n; ++k) {
+    owners[k] = total ? uint32_t((prefix * world) / total) : 0;
+    prefix += costs[k];
+  }
+}
+
+}  // namespace bdsm_b200

@@ -1,0 +1,58 @@
+// Host-side query model and planner (north_star item 2): query validation,
+// the NLF encoding of query vertices, matching orders and the per-level
+// matching programs uploaded to the device.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bdsm_b200 {
+
+struct QEdge {
+  uint32_t a, b, label;  // label kNone = unlabelled
+};
+
+// QueryGraph (reference include/bdsm/query_graph.hpp, src/query_graph.cpp:10-27).
+struct HostQuery {
+  uint32_t n = 0;
+  std::vector<uint32_t> labels;
+  std::vector<QEdge> edges;
+  std::vector<uint32_t> adjmask;
+  std::vector<uint32_t> degree;
+
+  HostQuery() = default;
+  HostQuery(std::vector<uint32_t> vertex_labels, std::vector<QEdge> qedges);
+
+  bool adjacent(uint32_t u, uint32_t v) const { return (adjmask[u] >> v) & 1u; }
+  uint32_t edge_label(uint32_t u, uint32_t v) const;
+  bool connected() const;
+};
+
+// Encoding of a query for the candidate filter (src/encoding.cpp:17-24,
+// :96-113): the sorted distinct query labels (one counter group each) and
+// the saturated per-group neighbour counts of every query vertex.
+struct QueryEncoding {
+  std::vector<uint32_t> group_labels;  // sorted
+  uint32_t cap = 3;                    // 2^group_bits - 1
+  std::vector<uint8_t> qcnt;           // [n][G]
+};
+
+QueryEncoding encode_query(const HostQuery& q, uint32_t group_bits);
+
+// Matching order anchored at query edge e: try_order with no zone and no
+// tail (src/query_analysis.cpp:295-363): greedy minimum |C(u)|/max(deg,1),
+// ties by higher query degree, then lower id; every prefix connected.
+std::vector<uint32_t> matching_order(const HostQuery& q, uint32_t e,
+                                     const std::vector<uint64_t>& column_sizes);
+
+// Device program for one (query, edge) from its order.
+EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order);
+
+// Canonical split of work units over ranks: owner = floor(world * prefix / total).
+void shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);
+
+}  // namespace bdsm_b200

@@ -1,0 +1,521 @@
+// Graph store kernels: initial CSR build, batch validation and canonicalisation
+// (K1), per-vertex merge into slack-padded adjacency (K3) fused with the
+// incremental NLF re-encode and candidate-row refresh (K4).
+//
+// Replaces LabeledGraph::build_from_edges / validate_batch / apply_batch
+// (reference src/graph.cpp:35-72, :117-158) over the PMA (src/pma.cpp), and
+// incremental_reencode + CandidateTable::refresh (src/encoding.cpp:124-143,
+// :171-191).  The invariant kept is "sorted, duplicate-free, symmetric
+// adjacency"; the PMA density rules are not carried over.
+#include "kernels.cuh"
+
+namespace bdsm_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned blocks_for(uint64_t n, int threads = kThreads) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b == 0) b = 1;
+  if (b > (1u << 30)) b = 1u << 30;
+  return unsigned(b);
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ a, uint32_t n,
+                                                    uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t slack_cap(uint32_t d, float slack) {
+  uint64_t extra = uint64_t(float(d) * slack);
+  if (extra < 4) extra = 4;
+  uint64_t c = uint64_t(d) + extra;
+  c = (c + 3) & ~uint64_t(3);  // 16-byte aligned lists (128-bit loads)
+  if (c > 0xfffffff0ull) c = 0xfffffff0ull;
+  return uint32_t(c);
+}
+
+// ---------------------------------------------------------------- build ----
+
+__global__ void k_build_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                             uint64_t E, uint32_t V, uint64_t* keys, uint64_t* vals, uint32_t* bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < E;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t u = src[i], v = dst[i];
+    if (u == v) atomicOr(bad, 1u);                 // self-loop
+    if (u >= V || v >= V) atomicOr(bad, 2u);       // unknown vertex
+    keys[2 * i] = (uint64_t(u) << 32) | v;
+    keys[2 * i + 1] = (uint64_t(v) << 32) | u;
+    if (vals) {
+      vals[2 * i] = i;
+      vals[2 * i + 1] = i;
+    }
+  }
+}
+
+__global__ void k_check_dups(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x + 1; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (keys[i] == keys[i - 1]) atomicOr(bad, 4u);  // duplicate edge
+  }
+}
+
+__global__ void k_degrees(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* deg) {
+  // keys are sorted: count run lengths at run ends.
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t s = uint32_t(keys[i] >> 32);
+    bool last = (i + 1 == n) || uint32_t(keys[i + 1] >> 32) != s;
+    if (last) {
+      // binary search the run start
+      uint64_t lo = 0, hi = i;
+      while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (uint32_t(keys[mid] >> 32) < s) lo = mid + 1;
+        else hi = mid;
+      }
+      deg[s] = uint32_t(i + 1 - lo);
+    }
+  }
+}
+
+__global__ void k_caps(const uint32_t* __restrict__ deg, uint32_t V, float slack, uint32_t* cap,
+                       uint64_t* cap64) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    uint32_t c = slack_cap(deg[v], slack);
+    cap[v] = c;
+    cap64[v] = c;
+  }
+}
+
+__global__ void k_scatter(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals,
+                          uint64_t n, const uint64_t* __restrict__ dense_off,
+                          const uint64_t* __restrict__ off, uint32_t* adj,
+                          const uint32_t* __restrict__ edge_labels, uint32_t* elab) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t k = keys[i];
+    uint32_t s = uint32_t(k >> 32);
+    uint64_t p = off[s] + (i - dense_off[s]);
+    adj[p] = uint32_t(k);
+    if (elab) elab[p] = edge_labels ? edge_labels[vals[i]] : kNone;
+  }
+}
+
+// Warp per vertex: copy every list into a fresh pool with fresh slack.
+__global__ void k_compact(DevGraphMut g, const uint64_t* __restrict__ new_off,
+                          const uint32_t* __restrict__ new_cap, uint32_t* new_adj, uint32_t* new_elab) {
+  uint32_t lane = threadIdx.x & 31;
+  uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t v = warp; v < g.V; v += nwarps) {
+    uint32_t d = g.deg[v];
+    const uint32_t* src = g.adj + g.off[v];
+    uint32_t* dst = new_adj + new_off[v];
+    for (uint32_t i = lane; i < d; i += 32) dst[i] = src[i];
+    if (new_elab) {
+      const uint32_t* es = g.elab + g.off[v];
+      uint32_t* ed = new_elab + new_off[v];
+      for (uint32_t i = lane; i < d; i += 32) ed[i] = es[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------- per batch ---
+
+// K1: canonicalise and validate each update (UpdateBatch ctor,
+// src/graph.cpp:8-23; validate_batch, src/graph.cpp:117-135).  Presence is a
+// binary search in the lower-degree endpoint's sorted list.
+__global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, DevGraph g,
+                          BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
+                          uint8_t* ecode) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    bdsm_update_dev up = ups[i];
+    uint32_t del = up.op != 0 ? 1u : 0u;
+    keys[2 * i] = (uint64_t(up.u) << 32) | up.v;
+    keys[2 * i + 1] = (uint64_t(up.v) << 32) | up.u;
+    vals[2 * i] = i | (del << 31);
+    vals[2 * i + 1] = i | (del << 31);
+    uint32_t lab = kNone;
+    uint8_t code = 0;
+    if (up.u == up.v) {
+      atomicMin(&st->selfloop_min, i);
+    } else if (up.u >= g.V || up.v >= g.V) {
+      code = 1;  // unknown vertex
+    } else {
+      uint32_t du = g.deg[up.u], dv = g.deg[up.v];
+      uint32_t x = du <= dv ? up.u : up.v, y = du <= dv ? up.v : up.u;
+      uint32_t dx = du <= dv ? du : dv;
+      const uint32_t* lst = g.adj + g.off[x];
+      uint32_t p = lower_bound_u32(lst, dx, y);
+      bool present = p < dx && lst[p] == y;
+      if (present && !del) code = 2;  // insert of existing edge
+      if (!present && del) code = 3;  // delete of missing edge
+      if (present && g.elab) lab = g.elab[g.off[x] + p];
+    }
+    if (code) atomicAdd(&st->err_count, 1u);
+    // labelled insert while the graph keeps no label array: abort, the host
+    // materialises the labels and reruns the batch (nothing applied yet)
+    if (!del && up.elab != kNone && !g.elab) st->overflow = 4;
+    ecode[i] = code;
+    dlab[i] = lab;
+  }
+}
+
+// After the radix sort of the 2n directed keys: conflicting pairs, segment
+// heads (distinct sources = touched vertices), insert flags for the merge
+// prefix, and the per-phase same-kind endpoint bitmaps used by the
+// visibility rule (UpdateIndex, src/matcher.cpp:27-40).
+__global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                            uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
+                            uint32_t* ins_bits, uint32_t* del_bits, uint32_t V) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += gridDim.x * blockDim.x) {
+    if (j == m) {
+      insflag[j] = 0;
+      continue;
+    }
+    uint64_t k = skeys[j];
+    uint32_t val = svals[j];
+    uint32_t src = uint32_t(k >> 32);
+    bool is_del = val >> 31;
+    if (j > 0 && skeys[j - 1] == k) {
+      uint32_t a = svals[j - 1] & 0x7fffffffu, b = val & 0x7fffffffu;
+      atomicMin(&st->conflict_min, a > b ? a : b);
+    }
+    bool h = j == 0 || uint32_t(skeys[j - 1] >> 32) != src;
+    head[j] = h ? 1 : 0;
+    insflag[j] = is_del ? 0u : 1u;
+    if (src < V) atomicOr((is_del ? del_bits : ins_bits) + (src >> 5), 1u << (src & 31));
+  }
+}
+
+__device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, uint32_t nt, uint32_t m) {
+  return t + 1 < nt ? heads[t + 1] : m;
+}
+
+// K3 (part 1): per touched vertex, new degree and relocation when the merged
+// list no longer fits its slack.
+__global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+                        const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
+                        BatchState* st, uint64_t* new_off, uint32_t* new_cap) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  uint32_t nt = st->n_touched;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    uint32_t x = uint32_t(skeys[s] >> 32);
+    uint32_t nins = ins_prefix[e] - ins_prefix[s];
+    uint32_t ndel = (e - s) - nins;
+    uint32_t dnew = g.deg[x] + nins - ndel;
+    if (dnew > g.cap[x]) {
+      uint32_t c = slack_cap(dnew, slack);
+      new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
+      new_cap[t] = c;
+      atomicAdd((unsigned long long*)&st->relocations, 1ull);
+    } else {
+      new_off[t] = g.off[x];
+      new_cap[t] = 0;  // in place
+    }
+  }
+}
+
+// Position of old element `a` (index i) in the merged list, and whether the
+// batch deletes it.  seg/segn: the vertex's sorted batch keys (destination
+// ids); ipre: insert prefix at the segment start.
+__device__ __forceinline__ void merged_pos(const uint64_t* seg, uint32_t segn,
+                                           const uint32_t* ins_prefix, uint32_t s, uint32_t a,
+                                           uint32_t i, uint32_t& p, bool& deleted) {
+  // lower_bound on the low 32 bits (same source throughout the segment)
+  uint32_t lo = 0, hi = segn;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (uint32_t(seg[mid]) < a) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t I = ins_prefix[s + lo] - ins_prefix[s];
+  uint32_t D = lo - I;
+  deleted = lo < segn && uint32_t(seg[lo]) == a;
+  p = i - D + I;
+}
+
+// K3 (part 2) + K4: one warp per touched vertex.  Insert slots are computed
+// first against the intact old list.  In place (merged list fits the slack)
+// the old elements move in two sweeps — ascending for left-movers, descending
+// for right-movers — and each sweep only overwrites slots whose element has
+// already moved (the merged order is a monotone map of the old order), then
+// the inserts fill their slots.  Relocated lists are merged out of place.
+// The same warp then re-streams the new list to recount per-label neighbour
+// counters and recompute the candidate row of every query (K4).
+__global__ void __launch_bounds__(256) k_merge_refresh(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+    const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
+    const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
+    const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
+    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (st->pool_top > g.pool_size) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) st->overflow = 1;
+    return;
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nt = st->n_touched;
+  uint64_t bytes = 0;
+  for (uint32_t t = warp; t < nt; t += nwarps) {
+    const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    const uint64_t* seg = skeys + s;
+    const uint32_t segn = e - s;
+    const uint32_t x = uint32_t(seg[0] >> 32);
+    const uint32_t dold = g.deg[x];
+    const uint64_t ooff = g.off[x];
+    const uint32_t nins = ins_prefix[e] - ins_prefix[s];
+    const uint32_t dnew = dold + nins - (segn - nins);
+    const bool reloc = new_cap[t] != 0;
+    const uint64_t noff = new_off[t];
+    uint32_t* src = g.adj + ooff;
+    uint32_t* dst = g.adj + noff;
+    uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
+    uint32_t* edst = g.elab ? g.elab + noff : nullptr;
+
+    // 1. insert slots against the intact old list
+    for (uint32_t k = lane; k < segn; k += 32) {
+      if (svals[s + k] >> 31) continue;  // delete
+      uint32_t y = uint32_t(seg[k]);
+      uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+      uint32_t db = k - ib;
+      ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
+    }
+    __syncwarp();
+    // 2. move old elements
+    if (reloc) {
+      for (uint32_t i = lane; i < dold; i += 32) {
+        uint32_t a = src[i], p;
+        bool dl;
+        merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
+        if (!dl) {
+          dst[p] = a;
+          if (edst) edst[p] = esrc[i];
+        }
+      }
+    } else if (dold > 0) {
+      uint32_t start = 0;
+      if (lane == 0) start = lower_bound_u32(src, dold, uint32_t(seg[0]));  // below: never moves
+      start = __shfl_sync(kFull, start, 0);
+      for (uint32_t base = start; base < dold; base += 32) {  // left-movers, ascending
+        uint32_t i = base + lane, a = 0, p = 0, el = kNone;
+        bool dl = true;
+        if (i < dold) {
+          a = src[i];
+          if (esrc) el = esrc[i];
+          merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
+        }
+        __syncwarp();
+        if (i < dold && !dl && p < i) {
+          dst[p] = a;
+          if (edst) edst[p] = el;
+        }
+        __syncwarp();
+      }
+      if (dold > start) {  // right-movers, descending
+        int nch = int((dold - start + 31) / 32);
+        for (int c = nch - 1; c >= 0; --c) {
+          uint32_t i = start + uint32_t(c) * 32 + lane, a = 0, p = 0, el = kNone;
+          bool dl = true;
+          if (i < dold) {
+            a = src[i];
+            if (esrc) el = esrc[i];
+            merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
+          }
+          __syncwarp();
+          if (i < dold && !dl && p > i) {
+            dst[p] = a;
+            if (edst) edst[p] = el;
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncwarp();
+    // 3. inserts
+    for (uint32_t k = lane; k < segn; k += 32) {
+      uint32_t val = svals[s + k];
+      if (val >> 31) continue;
+      uint32_t p = ipos[s + k];
+      dst[p] = uint32_t(seg[k]);
+      if (edst) edst[p] = ups[val & 0x7fffffffu].elab;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      g.deg[x] = dnew;
+      if (reloc) {
+        g.off[x] = noff;
+        g.cap[x] = new_cap[t];
+      }
+    }
+    bytes += 4ull * (uint64_t(dold) + dnew);
+    // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
+    for (uint32_t q = 0; q < nq; ++q) {
+      const DevQueryEnc& qe = qenc[q];
+      uint32_t cnt = 0;  // lane g holds group g's count
+      for (uint32_t base = 0; base < dnew; base += 32) {
+        uint32_t i = base + lane;
+        uint32_t lab = i < dnew ? __ldg(g.vlabel + dst[i]) : kNone;
+        for (uint32_t gi = 0; gi < qe.G; ++gi) {
+          uint32_t b = __ballot_sync(kFull, lab == qe.glabel[gi]);
+          if (lane == gi) cnt += __popc(b);
+        }
+      }
+      if (cnt > qe.cap) cnt = qe.cap;
+      uint32_t vl = g.vlabel[x];
+      uint32_t row = 0;
+      for (uint32_t u = 0; u < qe.n; ++u) {
+        bool ok = lane >= qe.G || cnt >= qe.qcnt[u][lane];
+        bool all = __all_sync(kFull, ok);
+        if (all && vl == qe.qlabel[u]) row |= 1u << u;
+      }
+      if (lane == 0) {
+        uint32_t before = rows[q][x];
+        if (before != row) {
+          rows[q][x] = row;
+          uint32_t diff = before ^ row;
+          while (diff) {
+            uint32_t u = __ffs(diff) - 1;
+            diff &= diff - 1;
+            atomicAdd((unsigned long long*)(colsize[q] + u),
+                      (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+}
+
+// Full encode (QueryEncodingState::initialize, src/matcher.cpp:10-18):
+// warp per vertex computes the candidate row of one query.
+__global__ void __launch_bounds__(256) k_encode_all(DevGraph g, const DevQueryEnc* __restrict__ qenc,
+                                                    uint32_t* rows) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const DevQueryEnc& qe = *qenc;
+  for (uint64_t v = warp; v < g.V; v += nwarps) {
+    uint32_t vl = g.vlabel[v];
+    bool any = false;
+    for (uint32_t u = 0; u < qe.n; ++u) any |= vl == qe.qlabel[u];
+    if (!any) {  // label absent from the query: empty row without a scan
+      if (lane == 0) rows[v] = 0;
+      continue;
+    }
+    uint32_t d = g.deg[v];
+    const uint32_t* lst = g.adj + g.off[v];
+    uint32_t cnt = 0;
+    for (uint32_t base = 0; base < d; base += 32) {
+      uint32_t i = base + lane;
+      uint32_t lab = i < d ? __ldg(g.vlabel + lst[i]) : kNone;
+      for (uint32_t gi = 0; gi < qe.G; ++gi) {
+        uint32_t b = __ballot_sync(kFull, lab == qe.glabel[gi]);
+        if (lane == gi) cnt += __popc(b);
+      }
+    }
+    if (cnt > qe.cap) cnt = qe.cap;
+    uint32_t row = 0;
+    for (uint32_t u = 0; u < qe.n; ++u) {
+      bool ok = lane >= qe.G || cnt >= qe.qcnt[u][lane];
+      if (__all_sync(kFull, ok) && vl == qe.qlabel[u]) row |= 1u << u;
+    }
+    if (lane == 0) rows[v] = row;
+  }
+}
+
+__global__ void k_column_sizes(const uint32_t* __restrict__ rows, uint32_t V, uint32_t n, uint64_t* out) {
+  __shared__ unsigned long long acc[32];
+  if (threadIdx.x < 32) acc[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t local[kMaxQ] = {0};
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    uint32_t r = rows[v];
+    for (uint32_t u = 0; u < n && u < kMaxQ; ++u) local[u] += (r >> u) & 1u;
+  }
+  for (uint32_t u = 0; u < n && u < kMaxQ; ++u) {
+    uint32_t c = local[u];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&acc[u], (unsigned long long)c);
+  }
+  __syncthreads();
+  if (threadIdx.x < n && threadIdx.x < kMaxQ && acc[threadIdx.x])
+    atomicAdd((unsigned long long*)out + threadIdx.x, acc[threadIdx.x]);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers ----
+
+void launch_build_keys(const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t V,
+                       uint64_t* keys, uint64_t* vals, uint32_t* bad, cudaStream_t s) {
+  k_build_keys<<<blocks_for(E), kThreads, 0, s>>>(src, dst, E, V, keys, vals, bad);
+}
+void launch_check_sorted_dups(const uint64_t* keys, uint64_t n, uint32_t* bad, cudaStream_t s) {
+  k_check_dups<<<blocks_for(n), kThreads, 0, s>>>(keys, n, bad);
+}
+void launch_degrees(const uint64_t* keys, uint64_t n, uint32_t* deg, cudaStream_t s) {
+  k_degrees<<<blocks_for(n), kThreads, 0, s>>>(keys, n, deg);
+}
+void launch_caps(const uint32_t* deg, uint32_t V, float slack, uint32_t* cap, uint64_t* cap64,
+                 cudaStream_t s) {
+  k_caps<<<blocks_for(V), kThreads, 0, s>>>(deg, V, slack, cap, cap64);
+}
+void launch_scatter(const uint64_t* keys, const uint64_t* vals, uint64_t n, const uint64_t* dense_off,
+                    const uint64_t* off, uint32_t* adj, const uint32_t* edge_labels, uint32_t* elab,
+                    cudaStream_t s) {
+  k_scatter<<<blocks_for(n), kThreads, 0, s>>>(keys, vals, n, dense_off, off, adj, edge_labels, elab);
+}
+void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* new_cap,
+                    uint32_t* new_adj, uint32_t* new_elab, cudaStream_t s) {
+  (void)new_cap;
+  k_compact<<<blocks_for(uint64_t(g_old.V) * 32), kThreads, 0, s>>>(g_old, new_off, new_cap, new_adj,
+                                                                    new_elab);
+}
+void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, BatchState* st,
+                    uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, cudaStream_t s) {
+  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, st, keys, vals, dlab, ecode);
+}
+void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
+                      uint8_t* head, uint32_t* insflag, uint32_t* ins_bits, uint32_t* del_bits,
+                      uint32_t V, cudaStream_t s) {
+  k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(skeys, svals, m, st, head, insflag,
+                                                              ins_bits, del_bits, V);
+}
+void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
+                  uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
+                  uint32_t* new_cap, cudaStream_t s) {
+  k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap);
+}
+void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
+                          const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
+                          DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
+                          uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
+                          uint64_t* const* colsize, BatchState* st, int num_sms, cudaStream_t s) {
+  // one warp per touched vertex (<= m), persistent over a bounded grid
+  uint64_t warps = m ? m : 1;
+  uint64_t blocks = (warps * 32 + 255) / 256;
+  uint64_t cap = uint64_t(num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
+                                                  new_cap, ipos, qenc, nq, rows, colsize, st);
+}
+void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
+  k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);
+}
+void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s) {
+  k_column_sizes<<<blocks_for(V), kThreads, 0, s>>>(rows, V, n, out);
+}
+
+}  // namespace bdsm_b200

