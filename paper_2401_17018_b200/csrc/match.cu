@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         r_cur = item.begin;
         r_end = min(item.begin + a.chunk, task.d);
         r_mask = 0;
-        r_drv = dpos;
+        r_drv = P.lv[2].backmask == 3u ? dpos : 0u;  // index into the backward list
       }
     }
     __syncwarp();

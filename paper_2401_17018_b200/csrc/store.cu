@@ -213,7 +213,7 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
     uint32_t nins = ins_prefix[e] - ins_prefix[s];
     uint32_t ndel = (e - s) - nins;
     uint32_t dnew = g.deg[x] + nins - ndel;
-    if (dnew > g.cap[x]) {
+    if (dnew > g.cap[x] || (nins && ndel)) {  // overflow, or a mixed segment (see merge)
       uint32_t c = slack_cap(dnew, slack);
       new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
       new_cap[t] = c;
@@ -305,25 +305,29 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
         }
       }
     } else if (dold > 0) {
+      // In place only for single-kind segments (k_alloc relocates mixed ones):
+      // delete-only lists move left (ascending sweep), insert-only lists move
+      // right (descending sweep); either sweep writes only to slots already read.
       uint32_t start = 0;
       if (lane == 0) start = lower_bound_u32(src, dold, uint32_t(seg[0]));  // below: never moves
       start = __shfl_sync(kFull, start, 0);
-      for (uint32_t base = start; base < dold; base += 32) {  // left-movers, ascending
-        uint32_t i = base + lane, a = 0, p = 0, el = kNone;
-        bool dl = true;
-        if (i < dold) {
-          a = src[i];
-          if (esrc) el = esrc[i];
-          merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
+      if (nins == 0) {
+        for (uint32_t base = start; base < dold; base += 32) {  // left-movers, ascending
+          uint32_t i = base + lane, a = 0, p = 0, el = kNone;
+          bool dl = true;
+          if (i < dold) {
+            a = src[i];
+            if (esrc) el = esrc[i];
+            merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
+          }
+          __syncwarp();
+          if (i < dold && !dl && p < i) {
+            dst[p] = a;
+            if (edst) edst[p] = el;
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        if (i < dold && !dl && p < i) {
-          dst[p] = a;
-          if (edst) edst[p] = el;
-        }
-        __syncwarp();
-      }
-      if (dold > start) {  // right-movers, descending
+      } else if (dold > start) {  // right-movers, descending
         int nch = int((dold - start + 31) / 32);
         for (int c = nch - 1; c >= 0; --c) {
           uint32_t i = start + uint32_t(c) * 32 + lane, a = 0, p = 0, el = kNone;
