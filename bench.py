@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the per-batch hot path (match_batch) — prints ONE JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one batch of the configured stream applied to the evolving graph:
+validate -> negative phase on G -> merge + refresh -> positive phase on G'
+-> counts.  Default workload: BASELINE.json configs[1]
+(C2, LiveJournal-shaped, 6-vertex query, 10K mixed updates per batch).
+
+  value   updates/s with the batch already resident in HBM (device-input
+          C ABI entry point), device time from CUDA events on the engine's
+          stream, max over ranks; L2 flushed between steps (outside timing).
+  e2e     same metric through the host-buffer C ABI call (H2D of the batch
+          and D2H of the counts inside the timed region), on a second engine
+          replaying the same stream; its counts must equal the first's.
+  roofline  dominant kernel's algorithmic bytes / its
+          CUDA-event time vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the UNMODIFIED reference (oracle/_ref/ref_bench) on a bounded
+          prefix sample of the same stream, all host threads (rank 0, N=1).
+
+--impl reference times the reference's own CPU path (oracle/_ref/ref_bench,
+else the oracle port) on the same workload and prints the same line shape.
+Multi-GPU (torchrun): graph replicated per rank, each batch's work units
+split by the cost-balanced rule, counts summed with an NCCL all-reduce.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workload as W  # noqa: E402
+
+METRIC = "ms per update batch & updates/s (incremental matches), LJ-shape 6-vertex query"
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.out = None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self.out = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.out, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.out:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.out.name) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.out.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference_binary(path: str, prefix: int, batches: int, time_cap: float, timeout: float):
+    """Runs oracle/_ref/ref_bench (else oracle/oracle_bench) on a workload file."""
+    ref = os.path.join(REPO, "oracle", "_ref", "ref_bench")
+    kind = "reference"
+    if not os.path.exists(ref):
+        subprocess.run(["make", "-s", "-C", os.path.join(REPO, "oracle")], check=False)
+        ref = os.path.join(REPO, "oracle", "oracle_bench")
+        kind = "port"
+    cores = os.cpu_count() or 1
+    flag = "--workers" if kind == "reference" else "--threads"
+    cmd = [ref, path, flag, str(cores), "--prefix", str(prefix), "--batches", str(batches),
+           "--time-cap", str(time_cap)]
+    log("cpu baseline:", " ".join(cmd))
+    t0 = time.time()
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    except subprocess.TimeoutExpired as e:
+        lines = [json.loads(l) for l in (e.stdout or b"").decode().splitlines() if l.startswith("{")]
+        return {"kind": kind, "cores": cores, "error": f"timeout after {timeout:.0f}s", "batches": lines[:-1]}
+    wall = time.time() - t0
+    summ = [l for l in lines if l.get("summary")]
+    per = [l for l in lines if "batch" in l]
+    if not summ:
+        return {"kind": kind, "cores": cores, "error": (out.stderr or out.stdout)[-300:], "batches": per}
+    return {"kind": kind, "cores": cores, "summary": summ[0], "batches": per, "wall_s": wall}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=None, help="override updates per batch")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-prefix", type=int, default=1000, help="updates per CPU-baseline sub-batch")
+    ap.add_argument("--cpu-batches", type=int, default=3)
+    ap.add_argument("--cpu-time-cap", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chunk", type=int, default=64)
+    args = ap.parse_args()
+
+    world, rank, local = dist_env()
+    if args.steps < 1 or args.warmup < 3:
+        log("warmup must be >= 3 and steps >= 1")
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+    return ours(args, world, rank, local)
+
+
+def gen_workload(args, nbatches, device):
+    t0 = time.time()
+    wl = W.build(args.config, nbatches, device=device, batch=args.batch)
+    log(f"workload {args.config}: {wl.meta} query labels={wl.qlabels} edges={wl.qedges} "
+        f"gen {time.time() - t0:.1f}s")
+    return wl
+
+
+def config_dict(args, wl, world):
+    m = wl.meta
+    return {"workload": f"{args.config}: {m['desc']}", "config_id": args.config, "V": m["V"], "E": m["E"],
+            "labels": m["L"], "generator": m["generator"], "d_max": m["d_max"], "batch_updates": m["batch"],
+            "batch_mode": m["mode"], "query_vertices": len(wl.qlabels), "query_edges": len(wl.qedges),
+            "query_labels": wl.qlabels, "query": wl.qedges, "seeds": m["seeds"],
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"replicated graph, work units split over {world} GPU(s)" if world > 1 else "1 GPU"}
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    nb = max(args.steps + args.warmup, 1)
+    device = "cuda" if torch.cuda.is_available() else "cpu"
+    wl = gen_workload(args, nb, device)
+    tmp = tempfile.mkdtemp(prefix="bdsm_ref_")
+    path = os.path.join(tmp, "workload.bin")
+    W.write_file(wl, path)
+    steps = args.steps
+    res = run_reference_binary(path, args.cpu_prefix, steps, time_cap=max(args.cpu_time_cap, 1.0) * 3,
+                               timeout=900)
+    shutil.rmtree(tmp, ignore_errors=True)
+    line = {"impl": "reference", "metric": METRIC, "unit": "updates/s", "higher_is_better": True,
+            "n_gpus": world, "steps": steps, "warmup": 0, "dtype": "u32", "data": "synthetic",
+            "config": config_dict(args, wl, 1), "vs_baseline": None}
+    if "summary" not in res:
+        line.update({"value": None, "unavailable": res.get("error", "reference failed")})
+    else:
+        s = res["summary"]
+        line.update({"value": s["updates_per_s"], "ms_per_step": s["median_ms"], "steps": s["batches"],
+                     "cpu_baseline": {"value": s["updates_per_s"], "unit": "updates/s", "cores": res["cores"],
+                                      "kind": res["kind"],
+                                      "sample": f"first {args.cpu_prefix} updates of each of {s['batches']} "
+                                                f"consecutive {wl.meta['batch']}-update batches (rest applied "
+                                                f"untimed); graph build {s.get('build_s', 0):.1f}s excluded"},
+                     "e2e": {"value": s["updates_per_s"], "unit": "updates/s", "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0},
+                     "per_batch": [{k: b[k] for k in ("positive", "negative", "ms", "dfs_visits")}
+                                   for b in res["batches"]]})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ours(args, world, rank, local):
+    import paper_2401_17018_b200 as bd
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}), flush=True)
+        return 1
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    nb = args.warmup + args.steps
+    wl = gen_workload(args, nb, dev)
+    torch.cuda.synchronize()
+
+    t0 = time.time()
+    engA = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
+                     chunk=args.chunk)
+    engA.add_query(wl.qlabels, wl.qedges)
+    engB = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
+                     chunk=args.chunk)
+    engB.add_query(wl.qlabels, wl.qedges)
+    log(f"engines built in {time.time() - t0:.1f}s")
+
+    # batches resident in HBM for `value`
+    dev_batches = [torch.from_numpy(b.view(np.uint32).reshape(-1, 4).copy()).to(dev) for b in wl.batches]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def allreduce(vals, op="sum"):
+        if world == 1:
+            return vals
+        import torch.distributed as dist
+        t = torch.tensor(vals, dtype=torch.float64 if op == "max" else torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.tolist()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up (both engines walk the same stream)
+    countsA, countsB = [], []
+    for i in range(args.warmup):
+        rA = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
+        rB = engB.match_batch(wl.batches[i])
+        countsA.append((rA.positive[0], rA.negative[0]))
+        countsB.append((rB.positive[0], rB.negative[0]))
+
+    statsA = []
+    dev_ms = []
+    with ClockSampler(local if not os.environ.get("CUDA_VISIBLE_DEVICES") else 0) as clk:
+        for i in range(args.warmup, nb):
+            flush.zero_()
+            barrier()
+            r = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
+            dev_ms.append(r.stats["ms_device"])
+            statsA.append(r.stats)
+            countsA.append((r.positive[0], r.negative[0]))
+        e2e_ms = []
+        for i in range(args.warmup, nb):
+            flush.zero_()
+            barrier()
+            t1 = time.perf_counter()
+            r = engB.match_batch(wl.batches[i])
+            e2e_ms.append((time.perf_counter() - t1) * 1e3)
+            countsB.append((r.positive[0], r.negative[0]))
+    barrier()
+    clocks = clk.summary()
+
+    tot_dev = allreduce([sum(dev_ms)], "max")[0]
+    tot_e2e = allreduce([sum(e2e_ms)], "max")[0]
+    flatA = allreduce([c for pn in countsA for c in pn])
+    flatB = allreduce([c for pn in countsB for c in pn])
+    if rank != 0:
+        return 0
+    updates = sum(len(b) for b in wl.batches[args.warmup:])
+    value = updates / (tot_dev / 1e3)
+    e2e_value = updates / (tot_e2e / 1e3)
+    parity_ok = flatA == flatB
+
+    # roofline of the dominant kernel (mean over the timed steps)
+    peak, peak_kind = peaks()
+    mk = statistics.mean(s["ms_match_kernel"] for s in statsA)
+    mg = statistics.mean(s["ms_merge_kernel"] for s in statsA)
+    bphase = statistics.mean(s["bytes_phase"] for s in statsA)
+    bupd = statistics.mean(s["bytes_update"] for s in statsA)
+    kern = {
+        "k_wbm (K6 matching, both phases)": (bphase, mk),
+        "k_alloc+k_merge_refresh (K3+K4)": (bupd, mg),
+    }
+    dom = max(kern, key=lambda k: kern[k][1])
+    ab, at = kern[dom]
+    achieved = ab / (at / 1e3) / 1e9 if at > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
+            "other": {k: {"bytes": v[0], "ms": v[1], "GB/s": (v[0] / (v[1] / 1e3) / 1e9 if v[1] > 0 else 0)}
+                      for k, v in kern.items() if k != dom},
+            "share_of_step": at / statistics.mean(dev_ms)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_dev / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config_dict(args, wl, world),
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "updates/s", "ms_per_step": tot_e2e / args.steps,
+                "h2d_bytes_per_step": int(16 * statistics.mean(len(b) for b in wl.batches[args.warmup:])),
+                "d2h_bytes_per_step": int(statsA[-1]["d2h_bytes"]),
+                "path": "bdsm_engine_apply_batch (host buffers, C ABI)"},
+        "gpu_launches": int(sum(s["kernel_launches"] for s in statsA)),
+        "cub_launches": int(sum(s["cub_launches"] for s in statsA)),
+        "roofline": roof,
+        "counts": {"positive": [c for c in flatA[0::2]], "negative": [c for c in flatA[1::2]],
+                   "e2e_equals_device_path": parity_ok},
+        "per_step": [{"ms": s["ms_device"], "neg_ms": s["ms_negative"], "merge_ms": s["ms_update"],
+                      "pos_ms": s["ms_positive"], "match_kernel_ms": s["ms_match_kernel"],
+                      "dfs_visits": s["dfs_visits"], "tasks": s["tasks"], "items": s["work_items"],
+                      "touched": s["touched"], "relocations": s["relocations"]} for s in statsA],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        tmp = tempfile.mkdtemp(prefix="bdsm_cpu_")
+        path = os.path.join(tmp, "workload.bin")
+        W.write_file(wl, path)
+        res = run_reference_binary(path, args.cpu_prefix, args.cpu_batches, args.cpu_time_cap, timeout=600)
+        shutil.rmtree(tmp, ignore_errors=True)
+        if "summary" in res:
+            s = res["summary"]
+            line["cpu_baseline"] = {
+                "value": s["updates_per_s"], "unit": "updates/s", "cores": res["cores"], "kind": res["kind"],
+                "median_ms_per_subbatch": s["median_ms"],
+                "sample": f"first {args.cpu_prefix} updates of each of the first {s['batches']} batches of the "
+                          f"same stream (rest applied untimed), {res['cores']} worker threads, "
+                          f"coalesce off; graph build {s.get('build_s', 0):.1f}s excluded",
+                "per_batch": [{k: b[k] for k in ("positive", "negative", "ms")} for b in res["batches"]]}
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "updates/s", "cores": res.get("cores"),
+                                    "kind": res.get("kind"), "sample": "failed", "error": res.get("error")}
+    print(json.dumps(line), flush=True)
+    engA.close()
+    engB.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

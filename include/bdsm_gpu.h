@@ -110,6 +110,10 @@ typedef struct bdsm_batch_stats {
   uint32_t timed_out;     /* bitmask of queries whose deadline passed (counts dropped) */
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
+  double ms_match_kernel;  /* CUDA-event time of the K6 matching kernels (both phases) */
+  double ms_merge_kernel;  /* CUDA-event time of K3 alloc + merge/refresh */
+  uint32_t kernel_launches;/* launches of this library's own kernels (CUB sort/scan excluded) */
+  uint32_t cub_launches;   /* CUB sort / select / scan calls */
 } bdsm_batch_stats;
 
 /* Engine lifecycle.  Replaces LabeledGraph::build_from_edges plus the

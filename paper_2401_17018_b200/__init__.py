@@ -65,7 +65,8 @@ class _Stats(C.Structure):
                 ("tasks", C.c_uint64), ("work_items", C.c_uint64), ("gen_calls", C.c_uint64),
                 ("bytes_phase", C.c_uint64), ("bytes_update", C.c_uint64), ("touched", C.c_uint64),
                 ("relocations", C.c_uint64), ("compactions", C.c_uint32), ("timed_out", C.c_uint32),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("ms_match_kernel", C.c_double),
+                ("ms_merge_kernel", C.c_double), ("kernel_launches", C.c_uint32), ("cub_launches", C.c_uint32)]
 
 
 _lib = None

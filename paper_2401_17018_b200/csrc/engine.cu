@@ -128,6 +128,18 @@ struct bdsm_engine {
   bdsm_update* h_ups = nullptr;
   size_t h_ups_cap = 0;
   cudaEvent_t ev[6] = {};
+  cudaEvent_t merge_ev[2] = {};
+  std::vector<cudaEvent_t> kev;  // pairs around K6 launches, then the merge pair
+  size_t kev_used = 0;
+  uint32_t launches = 0, cub_calls = 0;
+  cudaEvent_t next_kev() {
+    if (kev_used == kev.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      kev.push_back(e);
+    }
+    return kev[kev_used++];
+  }
 
   std::vector<bdsm_update_error> last_errors;
 
@@ -135,6 +147,9 @@ struct bdsm_engine {
     if (device >= 0) cudaSetDevice(device);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : merge_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : kev) cudaEventDestroy(e);
     if (h_st) cudaFreeHost(h_st);
     if (h_ups) cudaFreeHost(h_ups);
     if (stream) cudaStreamDestroy(stream);
@@ -558,7 +573,14 @@ struct bdsm_engine {
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_cost.p, cost_off.p, int(n + 1), stream));
       launch_anchor_emit(a, stream);
       CK(cudaMemsetAsync(&d_st.p->next_item, 0, sizeof(uint32_t), stream));
-      if (qs.q.n > 2) launch_wbm(a, num_sms, stream);
+      launches += 2;
+      cub_calls += 3;
+      if (qs.q.n > 2) {
+        CK(cudaEventRecord(next_kev(), stream));
+        launch_wbm(a, num_sms, stream);
+        CK(cudaEventRecord(next_kev(), stream));
+        ++launches;
+      }
     }
   }
 
@@ -598,8 +620,10 @@ struct bdsm_engine {
     ensure_batch(n);
     ensure_tasks(n);
     if (!h_st) CK(cudaMallocHost(&h_st, sizeof(BatchState)));
-    if (!ev[0])
+    if (!ev[0]) {
       for (auto& e : ev) CK(cudaEventCreate(&e));
+      for (auto& e : merge_ev) CK(cudaEventCreate(&e));
+    }
     d_st.ensure(1);
     const bdsm_update_dev* src;
     if (device_input) {
@@ -612,6 +636,9 @@ struct bdsm_engine {
     uint32_t compactions = 0;
     for (int attempt = 0;; ++attempt) {
       if (attempt > 8) throw std::runtime_error("batch could not be scheduled");
+      kev_used = 0;
+      launches = 0;
+      cub_calls = 0;
       CK(cudaEventRecord(ev[0], stream));
       if (!device_input) {
         CK(cudaMemcpyAsync(ups.p, h_ups, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
@@ -649,9 +676,14 @@ struct bdsm_engine {
       CK(cudaEventRecord(ev[1], stream));
       run_phase(uint32_t(n), 0);
       CK(cudaEventRecord(ev[2], stream));
+      cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
+      CK(cudaEventRecord(m0, stream));
       launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, stream);
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, src, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, num_sms, stream);
+      CK(cudaEventRecord(m1, stream));
+      launches += 4;  // prepare, post_sort, alloc, merge_refresh
+      cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);
       CK(cudaEventRecord(ev[4], stream));
@@ -716,6 +748,16 @@ struct bdsm_engine {
     st.ms_update = ms;
     cudaEventElapsedTime(&ms, ev[3], ev[4]);
     st.ms_positive = ms;
+    double mk = 0;
+    for (size_t i = 0; i + 1 < kev_used; i += 2) {
+      cudaEventElapsedTime(&ms, kev[i], kev[i + 1]);
+      mk += ms;
+    }
+    st.ms_match_kernel = mk;
+    cudaEventElapsedTime(&ms, merge_ev[0], merge_ev[1]);
+    st.ms_merge_kernel = ms;
+    st.kernel_launches = launches;
+    st.cub_launches = cub_calls;
     st.dfs_visits = b.visits;
     st.tasks = b.tasks_total;
     st.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
