@@ -66,6 +66,35 @@ struct Item {
   uint32_t begin;
 };
 
+// A donated DFS subtree (work sharing): the prefix
+// assignment M[0..level), and the driver-index range [begin, end) of `level`.
+// Either a driver range (ncand == 0) or an explicit list of already-filtered
+// candidates of `level` taken from the donor's current chunk.
+struct DynItem {
+  uint32_t task;
+  uint32_t level;
+  uint32_t begin;
+  uint32_t end;
+  uint32_t ncand;
+  uint32_t pad[3];
+  uint32_t M[kMaxQ];
+  uint32_t cand[32];
+};
+
+// Work-queue counters of one matching launch, each on its own 128-byte line
+// so idle warps polling the queue do not contend with the busy warps' atomics.
+struct alignas(128) PaddedU32 {
+  uint32_t v;
+  uint32_t pad[31];
+};
+struct QueueState {
+  PaddedU32 next_item;  // static work-item head
+  PaddedU32 dyn_head;   // donated-item queue: pop / push counters
+  PaddedU32 dyn_tail;
+  PaddedU32 busy;       // warps holding work
+  PaddedU32 idle;       // warps waiting for donations
+};
+
 // Device-side batch bookkeeping, copied back once per batch.
 struct BatchState {
   uint32_t err_count;            // validate_batch failures
@@ -76,7 +105,7 @@ struct BatchState {
   uint32_t timed_out;            // bitmask over queries
   uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
   uint32_t n_items[2];
-  uint32_t next_item;            // work-queue head of the running phase
+  uint32_t donations;            // statistics: donated subtrees
   uint32_t pad;
   uint64_t pool_top;             // adjacency pool bump pointer (elements)
   uint64_t relocations;

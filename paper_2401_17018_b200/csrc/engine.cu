@@ -122,6 +122,10 @@ struct bdsm_engine {
   DBuf<Task> tasks;
   DBuf<Item> items;
   size_t max_items = 0;
+  DBuf<DynItem> dyn;           // donated-subtree queue of the matching kernel
+  DBuf<QueueState> qstate;
+  DBuf<uint32_t> dyn_ready;
+  uint32_t epoch = 0;
   DBuf<uint8_t> cub_tmp;
   DBuf<BatchState> d_st;
   BatchState* h_st = nullptr;
@@ -510,6 +514,12 @@ struct bdsm_engine {
       max_items = std::max<size_t>(tasks.n * 4, size_t(1) << 22);
       items.ensure(max_items);
     }
+    if (!dyn.p) {
+      qstate.ensure(1);
+      dyn.ensure(size_t(1) << 20);  // 80 MiB of donated subtrees per launch
+      dyn_ready.ensure(dyn.n);
+      CK(cudaMemsetAsync(dyn_ready.p, 0, 4 * dyn_ready.n, stream));
+    }
   }
 
   void ensure_host_ups(size_t n) {
@@ -552,6 +562,11 @@ struct bdsm_engine {
     a.max_items = uint32_t(std::min<size_t>(max_items, 0xffffffffu));
     a.st = d_st.p;
     a.deadline_ns = 0;
+    a.q = qstate.p;
+    a.dyn = dyn.p;
+    a.dyn_ready = dyn_ready.p;
+    a.dyn_cap = uint32_t(dyn.n);
+    a.merge_ratio = 8;
     return a;
   }
 
@@ -572,7 +587,9 @@ struct bdsm_engine {
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_counts.p, item_off.p, int(n + 1), stream));
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_cost.p, cost_off.p, int(n + 1), stream));
       launch_anchor_emit(a, stream);
-      CK(cudaMemsetAsync(&d_st.p->next_item, 0, sizeof(uint32_t), stream));
+      // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
+      CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
+      a.epoch = ++epoch;
       launches += 2;
       cub_calls += 3;
       if (qs.q.n > 2) {

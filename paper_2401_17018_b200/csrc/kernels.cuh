@@ -91,6 +91,12 @@ struct PhaseArgs {
   uint32_t max_items;
   BatchState* st;
   uint64_t deadline_ns;          // 0: none
+  QueueState* q;                 // work-queue counters (reset before each launch)
+  DynItem* dyn;                  // donated-subtree queue
+  uint32_t* dyn_ready;           // per-slot epoch: slot is readable when == epoch
+  uint32_t dyn_cap;
+  uint32_t epoch;
+  uint32_t merge_ratio;          // merge-window intersection when |other| <= ratio x |driver|
 };
 
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);

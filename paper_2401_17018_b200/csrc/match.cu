@@ -184,78 +184,287 @@ __device__ __forceinline__ bool bit_set(const uint32_t* bits, uint32_t v) {
   return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
 }
 
-// K6: persistent warp-per-partial-match DFS counter.
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// Donated-subtree queue (bounded, indices only grow within one launch).
+__device__ __forceinline__ uint32_t dyn_reserve(QueueState* q, uint32_t cap) {
+  uint32_t t = ld_volatile(&q->dyn_tail.v);
+  while (t < cap) {
+    uint32_t old = atomicCAS(&q->dyn_tail.v, t, t + 1);
+    if (old == t) return t;
+    t = old;
+  }
+  return kNone;
+}
+
+__device__ __forceinline__ bool dyn_pop(QueueState* q, uint32_t* slot) {
+  uint32_t h = ld_volatile(&q->dyn_head.v);
+  while (true) {
+    if (h >= ld_volatile(&q->dyn_tail.v)) return false;
+    uint32_t old = atomicCAS(&q->dyn_head.v, h, h + 1);
+    if (old == h) {
+      *slot = h;
+      return true;
+    }
+    h = old;
+  }
+}
+
+constexpr int kFloorB = 8;  // backward lists per level with a tracked search floor
+
+// Membership of each lane's candidate c in the sorted list L[0, n), for
+// lanes with `want` (their candidates ascend with the lane id, and exceed
+// every candidate of earlier chunks).  Merge-path style: the warp walks
+// 32-element windows of L from the floor `fl` with one coalesced load per
+// window and resolves candidates by a 5-step shuffle search; `fl` ends at the
+// last window, a valid floor for the next chunk.
+__device__ __forceinline__ bool member_merge(const uint32_t* __restrict__ L, uint32_t n, uint32_t& fl,
+                                             uint32_t c, bool want, uint32_t lane, uint32_t* pos) {
+  bool found = false;
+  bool pending = want;
+  uint32_t f = fl;
+  while (__any_sync(kFull, pending)) {
+    if (f >= n) break;
+    uint32_t i = f + lane;
+    uint32_t w = i < n ? __ldg(L + i) : 0xffffffffu;
+    uint32_t wmax = __shfl_sync(kFull, w, 31);
+    uint32_t lo = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      uint32_t v = __shfl_sync(kFull, w, lo + step - 1);
+      if (v < c) lo += step;
+    }
+    uint32_t wl = __shfl_sync(kFull, w, lo);
+    if (pending && c <= wmax) {
+      found = wl == c;
+      *pos = f + lo;
+      pending = false;
+    }
+    if (__any_sync(kFull, pending)) f += 32;
+  }
+  fl = f;
+  return found;
+}
+
+// K6: persistent warp-per-partial-match DFS counter with work donation.
+//
+// Work sources, in order: static items (level-2 chunks of every anchor),
+// then subtrees donated by busy warps.  A busy warp checks every few chunk
+// fetches whether warps are idle and the donation queue is short; if so it
+// gives away the upper half of the remaining driver range at its shallowest
+// splittable level (the reference's active stealing takes the same share,
+// src/scheduler.cpp:49-64, claim_upper_half), pushing its prefix assignment.
+// Ranges are disjoint, so counts are exact regardless of scheduling.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
+  __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
   if (batch_aborted(a.st)) return;
+  BatchState* st = a.st;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
-  const uint32_t n_items = a.st->n_items[a.phase];
+  const uint32_t n_items = st->n_items[a.phase];
   const DevGraph& g = a.g;
   uint64_t count = 0, visits = 0, bytes = 0, calls = 0;
-  uint32_t tick = 0;
+  uint32_t tick = 0, dtick = 0, backoff = 500;
   bool timed_out = false;
+  bool static_done = false, was_idle = false;
 
   // Lane-distributed per-level DFS state: lane l holds level l's.
   uint64_t r_off = 0;   // driver list offset
   uint32_t r_cur = 0;   // next driver index to fetch
   uint32_t r_end = 0;   // end of driver range
   uint32_t r_mask = 0;  // unexplored candidates of the current chunk
-  uint32_t r_drv = 0;   // position of the driver among the backward neighbours
+  uint32_t r_drv = 0;   // index of the driver in the level's backward list
   uint32_t r_touch = 0; // lane l: is M[l] a same-kind batch endpoint
+  uint32_t r_dlen = 0;  // length of the driver list
 
   while (true) {
-    uint32_t item_idx = 0;
-    if (lane == 0) item_idx = atomicAdd(&a.st->next_item, 1u);
-    item_idx = __shfl_sync(kFull, item_idx, 0);
-    if (item_idx >= n_items) break;
-    if (a.deadline_ns) {
-      if (globaltimer() > a.deadline_ns) {
-        timed_out = true;
-        break;
+    // ---- acquire work ----------------------------------------------------
+    uint32_t kind = 0, ref = 0;  // 1 static item, 2 donated item, 3 exit
+    QueueState* Q = a.q;
+    if (lane == 0) {
+      // `busy` counts warps holding work; only holders push donations, so
+      // "no holder and an empty queue" means the launch is finished.  A warp
+      // between its pop and its increment may make others leave early; it
+      // still completes (and re-pops its own donations), so no work is lost.
+      if (!static_done) {
+        uint32_t idx = atomicAdd(&Q->next_item.v, 1u);
+        if (idx < n_items) {
+          kind = 1;
+          ref = idx;
+        } else {
+          static_done = true;
+        }
+      }
+      if (!kind && dyn_pop(Q, &ref)) kind = 2;
+      if (kind) {
+        atomicAdd(&Q->busy.v, 1u);
+      } else {
+        if (ld_volatile(&Q->busy.v) == 0 && ld_volatile(&Q->dyn_head.v) >= ld_volatile(&Q->dyn_tail.v)) kind = 3;
+        if (a.deadline_ns && globaltimer() > a.deadline_ns) kind = 3;
+      }
+      if (kind == 0 && !was_idle) {
+        atomicAdd(&Q->idle.v, 1u);
+        was_idle = true;
+      } else if (kind != 0 && was_idle) {
+        atomicSub(&Q->idle.v, 1u);
+        was_idle = false;
       }
     }
-    const Item item = a.items[item_idx];
-    if (item.task == kNone) continue;  // another rank's share
-    const Task task = a.tasks[item.task];
+    kind = __shfl_sync(kFull, kind, 0);
+    ref = __shfl_sync(kFull, ref, 0);
+    if (kind == 3) break;
+    if (kind == 0) {
+      __nanosleep(backoff);
+      if (backoff < 8000) backoff *= 2;
+      continue;
+    }
+    backoff = 500;
+    uint32_t task_id, lstart, rbegin, rend, ncand = 0;
+    if (kind == 1) {
+      const Item item = a.items[ref];
+      task_id = item.task;
+      lstart = 2;
+      rbegin = item.begin;
+      rend = 0;  // set below from the task
+    } else {
+      if (lane == 0)
+        while (ld_volatile(a.dyn_ready + ref) != a.epoch) __nanosleep(64);
+      __syncwarp();
+      __threadfence();
+      // L2-coherent loads (.cg): the slot was written by another SM in this launch
+      const DynItem* it = a.dyn + ref;
+      task_id = __ldcg(&it->task);
+      lstart = __ldcg(&it->level);
+      rbegin = __ldcg(&it->begin);
+      rend = __ldcg(&it->end);
+      ncand = __ldcg(&it->ncand);
+      if (lane < lstart) s_M[w][lane] = __ldcg(&it->M[lane]);
+      if (lane < ncand) s_cand[w][lstart][lane] = __ldcg(&it->cand[lane]);
+    }
+    if (task_id == kNone) {  // another rank's share
+      if (lane == 0) atomicSub(&Q->busy.v, 1u);
+      continue;
+    }
+    const Task task = a.tasks[task_id];
     const EdgeProg& P = a.progs[task.prog];
-    const bdsm_update_dev up = a.ups[task.upd];
     const uint32_t anchor = task.upd;
     const uint32_t n = P.n;
-    const uint32_t m0 = task.flip ? up.v : up.u, m1 = task.flip ? up.u : up.v;
-    if (lane == 0) {
-      s_M[w][0] = m0;
-      s_M[w][1] = m1;
-    }
-    // both anchor endpoints are same-kind batch endpoints by construction
-    r_touch = (lane == 0 || lane == 1) ? 1u : 0u;
-    {
-      uint32_t dpos;
-      uint32_t drv = level2_driver(P, m0, m1, g, &dpos);
-      if (lane == 2) {
-        r_off = g.off[drv];
-        r_cur = item.begin;
-        r_end = min(item.begin + a.chunk, task.d);
-        r_mask = 0;
-        r_drv = P.lv[2].backmask == 3u ? dpos : 0u;  // index into the backward list
+    if (kind == 1) {
+      const bdsm_update_dev up = a.ups[task.upd];
+      const uint32_t m0 = task.flip ? up.v : up.u, m1 = task.flip ? up.u : up.v;
+      if (lane == 0) {
+        s_M[w][0] = m0;
+        s_M[w][1] = m1;
       }
+      rend = min(rbegin + a.chunk, task.d);
     }
     __syncwarp();
-    uint32_t l = 2;
+    // anchor endpoints are same-kind batch endpoints by construction
+    r_touch = lane < 2 ? 1u : (lane < lstart ? (bit_set(a.touched_bits, s_M[w][lane]) ? 1u : 0u) : 0u);
+    {  // driver of the start level: smallest backward list (ties: lower position)
+      const LevelProg& lp = P.lv[lstart];
+      uint32_t best_deg = 0xffffffffu, best_b = 0;
+      for (uint32_t b = 0; b < lp.nback; ++b) {
+        uint32_t d = __ldg(g.deg + s_M[w][lp.back[b]]);
+        if (d < best_deg) {
+          best_deg = d;
+          best_b = b;
+        }
+      }
+      if (lane == lstart) {
+        r_off = __ldg(g.off + s_M[w][lp.back[best_b]]);
+        r_cur = rbegin;
+        r_end = rend;
+        r_mask = 0;
+        r_drv = best_b;
+        r_dlen = best_deg;
+        if (ncand) {  // donated candidate list: no driver fetching at this level
+          r_cur = r_end = 0;
+          r_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
+        }
+      }
+      if (lane < kFloorB) s_floor[w][lstart][lane] = 0;
+    }
+    __syncwarp();
+    uint32_t l = lstart;
     while (true) {
       uint32_t mask = __shfl_sync(kFull, r_mask, l);
       if (mask == 0) {
         const uint32_t cur = __shfl_sync(kFull, r_cur, l);
         const uint32_t end = __shfl_sync(kFull, r_end, l);
         if (cur >= end) {
-          if (l == 2) break;
+          if (l == lstart) break;
           --l;
           continue;
         }
+        // ---- donate work at the shallowest splittable level ---------------
+        // (upper half of the remaining driver range, or of the remaining
+        // candidates of an already-fetched chunk)
+        if (((++dtick) & 7u) == 0 && ld_volatile(&a.q->idle.v) != 0) {
+          uint32_t qlen = ld_volatile(&a.q->dyn_tail.v) - ld_volatile(&a.q->dyn_head.v);
+          if (qlen < ld_volatile(&a.q->idle.v)) {
+            bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= 64;
+            bool can_m = lane >= lstart && lane < l && __popc(r_mask) >= 2;
+            uint32_t cb = __ballot_sync(kFull, can_r || can_m);
+            if (cb) {
+              uint32_t j = __ffs(cb) - 1;
+              bool by_range = (__ballot_sync(kFull, can_r) >> j) & 1u;
+              uint32_t slot = 0;
+              if (lane == 0) slot = dyn_reserve(a.q, a.dyn_cap);
+              slot = __shfl_sync(kFull, slot, 0);
+              if (slot != kNone) {
+                DynItem* it = a.dyn + slot;
+                if (lane < j) it->M[lane] = s_M[w][lane];
+                if (by_range) {
+                  uint32_t cj = __shfl_sync(kFull, r_cur, j), ej = __shfl_sync(kFull, r_end, j);
+                  uint32_t mid = cj + (ej - cj) / 2;
+                  if (lane == j) r_end = mid;
+                  if (lane == 0) {
+                    it->begin = mid;
+                    it->end = ej;
+                    it->ncand = 0;
+                  }
+                } else {
+                  uint32_t mj = __shfl_sync(kFull, r_mask, j);
+                  uint32_t keep_n = (__popc(mj) + 1) / 2, kept = 0, rest = mj;
+                  for (uint32_t k = 0; k < keep_n; ++k) {
+                    uint32_t bit = rest & (~rest + 1u);
+                    kept |= bit;
+                    rest &= ~bit;
+                  }
+                  if (lane == j) r_mask = kept;
+                  // lane k < popc(rest) writes the k-th donated candidate
+                  bool mine = (rest >> lane) & 1u;
+                  uint32_t rank = __popc(rest & ((1u << lane) - 1u));
+                  if (mine) it->cand[rank] = s_cand[w][j][lane];
+                  if (lane == 0) {
+                    it->begin = 0;
+                    it->end = 0;
+                    it->ncand = __popc(rest);
+                  }
+                }
+                if (lane == 0) {
+                  it->task = task_id;
+                  it->level = j;
+                }
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) {
+                  atomicExch(a.dyn_ready + slot, a.epoch);
+                  atomicAdd(&st->donations, 1u);
+                }
+              }
+            }
+          }
+        }
+        const uint32_t end2 = __shfl_sync(kFull, r_end, l);  // may have shrunk
         const uint64_t doff = __shfl_sync(kFull, r_off, l);
         const uint32_t dpos = __shfl_sync(kFull, r_drv, l);
-        const uint32_t touched = __ballot_sync(kFull, r_touch) ;
+        const uint32_t touched = __ballot_sync(kFull, r_touch);
         if (lane == l) r_cur = cur + 32;
         if (a.deadline_ns && ((++tick & 255u) == 0) && globaltimer() > a.deadline_ns) {
           timed_out = true;
@@ -263,8 +472,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         }
         const LevelProg& lp = P.lv[l];
         const uint32_t idx = cur + lane;
-        bool ok = idx < end;
-        uint32_t c = 0;
+        bool ok = idx < end2;
+        uint32_t c = 0xffffffffu;
         if (ok) c = __ldg(g.adj + doff + idx);
         if (ok) ok = (__ldg(a.rows + c) & lp.qbit) != 0;
         if (ok && g.elab) ok = __ldg(g.elab + doff + idx) == lp.elab[dpos];
@@ -279,16 +488,31 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
             }
           }
         }
+        const uint32_t dlen = __shfl_sync(kFull, r_dlen, l);  // driver list length
         for (uint32_t b = 0; b < lp.nback; ++b) {  // other backward lists
           if (b == dpos) continue;
+          if (!__any_sync(kFull, ok)) break;
           const uint32_t x = s_M[w][lp.back[b]];
           const uint64_t xo = __ldg(g.off + x);
           const uint32_t xd = __ldg(g.deg + x);
-          if (ok) {
-            uint32_t p = lb_u32(g.adj + xo, xd, c);
-            ok = p < xd && __ldg(g.adj + xo + p) == c;
-            if (ok && g.elab) ok = __ldg(g.elab + xo + p) == lp.elab[b];
+          uint32_t fl = b < kFloorB ? s_floor[w][l][b] : 0;
+          uint32_t p = 0;
+          bool hit;
+          // comparable lengths: merge windows; skewed: floor-bounded binary search
+          if (uint64_t(xd) <= uint64_t(a.merge_ratio) * dlen) {
+            hit = member_merge(g.adj + xo, xd, fl, c, ok, lane, &p);
+          } else {
+            hit = false;
+            if (ok) {
+              p = fl + lb_u32(g.adj + xo + fl, xd - fl, c);
+              hit = p < xd && __ldg(g.adj + xo + p) == c;
+            }
+            uint32_t mp = __reduce_max_sync(kFull, ok ? p : 0u);
+            if (mp > fl) fl = mp;
           }
+          if (b < kFloorB && lane == 0) s_floor[w][l][b] = min(fl, xd);
+          if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
+          ok = ok && hit;
         }
         if (ok && (touched & lp.backmask) && bit_set(a.touched_bits, c)) {
           uint32_t tb = touched & lp.backmask;
@@ -338,18 +562,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
           r_end = best_deg;
           r_mask = 0;
           r_drv = best_b;
+          r_dlen = best_deg;
         }
+        if (lane < kFloorB) s_floor[w][l][lane] = 0;
         __syncwarp();
       }
     }
+    if (lane == 0) atomicSub(&a.q->busy.v, 1u);
     if (timed_out) break;
   }
   if (lane == 0) {
-    if (count) atomicAdd((unsigned long long*)&a.st->counts[a.phase][a.query], (unsigned long long)count);
-    if (visits) atomicAdd((unsigned long long*)&a.st->visits, (unsigned long long)visits);
-    if (bytes) atomicAdd((unsigned long long*)&a.st->bytes_phase, (unsigned long long)bytes);
-    if (calls) atomicAdd((unsigned long long*)&a.st->gen_calls, (unsigned long long)calls);
-    if (timed_out) atomicOr(&a.st->timed_out, 1u << a.query);
+    if (was_idle) atomicSub(&a.q->idle.v, 1u);
+    if (count) atomicAdd((unsigned long long*)&st->counts[a.phase][a.query], (unsigned long long)count);
+    if (visits) atomicAdd((unsigned long long*)&st->visits, (unsigned long long)visits);
+    if (bytes) atomicAdd((unsigned long long*)&st->bytes_phase, (unsigned long long)bytes);
+    if (calls) atomicAdd((unsigned long long*)&st->gen_calls, (unsigned long long)calls);
+    if (timed_out) atomicOr(&st->timed_out, 1u << a.query);
   }
 }
 
