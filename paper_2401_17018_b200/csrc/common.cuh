@@ -87,12 +87,15 @@ struct alignas(128) PaddedU32 {
   uint32_t v;
   uint32_t pad[31];
 };
+// Ticket queue: an idle warp takes ticket t once and waits on slot t's own
+// ready flag; donors reserve slots from `tail` when tickets > tail (a warp is
+// waiting).  `holders` counts warps working plus donated items not yet
+// finished, so holders == 0 means no work exists or can appear.
 struct QueueState {
   PaddedU32 next_item;  // static work-item head
-  PaddedU32 dyn_head;   // donated-item queue: pop / push counters
-  PaddedU32 dyn_tail;
-  PaddedU32 busy;       // warps holding work
-  PaddedU32 idle;       // warps waiting for donations
+  PaddedU32 tickets;    // tickets handed to idle warps
+  PaddedU32 tail;       // donated slots reserved
+  PaddedU32 holders;
 };
 
 // Device-side batch bookkeeping, copied back once per batch.

@@ -188,28 +188,13 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
-// Donated-subtree queue (bounded, indices only grow within one launch).
+// Donated-subtree ticket queue (slots are used once per launch).  A reserved
+// slot counts as a holder until the warp that takes it finishes.
 __device__ __forceinline__ uint32_t dyn_reserve(QueueState* q, uint32_t cap) {
-  uint32_t t = ld_volatile(&q->dyn_tail.v);
-  while (t < cap) {
-    uint32_t old = atomicCAS(&q->dyn_tail.v, t, t + 1);
-    if (old == t) return t;
-    t = old;
-  }
-  return kNone;
-}
-
-__device__ __forceinline__ bool dyn_pop(QueueState* q, uint32_t* slot) {
-  uint32_t h = ld_volatile(&q->dyn_head.v);
-  while (true) {
-    if (h >= ld_volatile(&q->dyn_tail.v)) return false;
-    uint32_t old = atomicCAS(&q->dyn_head.v, h, h + 1);
-    if (old == h) {
-      *slot = h;
-      return true;
-    }
-    h = old;
-  }
+  uint32_t t = atomicAdd(&q->tail.v, 1u);
+  if (t >= cap) return kNone;  // full: keep the work (tail overshoot is harmless)
+  atomicAdd(&q->holders.v, 1u);
+  return t;
 }
 
 constexpr int kFloorB = 8;  // backward lists per level with a tracked search floor
@@ -268,9 +253,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
   const uint32_t n_items = st->n_items[a.phase];
   const DevGraph& g = a.g;
   uint64_t count = 0, visits = 0, bytes = 0, calls = 0;
-  uint32_t tick = 0, dtick = 0, backoff = 500;
+  uint32_t tick = 0, dtick = 0;
   bool timed_out = false;
-  bool static_done = false, was_idle = false;
+  bool static_done = false;
+  uint32_t ticket = kNone;  // lane 0: outstanding ticket of this warp
 
   // Lane-distributed per-level DFS state: lane l holds level l's.
   uint64_t r_off = 0;   // driver list offset
@@ -286,43 +272,48 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
     uint32_t kind = 0, ref = 0;  // 1 static item, 2 donated item, 3 exit
     QueueState* Q = a.q;
     if (lane == 0) {
-      // `busy` counts warps holding work; only holders push donations, so
-      // "no holder and an empty queue" means the launch is finished.  A warp
-      // between its pop and its increment may make others leave early; it
-      // still completes (and re-pops its own donations), so no work is lost.
+      // Static items first (counted as held before the index is taken, so a
+      // waiter never sees holders == 0 while a static item is in flight).
       if (!static_done) {
+        atomicAdd(&Q->holders.v, 1u);
         uint32_t idx = atomicAdd(&Q->next_item.v, 1u);
         if (idx < n_items) {
           kind = 1;
           ref = idx;
         } else {
           static_done = true;
+          atomicSub(&Q->holders.v, 1u);
         }
       }
-      if (!kind && dyn_pop(Q, &ref)) kind = 2;
-      if (kind) {
-        atomicAdd(&Q->busy.v, 1u);
-      } else {
-        if (ld_volatile(&Q->busy.v) == 0 && ld_volatile(&Q->dyn_head.v) >= ld_volatile(&Q->dyn_tail.v)) kind = 3;
-        if (a.deadline_ns && globaltimer() > a.deadline_ns) kind = 3;
-      }
-      if (kind == 0 && !was_idle) {
-        atomicAdd(&Q->idle.v, 1u);
-        was_idle = true;
-      } else if (kind != 0 && was_idle) {
-        atomicSub(&Q->idle.v, 1u);
-        was_idle = false;
+      if (!kind) {
+        // Donated work: one ticket per idle period, then wait on that slot.
+        if (ticket == kNone) ticket = atomicAdd(&Q->tickets.v, 1u);
+        uint32_t backoff = 128, spins = 0;
+        while (true) {
+          if (ticket < a.dyn_cap && ld_volatile(a.dyn_ready + ticket) == a.epoch) {
+            kind = 2;
+            ref = ticket;
+            ticket = kNone;
+            break;
+          }
+          if ((++spins & 3u) == 0) {
+            if (ld_volatile(&Q->holders.v) == 0) {
+              kind = 3;
+              break;
+            }
+            if (a.deadline_ns && globaltimer() > a.deadline_ns) {
+              kind = 3;
+              break;
+            }
+          }
+          __nanosleep(backoff);
+          if (backoff < 4096) backoff *= 2;
+        }
       }
     }
     kind = __shfl_sync(kFull, kind, 0);
     ref = __shfl_sync(kFull, ref, 0);
     if (kind == 3) break;
-    if (kind == 0) {
-      __nanosleep(backoff);
-      if (backoff < 8000) backoff *= 2;
-      continue;
-    }
-    backoff = 500;
     uint32_t task_id, lstart, rbegin, rend, ncand = 0;
     if (kind == 1) {
       const Item item = a.items[ref];
@@ -331,8 +322,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
       rbegin = item.begin;
       rend = 0;  // set below from the task
     } else {
-      if (lane == 0)
-        while (ld_volatile(a.dyn_ready + ref) != a.epoch) __nanosleep(64);
       __syncwarp();
       __threadfence();
       // L2-coherent loads (.cg): the slot was written by another SM in this launch
@@ -346,7 +335,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
       if (lane < ncand) s_cand[w][lstart][lane] = __ldcg(&it->cand[lane]);
     }
     if (task_id == kNone) {  // another rank's share
-      if (lane == 0) atomicSub(&Q->busy.v, 1u);
+      if (lane == 0) atomicSub(&Q->holders.v, 1u);
       continue;
     }
     const Task task = a.tasks[task_id];
@@ -404,9 +393,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         // ---- donate work at the shallowest splittable level ---------------
         // (upper half of the remaining driver range, or of the remaining
         // candidates of an already-fetched chunk)
-        if (((++dtick) & 7u) == 0 && ld_volatile(&a.q->idle.v) != 0) {
-          uint32_t qlen = ld_volatile(&a.q->dyn_tail.v) - ld_volatile(&a.q->dyn_head.v);
-          if (qlen < ld_volatile(&a.q->idle.v)) {
+        if (((++dtick) & 3u) == 0) {
+          // demand: tickets handed out beyond the slots reserved so far
+          if (int32_t(ld_volatile(&a.q->tickets.v) - ld_volatile(&a.q->tail.v)) > 0) {
             bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= 64;
             bool can_m = lane >= lstart && lane < l && __popc(r_mask) >= 2;
             uint32_t cb = __ballot_sync(kFull, can_r || can_m);
@@ -568,11 +557,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         __syncwarp();
       }
     }
-    if (lane == 0) atomicSub(&a.q->busy.v, 1u);
+    if (lane == 0) atomicSub(&a.q->holders.v, 1u);
     if (timed_out) break;
   }
   if (lane == 0) {
-    if (was_idle) atomicSub(&a.q->idle.v, 1u);
     if (count) atomicAdd((unsigned long long*)&st->counts[a.phase][a.query], (unsigned long long)count);
     if (visits) atomicAdd((unsigned long long*)&st->visits, (unsigned long long)visits);
     if (bytes) atomicAdd((unsigned long long*)&st->bytes_phase, (unsigned long long)bytes);
