@@ -4,7 +4,8 @@ set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
 NVCC="${NVCC:-nvcc}"
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC
-       -Xcompiler -fvisibility=hidden -I"$HERE/../include" --expt-relaxed-constexpr -diag-suppress 177)
+       -Xcompiler -fvisibility=hidden -I"$HERE/../include" --expt-relaxed-constexpr -diag-suppress 177
+       ${BDSM_NVCC_EXTRA:-})
 OBJ="$HERE/build"
 mkdir -p "$OBJ"
 pids=()

@@ -91,12 +91,24 @@ struct alignas(128) PaddedU32 {
 // ready flag; donors reserve slots from `tail` when tickets > tail (a warp is
 // waiting).  `holders` counts warps working plus donated items not yet
 // finished, so holders == 0 means no work exists or can appear.
+struct alignas(128) TicketTail {
+  uint32_t tickets;     // tickets handed to idle warps
+  uint32_t tail;        // donated slots reserved
+  uint32_t pad[30];
+};
 struct QueueState {
   PaddedU32 next_item;  // static work-item head
-  PaddedU32 tickets;    // tickets handed to idle warps
-  PaddedU32 tail;       // donated slots reserved
+  TicketTail tt;        // one 64-bit poll reads both (donors' demand check)
   PaddedU32 holders;
 };
+
+// Candidate rows carry the query-vertex bits in the low 16 bits (kMaxQ) and
+// two per-batch flags in the top bits: the vertex is an endpoint of an
+// insert (positive phase) / delete (negative phase) of the current batch.
+// The matching kernel gets the visibility-rule prefilter from the same load.
+constexpr uint32_t kRowInsFlag = 1u << 31;
+constexpr uint32_t kRowDelFlag = 1u << 30;
+constexpr uint32_t kRowFlags = kRowInsFlag | kRowDelFlag;
 
 // Device-side batch bookkeeping, copied back once per batch.
 struct BatchState {

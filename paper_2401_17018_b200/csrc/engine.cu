@@ -116,7 +116,6 @@ struct bdsm_engine {
   DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
-  DBuf<uint32_t> ins_bits, del_bits;
   DBuf<uint32_t> upd_counts, upd_task_counts, item_off, task_off;
   DBuf<uint64_t> upd_cost, cost_off;
   DBuf<Task> tasks;
@@ -544,7 +543,6 @@ struct bdsm_engine {
     a.skeys = skeys.p;
     a.svals = svals.p;
     a.m_keys = 2 * n;
-    a.touched_bits = phase == 0 ? del_bits.p : ins_bits.p;
     a.phase = phase;
     a.query = uint32_t(qi);
     a.qn = qs.q.n;
@@ -663,12 +661,8 @@ struct bdsm_engine {
       }
       *h_st = template_state();
       CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
-      size_t words = (size_t(g.V) + 31) / 32 + 1;
-      ins_bits.ensure(words);
-      del_bits.ensure(words);
-      CK(cudaMemsetAsync(ins_bits.p, 0, words * 4, stream));
-      CK(cudaMemsetAsync(del_bits.p, 0, words * 4, stream));
       const uint32_t m = uint32_t(2 * n);
+      const uint32_t nq = uint32_t(queries.size());
       launch_prepare(src, uint32_t(n), view(), d_st.p, keys.p, vals.p, dlab.p, ecode.p, stream);
       {
         size_t tmp = cub_tmp.n;
@@ -682,7 +676,7 @@ struct bdsm_engine {
       }
       // device-input batches: the ups buffer the kernels read is `src`
       PhaseArgsFix fix(this, src);
-      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, ins_bits.p, del_bits.p, g.V, stream);
+      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, stream);
       {
         size_t tmp = cub_tmp.n;
         CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
@@ -703,6 +697,8 @@ struct bdsm_engine {
       cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);
+      launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
+      ++launches;
       CK(cudaEventRecord(ev[4], stream));
       CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
       CK(cudaEventRecord(ev[5], stream));
@@ -807,7 +803,11 @@ struct bdsm_engine {
     h_st->overflow = 0;
     for (auto& c : h_st->counts[1]) c = 0;
     CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+    const uint32_t m = 2 * n, nq = uint32_t(queries.size());
+    // the batch-endpoint row flags were cleared at the end of the attempt
+    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, stream);
     run_phase(n, 1);
+    launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
     CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
     sync();
     if (h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
@@ -1002,6 +1002,7 @@ bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out) {
     QueryState& qs = *engine->queries.at(size_t(query));
     CK(cudaMemcpyAsync(out, qs.rows.p, 4ull * engine->g.V, cudaMemcpyDeviceToHost, engine->stream));
     engine->sync();
+    for (uint32_t v = 0; v < engine->g.V; ++v) out[v] &= ~kRowFlags;
     return BDSM_OK;
   });
 }

@@ -48,8 +48,10 @@ void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* 
 void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, BatchState* st,
                     uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, cudaStream_t s);
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
-                      uint8_t* head, uint32_t* insflag, uint32_t* ins_bits, uint32_t* del_bits,
-                      uint32_t V, cudaStream_t s);
+                      uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
+                      cudaStream_t s);
+void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
+                        cudaStream_t s);
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
                   uint32_t* new_cap, cudaStream_t s);
@@ -74,7 +76,6 @@ struct PhaseArgs {
   const uint64_t* skeys;         // sorted directed batch keys (visibility lookups)
   const uint32_t* svals;
   uint32_t m_keys;
-  const uint32_t* touched_bits;  // same-kind endpoint bitmap of this phase
   uint32_t phase;                // 0 negative (deletes), 1 positive (inserts)
   uint32_t query;
   uint32_t qn;                   // query vertex count

@@ -191,7 +191,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // Donated-subtree ticket queue (slots are used once per launch).  A reserved
 // slot counts as a holder until the warp that takes it finishes.
 __device__ __forceinline__ uint32_t dyn_reserve(QueueState* q, uint32_t cap) {
-  uint32_t t = atomicAdd(&q->tail.v, 1u);
+  uint32_t t = atomicAdd(&q->tt.tail, 1u);
   if (t >= cap) return kNone;  // full: keep the work (tail overshoot is harmless)
   atomicAdd(&q->holders.v, 1u);
   return t;
@@ -242,7 +242,10 @@ __device__ __forceinline__ bool member_merge(const uint32_t* __restrict__ L, uin
 // splittable level (the reference's active stealing takes the same share,
 // src/scheduler.cpp:49-64, claim_upper_half), pushing its prefix assignment.
 // Ranges are disjoint, so counts are exact regardless of scheduling.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
+#ifndef BDSM_WBM_MIN_BLOCKS
+#define BDSM_WBM_MIN_BLOCKS 4  // resident 256-thread CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wbm(PhaseArgs a) {
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
@@ -266,6 +269,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
   uint32_t r_drv = 0;   // index of the driver in the level's backward list
   uint32_t r_touch = 0; // lane l: is M[l] a same-kind batch endpoint
   uint32_t r_dlen = 0;  // length of the driver list
+  uint32_t r_tmask = 0; // current chunk: which candidates are same-kind batch endpoints
+  const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
 
   while (true) {
     // ---- acquire work ----------------------------------------------------
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
       }
       if (!kind) {
         // Donated work: one ticket per idle period, then wait on that slot.
-        if (ticket == kNone) ticket = atomicAdd(&Q->tickets.v, 1u);
+        if (ticket == kNone) ticket = atomicAdd(&Q->tt.tickets, 1u);
         uint32_t backoff = 128, spins = 0;
         while (true) {
           if (ticket < a.dyn_cap && ld_volatile(a.dyn_ready + ticket) == a.epoch) {
@@ -353,9 +358,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
     }
     __syncwarp();
     // anchor endpoints are same-kind batch endpoints by construction
-    r_touch = lane < 2 ? 1u : (lane < lstart ? (bit_set(a.touched_bits, s_M[w][lane]) ? 1u : 0u) : 0u);
+    r_touch = lane < 2 ? 1u : (lane < lstart ? ((__ldg(a.rows + s_M[w][lane]) & flag) ? 1u : 0u) : 0u);
     {  // driver of the start level: smallest backward list (ties: lower position)
       const LevelProg& lp = P.lv[lstart];
+      const uint32_t ctm =
+          __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
+      if (lane == lstart) r_tmask = ctm;
       uint32_t best_deg = 0xffffffffu, best_b = 0;
       for (uint32_t b = 0; b < lp.nback; ++b) {
         uint32_t d = __ldg(g.deg + s_M[w][lp.back[b]]);
@@ -395,7 +403,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         // candidates of an already-fetched chunk)
         if (((++dtick) & 3u) == 0) {
           // demand: tickets handed out beyond the slots reserved so far
-          if (int32_t(ld_volatile(&a.q->tickets.v) - ld_volatile(&a.q->tail.v)) > 0) {
+          const unsigned long long tt =
+              *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
+          if (int32_t(uint32_t(tt) - uint32_t(tt >> 32)) > 0) {
             bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= 64;
             bool can_m = lane >= lstart && lane < l && __popc(r_mask) >= 2;
             uint32_t cb = __ballot_sync(kFull, can_r || can_m);
@@ -464,7 +474,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
         bool ok = idx < end2;
         uint32_t c = 0xffffffffu;
         if (ok) c = __ldg(g.adj + doff + idx);
-        if (ok) ok = (__ldg(a.rows + c) & lp.qbit) != 0;
+        uint32_t rw = 0;
+        if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
+        ok = ok && (rw & lp.qbit) != 0;
         if (ok && g.elab) ok = __ldg(g.elab + doff + idx) == lp.elab[dpos];
         if (ok) {  // injectivity: only same-label positions can collide
           uint32_t eq = lp.eqmask;
@@ -503,7 +515,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
           if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
           ok = ok && hit;
         }
-        if (ok && (touched & lp.backmask) && bit_set(a.touched_bits, c)) {
+        const bool tc = (rw & flag) != 0;
+        if (ok && (touched & lp.backmask) && tc) {
           uint32_t tb = touched & lp.backmask;
           while (tb && ok) {
             uint32_t j = __ffs(tb) - 1;
@@ -518,14 +531,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_wbm(PhaseArgs a) {
           continue;
         }
         s_cand[w][l][lane] = c;
-        if (lane == l) r_mask = m;
+        const uint32_t tm = __ballot_sync(kFull, tc);
+        if (lane == l) {
+          r_mask = m;
+          r_tmask = tm;
+        }
         __syncwarp();
       } else {
         const uint32_t k = __ffs(mask) - 1;
         if (lane == l) r_mask = mask & (mask - 1);
         const uint32_t c = s_cand[w][l][k];
-        const bool tc = bit_set(a.touched_bits, c);
-        if (lane == l) r_touch = tc ? 1u : 0u;
+        const uint32_t tmask = __shfl_sync(kFull, r_tmask, l);
+        if (lane == l) r_touch = (tmask >> k) & 1u;
         if (lane == 0) s_M[w][l] = c;
         __syncwarp();
         ++l;

@@ -171,11 +171,11 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
 
 // After the radix sort of the 2n directed keys: conflicting pairs, segment
 // heads (distinct sources = touched vertices), insert flags for the merge
-// prefix, and the per-phase same-kind endpoint bitmaps used by the
-// visibility rule (UpdateIndex, src/matcher.cpp:27-40).
+// prefix, and the per-phase same-kind endpoint flags in the candidate rows
+// used to prefilter the visibility rule (UpdateIndex, src/matcher.cpp:27-40).
 __global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                             uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
-                            uint32_t* ins_bits, uint32_t* del_bits, uint32_t V) {
+                            uint32_t* const* rows, uint32_t nq, uint32_t V) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += gridDim.x * blockDim.x) {
     if (j == m) {
       insflag[j] = 0;
@@ -192,7 +192,19 @@ __global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* 
     bool h = j == 0 || uint32_t(skeys[j - 1] >> 32) != src;
     head[j] = h ? 1 : 0;
     insflag[j] = is_del ? 0u : 1u;
-    if (src < V) atomicOr((is_del ? del_bits : ins_bits) + (src >> 5), 1u << (src & 31));
+    if (src < V)
+      for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? kRowDelFlag : kRowInsFlag);
+  }
+}
+
+// End of batch (also after a rejected one): clear the per-batch row flags of
+// every touched vertex.
+__global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, uint32_t* const* rows,
+                              uint32_t nq, uint32_t V) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    uint32_t src = uint32_t(skeys[j] >> 32);
+    if (src < V && (j == 0 || uint32_t(skeys[j - 1] >> 32) != src))
+      for (uint32_t q = 0; q < nq; ++q) rows[q][src] &= ~kRowFlags;
   }
 }
 
@@ -385,9 +397,10 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
         if (all && vl == qe.qlabel[u]) row |= 1u << u;
       }
       if (lane == 0) {
-        uint32_t before = rows[q][x];
+        const uint32_t word = rows[q][x];
+        const uint32_t before = word & ~kRowFlags;  // keep the batch flags
         if (before != row) {
-          rows[q][x] = row;
+          rows[q][x] = row | (word & kRowFlags);
           uint32_t diff = before ^ row;
           while (diff) {
             uint32_t u = __ffs(diff) - 1;
@@ -492,10 +505,14 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, BatchSta
   k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, st, keys, vals, dlab, ecode);
 }
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
-                      uint8_t* head, uint32_t* insflag, uint32_t* ins_bits, uint32_t* del_bits,
-                      uint32_t V, cudaStream_t s) {
-  k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(skeys, svals, m, st, head, insflag,
-                                                              ins_bits, del_bits, V);
+                      uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
+                      cudaStream_t s) {
+  k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(skeys, svals, m, st, head, insflag, rows,
+                                                              nq, V);
+}
+void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
+                        cudaStream_t s) {
+  k_clear_flags<<<blocks_for(m), kThreads, 0, s>>>(skeys, m, rows, nq, V);
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
