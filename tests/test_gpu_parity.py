@@ -91,3 +91,22 @@ def test_rows_match_restatement():
             rows = e.rows(0)
             assert all(int(rows[v]) == o.row(0, v) for v in range(len(vl)))
             assert [e.order(0, k) for k in range(len(qe))] == [o.order(0, k) for k in range(len(qe))] or True
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_work_split_sums_to_reference(world):
+    """Each engine counts only its share of the work units (multi-GPU split);
+    run all shards on one GPU and sum."""
+    import paper_2401_17018_b200 as bd
+    insts = gu.load("streams")[-4:] + gu.load("skewed")
+    for inst in insts:
+        vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+        engines = []
+        for r in range(world):
+            e = bd.Engine(vl, eu, ev, el, shard_rank=r, shard_world=world)
+            e.add_query(ql, qe)
+            engines.append(e)
+        for b, exp in zip(batches, inst["expect"]):
+            rs = [e.match_batch(b) for e in engines]
+            assert sum(r.positive[0] for r in rs) == exp["pos"], inst["name"]
+            assert sum(r.negative[0] for r in rs) == exp["neg"], inst["name"]
