@@ -31,6 +31,7 @@ struct DevGraph {
 // the query-edge label of each backward edge.  Built by the host planner.
 struct LevelProg {
   uint32_t qbit;                 // 1 << order[l] (candidate-row bit)
+  uint32_t vlo, vhi;             // internal-id range of label(order[l]) (ids are label-ordered)
   uint32_t backmask;             // positions j < l adjacent to order[l]
   uint32_t eqmask;               // positions j < l with label(order[j]) == label(order[l])
   uint32_t nback;
@@ -57,7 +58,8 @@ struct Task {
   uint32_t upd;
   uint32_t prog;
   uint32_t flip;
-  uint32_t d;                    // level-2 driver length (0 for 2-vertex queries)
+  uint32_t d;                    // level-2 driver range length (0 for 2-vertex queries)
+  uint32_t base;                 // start of that range in the driver list (label sub-range)
 };
 
 // One work unit: a chunk [begin, begin + chunk) of a task's level-2 driver.

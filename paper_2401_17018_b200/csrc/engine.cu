@@ -111,7 +111,8 @@ struct bdsm_engine {
   DBuf<uint64_t*> d_colsize;
 
   // batch buffers
-  DBuf<bdsm_update_dev> ups;
+  DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
+  DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
   DBuf<uint64_t> keys, skeys;
   DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap;
   DBuf<uint8_t> ecode, head;
@@ -173,11 +174,62 @@ struct bdsm_engine {
   void sync() { CK(cudaStreamSynchronize(stream)); }
 
   // ---------------------------------------------------------------- build --
+  // Internal vertex ids are ordered by (label, external id): every label class
+  // is one contiguous id range, so the label-L neighbours of any vertex form a
+  // contiguous sub-range of its sorted list (used by the matching kernel to
+  // shrink drivers and searches).  The C ABI speaks external ids only.
+  std::vector<uint32_t> new_of, old_of;           // external -> internal, internal -> external
+  std::vector<std::pair<uint32_t, std::pair<uint32_t, uint32_t>>> label_ranges;  // label -> [lo, hi)
+  DBuf<uint32_t> d_new_of;
+  const bdsm_graph_desc* orig_desc = nullptr;
+
   void build(const bdsm_graph_desc* d) {
     const uint32_t V = d->num_vertices;
     const uint64_t E = d->num_edges;
     if (E && (!d->src || !d->dst)) throw std::invalid_argument("edge arrays are null");
     if (V && !d->vertex_labels) throw std::invalid_argument("vertex labels are null");
+    orig_desc = d;
+    std::vector<uint64_t> key(V);
+    for (uint32_t v = 0; v < V; ++v) key[v] = (uint64_t(d->vertex_labels[v]) << 32) | v;
+    std::sort(key.begin(), key.end());
+    new_of.assign(V, 0);
+    old_of.assign(V, 0);
+    std::vector<uint32_t> lab(V);
+    label_ranges.clear();
+    for (uint32_t i = 0; i < V; ++i) {
+      uint32_t v = uint32_t(key[i]), l = uint32_t(key[i] >> 32);
+      old_of[i] = v;
+      new_of[v] = i;
+      lab[i] = l;
+      if (label_ranges.empty() || label_ranges.back().first != l) label_ranges.push_back({l, {i, i}});
+      label_ranges.back().second.second = i + 1;
+    }
+    key.clear();
+    key.shrink_to_fit();
+    std::vector<uint32_t> src(E), dst(E);
+    for (uint64_t i = 0; i < E; ++i) {
+      uint32_t u = d->src[i], v = d->dst[i];
+      if (u >= V || v >= V) throw_build_error(d, 2);
+      src[i] = new_of[u];
+      dst[i] = new_of[v];
+    }
+    bdsm_graph_desc internal{V, lab.data(), E, src.data(), dst.data(), d->edge_labels};
+    d_new_of.ensure(std::max<uint32_t>(V, 1));
+    if (V) CK(cudaMemcpyAsync(d_new_of.p, new_of.data(), 4ull * V, cudaMemcpyHostToDevice, stream));
+    build_internal(&internal);
+    orig_desc = nullptr;
+  }
+
+  std::pair<uint32_t, uint32_t> label_range(uint32_t label) const {
+    auto it = std::lower_bound(label_ranges.begin(), label_ranges.end(), label,
+                               [](const auto& e, uint32_t l) { return e.first < l; });
+    if (it == label_ranges.end() || it->first != label) return {0, 0};
+    return it->second;
+  }
+
+  void build_internal(const bdsm_graph_desc* d) {
+    const uint32_t V = d->num_vertices;
+    const uint64_t E = d->num_edges;
     g.V = V;
     n_edges = E;
     has_elab = false;
@@ -233,7 +285,7 @@ struct bdsm_engine {
       uint32_t hbad = 0;
       CK(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, stream));
       sync();
-      if (hbad) throw_build_error(d, hbad);
+      if (hbad) throw_build_error(orig_desc ? orig_desc : d, hbad);
       launch_degrees(sk, M, deg.p, stream);
       // capacities -> offsets; dense offsets for the scatter
       cap64.ensure(V);
@@ -426,9 +478,11 @@ struct bdsm_engine {
     qs.orders.clear();
     std::vector<EdgeProg> progs;
     std::vector<AnchorEdge> anchors;
+    std::vector<std::pair<uint32_t, uint32_t>> ranges(qs.q.n);
+    for (uint32_t u = 0; u < qs.q.n; ++u) ranges[u] = label_range(qs.q.labels[u]);
     for (uint32_t e = 0; e < qs.q.edges.size(); ++e) {
       qs.orders.push_back(matching_order(qs.q, e, cs));
-      progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back()));
+      progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back(), ranges));
       const QEdge& qe = qs.q.edges[e];
       anchors.push_back({qs.q.labels[qe.a], qs.q.labels[qe.b], qe.label, e});
     }
@@ -482,6 +536,7 @@ struct bdsm_engine {
     cap_n = std::max<size_t>(cap_n, 1024);
     size_t m = 2 * cap_n;
     ups.ensure(cap_n);
+    ups_ext.ensure(cap_n);
     keys.ensure(m);
     skeys.ensure(m);
     vals.ensure(m);
@@ -646,7 +701,7 @@ struct bdsm_engine {
     } else {
       ensure_host_ups(n);
       std::memcpy(h_ups, updates, n * sizeof(bdsm_update));
-      src = ups.p;
+      src = ups_ext.p;
     }
     uint32_t compactions = 0;
     for (int attempt = 0;; ++attempt) {
@@ -656,14 +711,15 @@ struct bdsm_engine {
       cub_calls = 0;
       CK(cudaEventRecord(ev[0], stream));
       if (!device_input) {
-        CK(cudaMemcpyAsync(ups.p, h_ups, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(ups_ext.p, h_ups, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
         st.h2d_bytes = n * sizeof(bdsm_update);
       }
       *h_st = template_state();
       CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
       const uint32_t m = uint32_t(2 * n);
       const uint32_t nq = uint32_t(queries.size());
-      launch_prepare(src, uint32_t(n), view(), d_st.p, keys.p, vals.p, dlab.p, ecode.p, stream);
+      launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
+                     stream);
       {
         size_t tmp = cub_tmp.n;
         cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
@@ -675,7 +731,6 @@ struct bdsm_engine {
           CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
       }
       // device-input batches: the ups buffer the kernels read is `src`
-      PhaseArgsFix fix(this, src);
       launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, stream);
       {
         size_t tmp = cub_tmp.n;
@@ -690,7 +745,7 @@ struct bdsm_engine {
       cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
       CK(cudaEventRecord(m0, stream));
       launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, stream);
-      launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, src, g, new_off.p, new_cap.p, ipos.p,
+      launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, num_sms, stream);
       CK(cudaEventRecord(m1, stream));
       launches += 4;  // prepare, post_sort, alloc, merge_refresh
@@ -799,7 +854,7 @@ struct bdsm_engine {
   };
 
   void rerun_positive(uint32_t n, const bdsm_update_dev* src) {
-    PhaseArgsFix fix(this, src);
+    (void)src;
     h_st->overflow = 0;
     for (auto& c : h_st->counts[1]) c = 0;
     CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
@@ -979,16 +1034,20 @@ size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, siz
   size_t d = 0;
   guarded([&]() -> bdsm_status {
     CK(cudaSetDevice(engine->device));
+    const uint32_t iv = engine->new_of[v];
     uint32_t dv = 0;
     uint64_t o = 0;
-    CK(cudaMemcpyAsync(&dv, engine->deg.p + v, 4, cudaMemcpyDeviceToHost, engine->stream));
-    CK(cudaMemcpyAsync(&o, engine->off.p + v, 8, cudaMemcpyDeviceToHost, engine->stream));
+    CK(cudaMemcpyAsync(&dv, engine->deg.p + iv, 4, cudaMemcpyDeviceToHost, engine->stream));
+    CK(cudaMemcpyAsync(&o, engine->off.p + iv, 8, cudaMemcpyDeviceToHost, engine->stream));
     engine->sync();
     d = dv;
     if (out && cap) {
-      CK(cudaMemcpyAsync(out, engine->adj.p + o, 4 * std::min<size_t>(cap, dv), cudaMemcpyDeviceToHost,
-                         engine->stream));
+      std::vector<uint32_t> lst(dv);
+      CK(cudaMemcpyAsync(lst.data(), engine->adj.p + o, 4ull * dv, cudaMemcpyDeviceToHost, engine->stream));
       engine->sync();
+      for (auto& x : lst) x = engine->old_of[x];  // external ids, ascending (LabeledGraph::neighbors)
+      std::sort(lst.begin(), lst.end());
+      std::copy(lst.begin(), lst.begin() + std::min<size_t>(cap, dv), out);
     }
     return BDSM_OK;
   });
@@ -1000,9 +1059,10 @@ bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out) {
   return guarded([&]() -> bdsm_status {
     CK(cudaSetDevice(engine->device));
     QueryState& qs = *engine->queries.at(size_t(query));
-    CK(cudaMemcpyAsync(out, qs.rows.p, 4ull * engine->g.V, cudaMemcpyDeviceToHost, engine->stream));
+    std::vector<uint32_t> rows(engine->g.V);
+    CK(cudaMemcpyAsync(rows.data(), qs.rows.p, 4ull * engine->g.V, cudaMemcpyDeviceToHost, engine->stream));
     engine->sync();
-    for (uint32_t v = 0; v < engine->g.V; ++v) out[v] &= ~kRowFlags;
+    for (uint32_t v = 0; v < engine->g.V; ++v) out[v] = rows[engine->new_of[v]] & ~kRowFlags;
     return BDSM_OK;
   });
 }

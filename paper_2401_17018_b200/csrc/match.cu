@@ -68,10 +68,19 @@ __device__ __forceinline__ uint32_t level2_driver(const EdgeProg& p, uint32_t m0
   return b0 ? m0 : m1;
 }
 
-struct AnchorCounts {
-  uint32_t tasks, items;
-  uint64_t cost;
-};
+// Level-2 driver range of an anchor: the sub-range of the driver list holding
+// order[2]'s label (ids are label-ordered, so it is contiguous).
+__device__ __forceinline__ void level2_range(const EdgeProg& p, uint32_t m0, uint32_t m1, const DevGraph& g,
+                                             uint32_t* base, uint32_t* len) {
+  uint32_t pos;
+  const uint32_t drv = level2_driver(p, m0, m1, g, &pos);
+  const uint32_t* lst = g.adj + g.off[drv];
+  const uint32_t d = g.deg[drv];
+  const uint32_t lo = lb_u32(lst, d, p.lv[2].vlo);
+  const uint32_t hi = p.lv[2].vhi > p.lv[2].vlo ? lb_u32(lst, d, p.lv[2].vhi) : lo;
+  *base = lo;
+  *len = hi - lo;
+}
 
 // Visits every anchor of update i in canonical order.
 template <typename F>
@@ -101,8 +110,8 @@ __global__ void k_anchor_count(PhaseArgs a) {
           return;
         }
         const EdgeProg& p = a.progs[prog];
-        uint32_t m0 = flip ? up.v : up.u, m1 = flip ? up.u : up.v, pos;
-        uint32_t d = a.g.deg[level2_driver(p, m0, m1, a.g, &pos)];
+        uint32_t m0 = flip ? up.v : up.u, m1 = flip ? up.u : up.v, base, d;
+        level2_range(p, m0, m1, a.g, &base, &d);
         ni += (d + a.chunk - 1) / a.chunk;
         cost += d;
       });
@@ -133,14 +142,14 @@ __global__ void k_anchor_emit(PhaseArgs a) {
       if (a.qn <= 2) {
         uint32_t owner = a.shard_world > 1 ? uint32_t((unsigned __int128)c * a.shard_world / total_cost) : 0;
         if (owner == a.shard_rank) ++direct;
-        a.tasks[t++] = Task{i, prog, flip, 0};
+        a.tasks[t++] = Task{i, prog, flip, 0, 0};
         c += 1;
         return;
       }
       const EdgeProg& p = a.progs[prog];
-      uint32_t m0 = flip ? up.v : up.u, m1 = flip ? up.u : up.v, pos;
-      uint32_t d = a.g.deg[level2_driver(p, m0, m1, a.g, &pos)];
-      a.tasks[t] = Task{i, prog, flip, d};
+      uint32_t m0 = flip ? up.v : up.u, m1 = flip ? up.u : up.v, base, d;
+      level2_range(p, m0, m1, a.g, &base, &d);
+      a.tasks[t] = Task{i, prog, flip, d, base};
       // level-2 GenCandidates call of this anchor (SURVEY.md §8(d) B_phase)
       uint32_t bm = p.lv[2].backmask;
       if (bm & 1u) bytes += 4ull * a.g.deg[m0];
@@ -242,6 +251,52 @@ __device__ __forceinline__ bool member_merge(const uint32_t* __restrict__ L, uin
 // splittable level (the reference's active stealing takes the same share,
 // src/scheduler.cpp:49-64, claim_upper_half), pushing its prefix assignment.
 // Ranges are disjoint, so counts are exact regardless of scheduling.
+// GenCandidates setup for a level (warp-collective): the driver is the
+// smallest backward list (ties: lower position, as the reference's order of
+// intersection does not matter for the result); every backward list's label
+// sub-range [lo, hi) of label(order[l]) is found by one parallel round of
+// binary searches (lanes 2b / 2b+1), lists of <= 32 entries keep their whole
+// extent (the candidate-row label test filters them).  The sub-ranges seed the
+// membership-search floors / ceilings.
+struct LevelSetup {
+  uint64_t drv_off;
+  uint32_t drv_b, lo, hi, deg_sum;
+};
+
+__device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const DevGraph& g, const uint32_t* M,
+                                                  uint32_t lane, uint32_t* floor_l, uint32_t* ceil_l) {
+  const uint32_t nb = lp.nback;
+  uint32_t myd = 0xffffffffu;
+  uint64_t myo = 0;
+  if (lane < nb) {
+    const uint32_t x = M[lp.back[lane]];
+    myd = __ldg(g.deg + x);
+    myo = __ldg(g.off + x);
+  }
+  const uint32_t mn = __reduce_min_sync(kFull, myd);
+  LevelSetup s;
+  s.drv_b = __ffs(__ballot_sync(kFull, myd == mn)) - 1;
+  s.deg_sum = __reduce_add_sync(kFull, lane < nb ? myd : 0u);
+  const uint32_t lb_list = (lane >> 1) & 31;
+  const uint32_t bd = __shfl_sync(kFull, myd, lb_list);
+  const uint64_t bo = __shfl_sync(kFull, myo, lb_list);
+  uint32_t bnd = 0;
+  if (lane < 2 * nb) {
+    if (bd <= 32) bnd = (lane & 1) ? bd : 0u;
+    else bnd = lb_u32(g.adj + bo, bd, (lane & 1) ? lp.vhi : lp.vlo);
+  }
+  const uint32_t f = __shfl_sync(kFull, bnd, (2 * lane) & 31);
+  const uint32_t c = __shfl_sync(kFull, bnd, (2 * lane + 1) & 31);
+  if (lane < nb && lane < kFloorB) {
+    floor_l[lane] = f;
+    ceil_l[lane] = c;
+  }
+  s.lo = __shfl_sync(kFull, bnd, 2 * s.drv_b);
+  s.hi = __shfl_sync(kFull, bnd, 2 * s.drv_b + 1);
+  s.drv_off = __shfl_sync(kFull, myo, s.drv_b);
+  return s;
+}
+
 #ifndef BDSM_WBM_MIN_BLOCKS
 #define BDSM_WBM_MIN_BLOCKS 4  // resident 256-thread CTAs per SM the register budget must allow
 #endif
@@ -249,6 +304,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
+  __shared__ uint32_t s_ceil[kWarpsPerBlock][kMaxQ][kFloorB];
   if (batch_aborted(a.st)) return;
   BatchState* st = a.st;
   const uint32_t lane = threadIdx.x & 31;
@@ -354,37 +410,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         s_M[w][0] = m0;
         s_M[w][1] = m1;
       }
-      rend = min(rbegin + a.chunk, task.d);
+      rend = task.base + min(rbegin + a.chunk, task.d);
+      rbegin = task.base + rbegin;
     }
     __syncwarp();
     // anchor endpoints are same-kind batch endpoints by construction
     r_touch = lane < 2 ? 1u : (lane < lstart ? ((__ldg(a.rows + s_M[w][lane]) & flag) ? 1u : 0u) : 0u);
-    {  // driver of the start level: smallest backward list (ties: lower position)
+    {  // start level: the item gives the driver range (or a candidate list)
       const LevelProg& lp = P.lv[lstart];
       const uint32_t ctm =
           __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
       if (lane == lstart) r_tmask = ctm;
-      uint32_t best_deg = 0xffffffffu, best_b = 0;
-      for (uint32_t b = 0; b < lp.nback; ++b) {
-        uint32_t d = __ldg(g.deg + s_M[w][lp.back[b]]);
-        if (d < best_deg) {
-          best_deg = d;
-          best_b = b;
-        }
-      }
+      const LevelSetup su = setup_level(lp, g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart]);
       if (lane == lstart) {
-        r_off = __ldg(g.off + s_M[w][lp.back[best_b]]);
+        r_off = su.drv_off;
         r_cur = rbegin;
         r_end = rend;
         r_mask = 0;
-        r_drv = best_b;
-        r_dlen = best_deg;
+        r_drv = su.drv_b;
+        r_dlen = rend > rbegin ? rend - rbegin : 0;
         if (ncand) {  // donated candidate list: no driver fetching at this level
           r_cur = r_end = 0;
           r_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
         }
       }
-      if (lane < kFloorB) s_floor[w][lstart][lane] = 0;
     }
     __syncwarp();
     uint32_t l = lstart;
@@ -489,29 +538,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
             }
           }
         }
-        const uint32_t dlen = __shfl_sync(kFull, r_dlen, l);  // driver list length
+        const uint32_t remain = end2 - cur;  // driver entries left in this range
         for (uint32_t b = 0; b < lp.nback; ++b) {  // other backward lists
           if (b == dpos) continue;
           if (!__any_sync(kFull, ok)) break;
           const uint32_t x = s_M[w][lp.back[b]];
           const uint64_t xo = __ldg(g.off + x);
           const uint32_t xd = __ldg(g.deg + x);
+          // search window: label sub-range [floor, ceil), the floor advancing
+          // with the (ascending) driver chunks
           uint32_t fl = b < kFloorB ? s_floor[w][l][b] : 0;
+          const uint32_t ce = b < kFloorB ? s_ceil[w][l][b] : xd;
           uint32_t p = 0;
           bool hit;
           // comparable lengths: merge windows; skewed: floor-bounded binary search
-          if (uint64_t(xd) <= uint64_t(a.merge_ratio) * dlen) {
-            hit = member_merge(g.adj + xo, xd, fl, c, ok, lane, &p);
+          if (uint64_t(ce - min(fl, ce)) <= uint64_t(a.merge_ratio) * remain) {
+            hit = member_merge(g.adj + xo, ce, fl, c, ok, lane, &p);
           } else {
             hit = false;
             if (ok) {
-              p = fl + lb_u32(g.adj + xo + fl, xd - fl, c);
-              hit = p < xd && __ldg(g.adj + xo + p) == c;
+              p = fl + lb_u32(g.adj + xo + fl, ce - fl, c);
+              hit = p < ce && __ldg(g.adj + xo + p) == c;
             }
             uint32_t mp = __reduce_max_sync(kFull, ok ? p : 0u);
             if (mp > fl) fl = mp;
           }
-          if (b < kFloorB && lane == 0) s_floor[w][l][b] = min(fl, xd);
+          if (b < kFloorB && lane == 0) s_floor[w][l][b] = min(fl, ce);
           if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
           ok = ok && hit;
         }
@@ -546,31 +598,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         if (lane == 0) s_M[w][l] = c;
         __syncwarp();
         ++l;
-        // GenCandidates for level l: driver = smallest backward list
-        const LevelProg& lp = P.lv[l];
-        uint32_t best_deg = 0xffffffffu, best_b = 0;
-        uint64_t sum = 0;
-        for (uint32_t b = 0; b < lp.nback; ++b) {
-          uint32_t x = s_M[w][lp.back[b]];
-          uint32_t d = __ldg(g.deg + x);
-          sum += d;
-          if (d < best_deg) {
-            best_deg = d;
-            best_b = b;
-          }
-        }
-        bytes += 4 * sum;
+        // GenCandidates for level l: driver = smallest backward list, range =
+        // its label sub-range
+        const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l]);
+        bytes += 4ull * su.deg_sum;
         ++calls;
         if (lane == l) {
-          uint32_t x = s_M[w][lp.back[best_b]];
-          r_off = __ldg(g.off + x);
-          r_cur = 0;
-          r_end = best_deg;
+          r_off = su.drv_off;
+          r_cur = su.lo;
+          r_end = su.hi;
           r_mask = 0;
-          r_drv = best_b;
-          r_dlen = best_deg;
+          r_drv = su.drv_b;
+          r_dlen = su.hi - su.lo;
         }
-        if (lane < kFloorB) s_floor[w][l][lane] = 0;
         __syncwarp();
       }
     }

@@ -99,7 +99,8 @@ std::vector<uint32_t> matching_order(const HostQuery& q, uint32_t e,
   return order;
 }
 
-EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order) {
+EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order,
+                       const std::vector<std::pair<uint32_t, uint32_t>>& label_range) {
   EdgeProg p{};
   p.n = q.n;
   p.query = query_index;
@@ -108,6 +109,8 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
     LevelProg& lp = p.lv[l];
     uint32_t u = order[l];
     lp.qbit = 1u << u;
+    lp.vlo = label_range[u].first;
+    lp.vhi = label_range[u].second;
     lp.nback = 0;
     for (uint32_t j = 0; j < l; ++j) {
       if (q.adjacent(order[j], u)) {

@@ -133,11 +133,16 @@ __global__ void k_compact(DevGraphMut g, const uint64_t* __restrict__ new_off,
 // K1: canonicalise and validate each update (UpdateBatch ctor,
 // src/graph.cpp:8-23; validate_batch, src/graph.cpp:117-135).  Presence is a
 // binary search in the lower-degree endpoint's sorted list.
+// External vertex ids are translated to the internal label-ordered ids here;
+// every later kernel reads the translated copy `iups`.
 __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, DevGraph g,
-                          BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
-                          uint8_t* ecode) {
+                          const uint32_t* __restrict__ new_of, bdsm_update_dev* iups, BatchState* st,
+                          uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
+    if (up.u < g.V) up.u = new_of[up.u];
+    if (up.v < g.V) up.v = new_of[up.v];
+    iups[i] = up;
     uint32_t del = up.op != 0 ? 1u : 0u;
     keys[2 * i] = (uint64_t(up.u) << 32) | up.v;
     keys[2 * i + 1] = (uint64_t(up.v) << 32) | up.u;
@@ -500,9 +505,10 @@ void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* 
   k_compact<<<blocks_for(uint64_t(g_old.V) * 32), kThreads, 0, s>>>(g_old, new_off, new_cap, new_adj,
                                                                     new_elab);
 }
-void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, BatchState* st,
-                    uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, cudaStream_t s) {
-  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, st, keys, vals, dlab, ecode);
+void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const uint32_t* new_of,
+                    bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
+                    uint8_t* ecode, cudaStream_t s) {
+  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode);
 }
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
                       uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
