@@ -46,6 +46,9 @@ CONFIGS = {
     "C5": dict(kind="chunglu", V=1_000_000, E=10_000_000, L=1, qsize=5, qcat="clique", batch=10_000,
                mode="mixed", dmax=5_000, gamma=2.3,
                desc="Batch-size sweep with unlabelled 5-vertex clique query"),
+    "C5cycle": dict(kind="chunglu", V=1_000_000, E=10_000_000, L=1, qsize=5, qcat="cycle", batch=10_000,
+                    mode="mixed", dmax=5_000, gamma=2.3,
+                    desc="Batch-size sweep with unlabelled 5-cycle query"),
 }
 
 
@@ -323,6 +326,10 @@ def build(name: str, nbatches: int, seed_graph: int = 1, seed_query: int = 7, se
         n = cfg["qsize"]
         ql = [0] * n
         qe = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    elif cfg["qcat"] == "cycle":
+        n = cfg["qsize"]
+        ql = [0] * n
+        qe = [(i, (i + 1) % n) for i in range(n)]
     else:
         ql, qe = extract_query(csr, labels, cfg["qsize"], cfg["qcat"], seed_query)
     bsz = batch or cfg["batch"]
