@@ -154,7 +154,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batch", type=int, default=None, help="override updates per batch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-prefix", type=int, default=1000, help="updates per CPU-baseline sub-batch")
+    ap.add_argument("--cpu-prefix", type=int, default=100, help="updates per CPU-baseline sub-batch")
     ap.add_argument("--cpu-batches", type=int, default=3)
     ap.add_argument("--cpu-time-cap", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -164,10 +164,15 @@ def main():
     world, rank, local = dist_env()
     if args.steps < 1 or args.warmup < 3:
         log("warmup must be >= 3 and steps >= 1")
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if ndev:
+        # more ranks than GPUs (functional test of the split on a 1-GPU box):
+        # ranks share devices and the counts go through gloo
+        local = local % ndev
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
+        backend = "nccl" if ndev >= world else "gloo"
+        if ndev:
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     if args.impl == "reference":
@@ -256,7 +261,8 @@ def ours(args, world, rank, local):
         if world == 1:
             return vals
         import torch.distributed as dist
-        t = torch.tensor(vals, dtype=torch.float64 if op == "max" else torch.int64, device=dev)
+        on = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(vals, dtype=torch.float64 if op == "max" else torch.int64, device=on)
         dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return t.tolist()
 
@@ -352,6 +358,23 @@ def ours(args, world, rank, local):
         W.write_file(wl, path)
         res = run_reference_binary(path, args.cpu_prefix, args.cpu_batches, args.cpu_time_cap, timeout=600)
         shutil.rmtree(tmp, ignore_errors=True)
+        if res.get("batches"):
+            # Full-scale parity against the reference itself: replay the same
+            # sub-batch protocol (prefix counted, rest applied) on a fresh engine.
+            engC = bd.Engine(wl.labels, wl.src, wl.dst, device=local, chunk=args.chunk)
+            engC.add_query(wl.qlabels, wl.qedges)
+            ours_sub = []
+            for b, ref_b in zip(wl.batches, res["batches"]):
+                P = ref_b["updates"]
+                r = engC.match_batch(b[:P])
+                ours_sub.append((r.positive[0], r.negative[0]))
+                if P < len(b):
+                    engC.match_batch(b[P:])
+            engC.close()
+            refc = [(b["positive"], b["negative"]) for b in res["batches"]]
+            line["parity_vs_reference"] = {
+                "protocol": "reference sub-batches (first P updates of each batch counted, rest applied)",
+                "reference": refc, "ours": ours_sub, "equal": refc == ours_sub[:len(refc)]}
         if "summary" in res:
             s = res["summary"]
             line["cpu_baseline"] = {
