@@ -112,6 +112,18 @@ constexpr uint32_t kRowInsFlag = 1u << 31;
 constexpr uint32_t kRowDelFlag = 1u << 30;
 constexpr uint32_t kRowFlags = kRowInsFlag | kRowDelFlag;
 
+// Per-batch open-addressing table of the directed update keys (x << 32 | y)
+// -> (batch index | op << 31), for O(1) visibility-rule lookups.
+constexpr unsigned long long kEmptyKey = ~0ull;
+__host__ __device__ __forceinline__ uint32_t pair_hash(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return uint32_t(k);
+}
+
 // Device-side batch bookkeeping, copied back once per batch.
 struct BatchState {
   uint32_t err_count;            // validate_batch failures

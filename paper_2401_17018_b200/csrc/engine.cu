@@ -117,6 +117,8 @@ struct bdsm_engine {
   DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
+  DBuf<unsigned long long> hkeys;  // visibility table of the batch
+  DBuf<uint32_t> hvals;
   DBuf<uint32_t> upd_counts, upd_task_counts, item_off, task_off;
   DBuf<uint64_t> upd_cost, cost_off;
   DBuf<Task> tasks;
@@ -557,6 +559,10 @@ struct bdsm_engine {
     upd_cost.ensure(cap_n + 1);
     cost_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
+    size_t hcap = 1024;
+    while (hcap < 4 * cap_n) hcap <<= 1;  // >= 2x the 2|dB| directed keys
+    hkeys.ensure(hcap);
+    hvals.ensure(hcap);
     batch_cap = cap_n;
   }
 
@@ -598,6 +604,9 @@ struct bdsm_engine {
     a.skeys = skeys.p;
     a.svals = svals.p;
     a.m_keys = 2 * n;
+    a.hkeys = hkeys.p;
+    a.hvals = hvals.p;
+    a.hmask = uint32_t(hkeys.n - 1);
     a.phase = phase;
     a.query = uint32_t(qi);
     a.qn = qs.q.n;
@@ -731,7 +740,9 @@ struct bdsm_engine {
           CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
       }
       // device-input batches: the ups buffer the kernels read is `src`
-      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, stream);
+      CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
+      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
+                       uint32_t(hkeys.n - 1), stream);
       {
         size_t tmp = cub_tmp.n;
         CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
@@ -860,7 +871,9 @@ struct bdsm_engine {
     CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
     const uint32_t m = 2 * n, nq = uint32_t(queries.size());
     // the batch-endpoint row flags were cleared at the end of the attempt
-    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, stream);
+    CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
+    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
+                     uint32_t(hkeys.n - 1), stream);
     run_phase(n, 1);
     launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
     CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));

@@ -50,7 +50,7 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const ui
                     uint8_t* ecode, cudaStream_t s);
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
                       uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                      cudaStream_t s);
+                      unsigned long long* hkeys, uint32_t* hvals, uint32_t hmask, cudaStream_t s);
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
                         cudaStream_t s);
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
@@ -74,9 +74,12 @@ struct PhaseArgs {
   uint32_t n_anchor;
   const EdgeProg* progs;
   const uint32_t* rows;          // candidate rows of this query
-  const uint64_t* skeys;         // sorted directed batch keys (visibility lookups)
+  const uint64_t* skeys;         // sorted directed batch keys
   const uint32_t* svals;
   uint32_t m_keys;
+  const unsigned long long* hkeys;  // visibility table (pair_hash, linear probing)
+  const uint32_t* hvals;
+  uint32_t hmask;
   uint32_t phase;                // 0 negative (deletes), 1 positive (inserts)
   uint32_t query;
   uint32_t qn;                   // query vertex count

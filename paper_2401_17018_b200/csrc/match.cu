@@ -181,12 +181,18 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // Is the data edge (x, c) a same-kind batch update with order < anchor?
 // (dedupe_by_order, src/matcher.cpp:110-117, applied at generation time.)
 __device__ __forceinline__ bool hidden_edge(const PhaseArgs& a, uint32_t x, uint32_t c, uint32_t anchor) {
-  uint64_t key = (uint64_t(x) << 32) | c;
-  uint32_t p = lb_u64(a.skeys, a.m_keys, key);
-  if (p >= a.m_keys || __ldg(a.skeys + p) != key) return false;
-  uint32_t val = __ldg(a.svals + p);
-  bool is_del = val >> 31;
-  return is_del == (a.phase == 0) && (val & 0x7fffffffu) < anchor;
+  const unsigned long long key = (uint64_t(x) << 32) | c;
+  uint32_t pos = pair_hash(key) & a.hmask;
+  while (true) {  // linear probing; the table is at most half full
+    const unsigned long long k = __ldg(a.hkeys + pos);
+    if (k == key) {
+      const uint32_t val = __ldg(a.hvals + pos);
+      const bool is_del = val >> 31;
+      return is_del == (a.phase == 0) && (val & 0x7fffffffu) < anchor;
+    }
+    if (k == kEmptyKey) return false;
+    pos = (pos + 1) & a.hmask;
+  }
 }
 
 __device__ __forceinline__ bool bit_set(const uint32_t* bits, uint32_t v) {
@@ -323,8 +329,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   uint32_t r_end = 0;   // end of driver range
   uint32_t r_mask = 0;  // unexplored candidates of the current chunk
   uint32_t r_drv = 0;   // index of the driver in the level's backward list
-  uint32_t r_touch = 0; // lane l: is M[l] a same-kind batch endpoint
-  uint32_t r_dlen = 0;  // length of the driver list
   uint32_t r_tmask = 0; // current chunk: which candidates are same-kind batch endpoints
   const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
 
@@ -414,47 +418,56 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
       rbegin = task.base + rbegin;
     }
     __syncwarp();
-    // anchor endpoints are same-kind batch endpoints by construction
-    r_touch = lane < 2 ? 1u : (lane < lstart ? ((__ldg(a.rows + s_M[w][lane]) & flag) ? 1u : 0u) : 0u);
-    {  // start level: the item gives the driver range (or a candidate list)
-      const LevelProg& lp = P.lv[lstart];
-      const uint32_t ctm =
-          __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
-      if (lane == lstart) r_tmask = ctm;
-      const LevelSetup su = setup_level(lp, g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart]);
-      if (lane == lstart) {
-        r_off = su.drv_off;
-        r_cur = rbegin;
-        r_end = rend;
-        r_mask = 0;
-        r_drv = su.drv_b;
-        r_dlen = rend > rbegin ? rend - rbegin : 0;
-        if (ncand) {  // donated candidate list: no driver fetching at this level
-          r_cur = r_end = 0;
-          r_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
-        }
+    // Positions whose assigned vertex is a same-kind batch endpoint (bit j <->
+    // M[j]; the anchor endpoints always are), uniform across the warp.
+    uint32_t touched = 3u | __ballot_sync(kFull, lane >= 2 && lane < lstart &&
+                                                     (__ldg(a.rows + s_M[w][lane]) & flag));
+    // The current level's state lives in uniform registers; shallower levels
+    // are parked in the lane-distributed stack (lane j holds level j), so the
+    // hot chunk loop needs no shuffles.
+    uint64_t c_off;
+    uint32_t c_cur, c_end, c_mask, c_drv, c_tmask;
+    {
+      c_tmask = __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
+      const LevelSetup su = setup_level(P.lv[lstart], g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart]);
+      c_off = su.drv_off;
+      c_drv = su.drv_b;
+      c_cur = rbegin;
+      c_end = rend;
+      c_mask = 0;
+      if (ncand) {  // donated candidate list: no driver fetching at this level
+        c_cur = c_end = 0;
+        c_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
       }
     }
-    __syncwarp();
     uint32_t l = lstart;
     while (true) {
-      uint32_t mask = __shfl_sync(kFull, r_mask, l);
-      if (mask == 0) {
-        const uint32_t cur = __shfl_sync(kFull, r_cur, l);
-        const uint32_t end = __shfl_sync(kFull, r_end, l);
-        if (cur >= end) {
+      if (c_mask == 0) {
+        if (c_cur >= c_end) {
           if (l == lstart) break;
-          --l;
+          --l;  // backtrack: restore the parked state of level l
+          c_off = __shfl_sync(kFull, r_off, l);
+          c_cur = __shfl_sync(kFull, r_cur, l);
+          c_end = __shfl_sync(kFull, r_end, l);
+          c_mask = __shfl_sync(kFull, r_mask, l);
+          c_drv = __shfl_sync(kFull, r_drv, l);
+          c_tmask = __shfl_sync(kFull, r_tmask, l);
+          touched &= (1u << l) - 1u;
           continue;
         }
         // ---- donate work at the shallowest splittable level ---------------
         // (upper half of the remaining driver range, or of the remaining
         // candidates of an already-fetched chunk)
-        if (((++dtick) & 3u) == 0) {
+        if (((++dtick) & 7u) == 0) {
           // demand: tickets handed out beyond the slots reserved so far
           const unsigned long long tt =
               *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
           if (int32_t(uint32_t(tt) - uint32_t(tt >> 32)) > 0) {
+            if (lane == l) {  // park the current level: the stack now covers [lstart, l]
+              r_cur = c_cur;
+              r_end = c_end;
+              r_mask = 0;
+            }
             bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= 64;
             bool can_m = lane >= lstart && lane < l && __popc(r_mask) >= 2;
             uint32_t cb = __ballot_sync(kFull, can_r || can_m);
@@ -505,15 +518,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
                   atomicExch(a.dyn_ready + slot, a.epoch);
                   atomicAdd(&st->donations, 1u);
                 }
+                c_end = __shfl_sync(kFull, r_end, l);  // shrinks when j == l
               }
             }
           }
         }
-        const uint32_t end2 = __shfl_sync(kFull, r_end, l);  // may have shrunk
-        const uint64_t doff = __shfl_sync(kFull, r_off, l);
-        const uint32_t dpos = __shfl_sync(kFull, r_drv, l);
-        const uint32_t touched = __ballot_sync(kFull, r_touch);
-        if (lane == l) r_cur = cur + 32;
+        const uint32_t cur = c_cur;
+        const uint32_t end2 = c_end;
+        const uint32_t dpos = c_drv;
+        c_cur += 32;
         if (a.deadline_ns && ((++tick & 255u) == 0) && globaltimer() > a.deadline_ns) {
           timed_out = true;
           break;
@@ -522,11 +535,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         const uint32_t idx = cur + lane;
         bool ok = idx < end2;
         uint32_t c = 0xffffffffu;
-        if (ok) c = __ldg(g.adj + doff + idx);
+        if (ok) c = __ldg(g.adj + c_off + idx);
         uint32_t rw = 0;
         if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
         ok = ok && (rw & lp.qbit) != 0;
-        if (ok && g.elab) ok = __ldg(g.elab + doff + idx) == lp.elab[dpos];
+        if (ok && g.elab) ok = __ldg(g.elab + c_off + idx) == lp.elab[dpos];
         if (ok) {  // injectivity: only same-label positions can collide
           uint32_t eq = lp.eqmask;
           while (eq) {
@@ -583,19 +596,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
           continue;
         }
         s_cand[w][l][lane] = c;
-        const uint32_t tm = __ballot_sync(kFull, tc);
-        if (lane == l) {
-          r_mask = m;
-          r_tmask = tm;
-        }
+        c_mask = m;
+        c_tmask = __ballot_sync(kFull, tc);
         __syncwarp();
       } else {
-        const uint32_t k = __ffs(mask) - 1;
-        if (lane == l) r_mask = mask & (mask - 1);
+        const uint32_t k = __ffs(c_mask) - 1;
+        c_mask &= c_mask - 1;
         const uint32_t c = s_cand[w][l][k];
-        const uint32_t tmask = __shfl_sync(kFull, r_tmask, l);
-        if (lane == l) r_touch = (tmask >> k) & 1u;
         if (lane == 0) s_M[w][l] = c;
+        touched |= ((c_tmask >> k) & 1u) << l;
+        if (lane == l) {  // park level l
+          r_off = c_off;
+          r_cur = c_cur;
+          r_end = c_end;
+          r_mask = c_mask;
+          r_drv = c_drv;
+          r_tmask = c_tmask;
+        }
         __syncwarp();
         ++l;
         // GenCandidates for level l: driver = smallest backward list, range =
@@ -603,15 +620,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l]);
         bytes += 4ull * su.deg_sum;
         ++calls;
-        if (lane == l) {
-          r_off = su.drv_off;
-          r_cur = su.lo;
-          r_end = su.hi;
-          r_mask = 0;
-          r_drv = su.drv_b;
-          r_dlen = su.hi - su.lo;
-        }
-        __syncwarp();
+        c_off = su.drv_off;
+        c_cur = su.lo;
+        c_end = su.hi;
+        c_mask = 0;
+        c_drv = su.drv_b;
+        c_tmask = 0;
       }
     }
     if (lane == 0) atomicSub(&a.q->holders.v, 1u);

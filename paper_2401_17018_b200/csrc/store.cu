@@ -180,7 +180,8 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
 // used to prefilter the visibility rule (UpdateIndex, src/matcher.cpp:27-40).
 __global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                             uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
-                            uint32_t* const* rows, uint32_t nq, uint32_t V) {
+                            uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys,
+                            uint32_t* hvals, uint32_t hmask) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += gridDim.x * blockDim.x) {
     if (j == m) {
       insflag[j] = 0;
@@ -199,6 +200,16 @@ __global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* 
     insflag[j] = is_del ? 0u : 1u;
     if (src < V)
       for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? kRowDelFlag : kRowInsFlag);
+    // visibility table: linear probing (duplicates only in rejected batches)
+    uint32_t pos = pair_hash(k) & hmask;
+    for (uint32_t probe = 0; probe <= hmask; ++probe) {
+      unsigned long long prev = atomicCAS(hkeys + pos, kEmptyKey, (unsigned long long)k);
+      if (prev == kEmptyKey || prev == k) {
+        hvals[pos] = val;
+        break;
+      }
+      pos = (pos + 1) & hmask;
+    }
   }
 }
 
@@ -512,9 +523,9 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const ui
 }
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
                       uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                      cudaStream_t s) {
+                      unsigned long long* hkeys, uint32_t* hvals, uint32_t hmask, cudaStream_t s) {
   k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(skeys, svals, m, st, head, insflag, rows,
-                                                              nq, V);
+                                                              nq, V, hkeys, hvals, hmask);
 }
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
                         cudaStream_t s) {
