@@ -323,10 +323,19 @@ def ours(args, world, rank, local):
         "k_alloc+k_merge_refresh (K3+K4)": (bupd, mg),
     }
     dom = max(kern, key=lambda k: kern[k][1])
+    traffic = None  # DRAM bytes per launch of k_wbm from the committed ncu --set full capture
+    try:
+        with open(os.path.join(REPO, "profiles", "wbm_traffic.json")) as f:
+            tr = json.load(f)
+        if dom.startswith(tr["kernel"]):
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     ab, at = kern[dom]
     achieved = ab / (at / 1e3) / 1e9 if at > 0 else 0.0
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+            "traffic_source": "profiles/wbm_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
             "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
             "other": {k: {"bytes": v[0], "ms": v[1], "GB/s": (v[0] / (v[1] / 1e3) / 1e9 if v[1] > 0 else 0)}
                       for k, v in kern.items() if k != dom},

@@ -19,3 +19,7 @@ for p in "${pids[@]}"; do wait "$p" || { cat "$OBJ"/*.ptxas.log; exit 1; }; done
 "$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o "$HERE/libbdsm_b200.so" \
     "$OBJ/store.o" "$OBJ/match.o" "$OBJ/engine.o" "$OBJ/planner.o"
 echo "built $HERE/libbdsm_b200.so"
+# `bdsm run` CLI (drop-in for the reference's tools/bdsm.cpp), linked against the C ABI
+g++ -std=c++17 -O2 -I"$HERE/../include" "$HERE/csrc/cli.cpp" "$HERE/csrc/textio.cpp" \
+    -L"$HERE" -lbdsm_b200 -Wl,-rpath,'$ORIGIN' -o "$HERE/bdsm"
+echo "built $HERE/bdsm"
