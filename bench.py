@@ -316,7 +316,10 @@ def ours(args, world, rank, local):
     peak, peak_kind = peaks()
     mk = statistics.mean(s["ms_match_kernel"] for s in statsA)
     mg = statistics.mean(s["ms_merge_kernel"] for s in statsA)
-    bphase = statistics.mean(s["bytes_phase"] for s in statsA)
+    # algorithmic bytes of the GenCandidates calls the kernel makes (SURVEY.md
+    # §8(d) per-call figure); the reference DFS tree's B_phase is reported beside
+    bphase = statistics.mean(s["bytes_kernel"] for s in statsA)
+    bphase_ref = statistics.mean(s["bytes_phase"] for s in statsA)
     bupd = statistics.mean(s["bytes_update"] for s in statsA)
     kern = {
         "k_wbm (K6 matching, both phases)": (bphase, mk),
@@ -337,6 +340,10 @@ def ours(args, world, rank, local):
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
             "traffic_source": "profiles/wbm_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
             "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
+            "algorithmic_bytes": "4 B x backward-neighbour degrees per GenCandidates call made by k_wbm "
+                                 "(SURVEY.md §8(d)), per step (negative + positive launch)",
+            "reference_tree_bytes_per_step": bphase_ref,
+            "reference_tree_equivalent_GBps": bphase_ref / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
             "other": {k: {"bytes": v[0], "ms": v[1], "GB/s": (v[0] / (v[1] / 1e3) / 1e9 if v[1] > 0 else 0)}
                       for k, v in kern.items() if k != dom},
             "share_of_step": at / statistics.mean(dev_ms)}

@@ -114,6 +114,9 @@ typedef struct bdsm_batch_stats {
   double ms_merge_kernel;  /* CUDA-event time of K3 alloc + merge/refresh */
   uint32_t kernel_launches;/* launches of this library's own kernels (CUB sort/scan excluded) */
   uint32_t cub_launches;   /* CUB sort / select / scan calls */
+  uint64_t bytes_kernel;   /* 4 B x backward degrees of the GenCandidates calls the kernel actually made
+                              (bytes_phase counts them on the reference's DFS tree; the kernel counts
+                              independent query tails once per prefix instead of enumerating them) */
 } bdsm_batch_stats;
 
 /* Engine lifecycle.  Replaces LabeledGraph::build_from_edges plus the

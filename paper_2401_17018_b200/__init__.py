@@ -66,7 +66,8 @@ class _Stats(C.Structure):
                 ("bytes_phase", C.c_uint64), ("bytes_update", C.c_uint64), ("touched", C.c_uint64),
                 ("relocations", C.c_uint64), ("compactions", C.c_uint32), ("timed_out", C.c_uint32),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("ms_match_kernel", C.c_double),
-                ("ms_merge_kernel", C.c_double), ("kernel_launches", C.c_uint32), ("cub_launches", C.c_uint32)]
+                ("ms_merge_kernel", C.c_double), ("kernel_launches", C.c_uint32), ("cub_launches", C.c_uint32),
+                ("bytes_kernel", C.c_uint64)]
 
 
 _lib = None

@@ -42,6 +42,7 @@ struct LevelProg {
 struct EdgeProg {
   uint32_t n;                    // query vertex count
   uint32_t query;                // query index
+  uint32_t tail;                 // first level T of the independent tail (levels > T are counted, not enumerated)
   uint32_t order[kMaxQ];
   LevelProg lv[kMaxQ];
 };
@@ -145,6 +146,7 @@ struct BatchState {
   uint64_t items_total;
   uint64_t gen_calls;
   uint64_t bytes_phase;
+  uint64_t bytes_kernel;         // 4 B x backward degrees of the GenCandidates calls the kernel made
 };
 
 }  // namespace bdsm_b200

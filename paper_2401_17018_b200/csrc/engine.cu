@@ -842,6 +842,7 @@ struct bdsm_engine {
     st.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
     st.gen_calls = b.gen_calls;
     st.bytes_phase = b.bytes_phase;
+    st.bytes_kernel = b.bytes_kernel;
     st.bytes_update = b.bytes_update + 16ull * n;
     st.touched = b.n_touched;
     st.relocations = b.relocations;

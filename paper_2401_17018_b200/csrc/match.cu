@@ -303,6 +303,122 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   return s;
 }
 
+// One 32-candidate chunk [cur, end2) of level l's driver list: each lane
+// filters its candidate c — candidate-row bit (CandidateTable::is_candidate),
+// edge label, injectivity against same-label assigned positions, membership
+// in every other backward list (intersect_sorted, src/matcher.cpp:59-73) and
+// the lowest-order visibility rule (dedupe_by_order, :110-117) — and the
+// survivors are returned as a ballot.  `tc`: c is a same-kind batch endpoint.
+__device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const LevelProg& lp, const uint32_t* M,
+                                                 uint32_t* floor_l, const uint32_t* ceil_l, uint64_t c_off,
+                                                 uint32_t cur, uint32_t end2, uint32_t dpos, uint32_t touched,
+                                                 uint32_t anchor, uint32_t flag, uint32_t lane, uint32_t& c_out,
+                                                 bool& tc_out) {
+  const DevGraph& g = a.g;
+  const uint32_t idx = cur + lane;
+  bool ok = idx < end2;
+  uint32_t c = 0xffffffffu;
+  if (ok) c = __ldg(g.adj + c_off + idx);
+  uint32_t rw = 0;
+  if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
+  ok = ok && (rw & lp.qbit) != 0;
+  if (ok && g.elab) ok = __ldg(g.elab + c_off + idx) == lp.elab[dpos];
+  if (ok) {  // injectivity: only same-label positions can collide
+    uint32_t eq = lp.eqmask;
+    while (eq) {
+      uint32_t j = __ffs(eq) - 1;
+      eq &= eq - 1;
+      if (M[j] == c) {
+        ok = false;
+        break;
+      }
+    }
+  }
+  const uint32_t remain = end2 - cur;  // driver entries left in this range
+  for (uint32_t b = 0; b < lp.nback; ++b) {  // other backward lists
+    if (b == dpos) continue;
+    if (!__any_sync(kFull, ok)) break;
+    const uint32_t x = M[lp.back[b]];
+    const uint64_t xo = __ldg(g.off + x);
+    const uint32_t xd = __ldg(g.deg + x);
+    // search window: label sub-range [floor, ceil), the floor advancing
+    // with the (ascending) driver chunks
+    uint32_t fl = b < kFloorB ? floor_l[b] : 0;
+    const uint32_t ce = b < kFloorB ? ceil_l[b] : xd;
+    uint32_t p = 0;
+    bool hit;
+    // comparable lengths: merge windows; skewed: floor-bounded binary search
+    if (uint64_t(ce - min(fl, ce)) <= uint64_t(a.merge_ratio) * remain) {
+      hit = member_merge(g.adj + xo, ce, fl, c, ok, lane, &p);
+    } else {
+      hit = false;
+      if (ok) {
+        p = fl + lb_u32(g.adj + xo + fl, ce - fl, c);
+        hit = p < ce && __ldg(g.adj + xo + p) == c;
+      }
+      uint32_t mp = __reduce_max_sync(kFull, ok ? p : 0u);
+      if (mp > fl) fl = mp;
+    }
+    if (b < kFloorB && lane == 0) floor_l[b] = min(fl, ce);
+    if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
+    ok = ok && hit;
+  }
+  const bool tc = (rw & flag) != 0;
+  if (ok && (touched & lp.backmask) && tc) {
+    uint32_t tb = touched & lp.backmask;
+    while (tb && ok) {
+      uint32_t j = __ffs(tb) - 1;
+      tb &= tb - 1;
+      if (hidden_edge(a, M[j], c, anchor)) ok = false;
+    }
+  }
+  c_out = c;
+  tc_out = tc;
+  return __ballot_sync(kFull, ok);
+}
+
+// Independent tail (EdgeProg::tail): levels T+1..n-1 have all their backward
+// neighbours in the prefix M[0..T) and pairwise distinct labels, so given the
+// prefix their candidate sets are independent and every level-T candidate
+// roots the same subtree: Π_{t>T} |C_t| matches.  The reference enumerates
+// that subtree per level-T candidate; here it is counted once per prefix and
+// multiplied.  Also returns, per level-T candidate, the DFS visits
+// (1 + Σ_k Π_{T<s<=k} |C_s|), GenCandidates calls and B_phase bytes the
+// reference tree spends below it, so MatchStats-style
+// counters stay those of the reference tree.
+struct TailFactor {
+  unsigned long long f, v, b, c;
+};
+
+__device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& P, uint32_t T, uint32_t w,
+                                            const uint32_t* M, uint32_t (*s_floor)[kMaxQ][kFloorB],
+                                            uint32_t (*s_ceil)[kMaxQ][kFloorB], uint32_t touched, uint32_t anchor,
+                                            uint32_t flag, uint32_t lane, TailFactor* out,
+                                            unsigned long long* stat) {
+  unsigned long long prod = 1, v = 1, b = 0, c = 0;
+  for (uint32_t t = T + 1; t < P.n; ++t) {
+    const LevelProg& lp = P.lv[t];
+    const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t]);
+    __syncwarp();
+    b += prod * 4ull * su.deg_sum;  // one call per visit at level t-1
+    c += prod;
+    if (lane == 0) stat[4] += 4ull * su.deg_sum;
+    unsigned long long cnt = 0;
+    for (uint32_t cur = su.lo; cur < su.hi; cur += 32) {
+      uint32_t cc;
+      bool tc;
+      cnt += __popc(filter_chunk(a, lp, M, s_floor[w][t], s_ceil[w][t], su.drv_off, cur, su.hi, su.drv_b, touched,
+                                 anchor, flag, lane, cc, tc));
+      __syncwarp();
+    }
+    prod *= cnt;
+    v += prod;
+    if (prod == 0) break;  // the reference tree has no deeper nodes either
+  }
+  if (lane == 0) *out = TailFactor{prod, v, b, c};
+  __syncwarp();
+}
+
 #ifndef BDSM_WBM_MIN_BLOCKS
 #define BDSM_WBM_MIN_BLOCKS 4  // resident 256-thread CTAs per SM the register budget must allow
 #endif
@@ -311,14 +427,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
   __shared__ uint32_t s_ceil[kWarpsPerBlock][kMaxQ][kFloorB];
+  __shared__ TailFactor s_tail[kWarpsPerBlock];
+  // per-warp counters (lane 0 updates them; kept out of the register budget)
+  __shared__ unsigned long long s_stat[kWarpsPerBlock][5];  // count, visits, bytes, calls, kernel bytes
   if (batch_aborted(a.st)) return;
   BatchState* st = a.st;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
   const uint32_t n_items = st->n_items[a.phase];
   const DevGraph& g = a.g;
-  uint64_t count = 0, visits = 0, bytes = 0, calls = 0;
-  uint32_t tick = 0, dtick = 0;
+  unsigned long long* stat = s_stat[threadIdx.x >> 5];
+  if ((threadIdx.x & 31) < 5) stat[threadIdx.x & 31] = 0;
+  __syncwarp();
+  uint32_t dtick = 0;
   bool timed_out = false;
   bool static_done = false;
   uint32_t ticket = kNone;  // lane 0: outstanding ticket of this warp
@@ -406,7 +527,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     const Task task = a.tasks[task_id];
     const EdgeProg& P = a.progs[task.prog];
     const uint32_t anchor = task.upd;
-    const uint32_t n = P.n;
+    const uint32_t T = P.tail;  // deepest DFS level; deeper levels are counted by tail_factor
     if (kind == 1) {
       const bdsm_update_dev up = a.ups[task.upd];
       const uint32_t m0 = task.flip ? up.v : up.u, m1 = task.flip ? up.u : up.v;
@@ -430,6 +551,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     {
       c_tmask = __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
       const LevelSetup su = setup_level(P.lv[lstart], g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart]);
+      if (lane == 0) stat[4] += 4ull * su.deg_sum;
       c_off = su.drv_off;
       c_drv = su.drv_b;
       c_cur = rbegin;
@@ -439,6 +561,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         c_cur = c_end = 0;
         c_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
       }
+      if (lstart == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat);
     }
     uint32_t l = lstart;
     while (true) {
@@ -457,8 +580,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         }
         // ---- donate work at the shallowest splittable level ---------------
         // (upper half of the remaining driver range, or of the remaining
-        // candidates of an already-fetched chunk)
+        // candidates of an already-fetched chunk); the deadline is polled on
+        // the same cadence.
         if (((++dtick) & 7u) == 0) {
+          if (a.deadline_ns && (dtick & 255u) == 0 &&
+              __shfl_sync(kFull, uint32_t(globaltimer() > a.deadline_ns), 0)) {
+            timed_out = true;
+            break;
+          }
           // demand: tickets handed out beyond the slots reserved so far
           const unsigned long long tt =
               *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
@@ -524,77 +653,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
           }
         }
         const uint32_t cur = c_cur;
-        const uint32_t end2 = c_end;
-        const uint32_t dpos = c_drv;
         c_cur += 32;
-        if (a.deadline_ns && ((++tick & 255u) == 0) && globaltimer() > a.deadline_ns) {
-          timed_out = true;
-          break;
-        }
-        const LevelProg& lp = P.lv[l];
-        const uint32_t idx = cur + lane;
-        bool ok = idx < end2;
-        uint32_t c = 0xffffffffu;
-        if (ok) c = __ldg(g.adj + c_off + idx);
-        uint32_t rw = 0;
-        if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
-        ok = ok && (rw & lp.qbit) != 0;
-        if (ok && g.elab) ok = __ldg(g.elab + c_off + idx) == lp.elab[dpos];
-        if (ok) {  // injectivity: only same-label positions can collide
-          uint32_t eq = lp.eqmask;
-          while (eq) {
-            uint32_t j = __ffs(eq) - 1;
-            eq &= eq - 1;
-            if (s_M[w][j] == c) {
-              ok = false;
-              break;
-            }
+        uint32_t c;
+        bool tc;
+        const uint32_t m = filter_chunk(a, P.lv[l], s_M[w], s_floor[w][l], s_ceil[w][l], c_off, cur, c_end, c_drv,
+                                        touched, anchor, flag, lane, c, tc);
+        if (l == T) {  // last DFS level: every survivor roots the counted tail
+          const unsigned long long pm = __popc(m);
+          if (pm && lane == 0) {
+            const TailFactor tf = s_tail[w];
+            stat[0] += pm * tf.f;
+            stat[1] += pm * tf.v;
+            stat[2] += pm * tf.b;
+            stat[3] += pm * tf.c;
           }
-        }
-        const uint32_t remain = end2 - cur;  // driver entries left in this range
-        for (uint32_t b = 0; b < lp.nback; ++b) {  // other backward lists
-          if (b == dpos) continue;
-          if (!__any_sync(kFull, ok)) break;
-          const uint32_t x = s_M[w][lp.back[b]];
-          const uint64_t xo = __ldg(g.off + x);
-          const uint32_t xd = __ldg(g.deg + x);
-          // search window: label sub-range [floor, ceil), the floor advancing
-          // with the (ascending) driver chunks
-          uint32_t fl = b < kFloorB ? s_floor[w][l][b] : 0;
-          const uint32_t ce = b < kFloorB ? s_ceil[w][l][b] : xd;
-          uint32_t p = 0;
-          bool hit;
-          // comparable lengths: merge windows; skewed: floor-bounded binary search
-          if (uint64_t(ce - min(fl, ce)) <= uint64_t(a.merge_ratio) * remain) {
-            hit = member_merge(g.adj + xo, ce, fl, c, ok, lane, &p);
-          } else {
-            hit = false;
-            if (ok) {
-              p = fl + lb_u32(g.adj + xo + fl, ce - fl, c);
-              hit = p < ce && __ldg(g.adj + xo + p) == c;
-            }
-            uint32_t mp = __reduce_max_sync(kFull, ok ? p : 0u);
-            if (mp > fl) fl = mp;
-          }
-          if (b < kFloorB && lane == 0) s_floor[w][l][b] = min(fl, ce);
-          if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
-          ok = ok && hit;
-        }
-        const bool tc = (rw & flag) != 0;
-        if (ok && (touched & lp.backmask) && tc) {
-          uint32_t tb = touched & lp.backmask;
-          while (tb && ok) {
-            uint32_t j = __ffs(tb) - 1;
-            tb &= tb - 1;
-            if (hidden_edge(a, s_M[w][j], c, anchor)) ok = false;
-          }
-        }
-        const uint32_t m = __ballot_sync(kFull, ok);
-        visits += __popc(m);
-        if (l + 1 == n) {
-          count += __popc(m);
           continue;
         }
+        if (lane == 0) stat[1] += __popc(m);
         s_cand[w][l][lane] = c;
         c_mask = m;
         c_tmask = __ballot_sync(kFull, tc);
@@ -618,24 +693,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         // GenCandidates for level l: driver = smallest backward list, range =
         // its label sub-range
         const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l]);
-        bytes += 4ull * su.deg_sum;
-        ++calls;
+        if (lane == 0) {
+          stat[2] += 4ull * su.deg_sum;
+          stat[3] += 1;
+          stat[4] += 4ull * su.deg_sum;
+        }
         c_off = su.drv_off;
         c_cur = su.lo;
         c_end = su.hi;
         c_mask = 0;
         c_drv = su.drv_b;
         c_tmask = 0;
+        if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat);
       }
     }
     if (lane == 0) atomicSub(&a.q->holders.v, 1u);
     if (timed_out) break;
   }
+  __syncwarp();
   if (lane == 0) {
-    if (count) atomicAdd((unsigned long long*)&st->counts[a.phase][a.query], (unsigned long long)count);
-    if (visits) atomicAdd((unsigned long long*)&st->visits, (unsigned long long)visits);
-    if (bytes) atomicAdd((unsigned long long*)&st->bytes_phase, (unsigned long long)bytes);
-    if (calls) atomicAdd((unsigned long long*)&st->gen_calls, (unsigned long long)calls);
+    if (stat[0]) atomicAdd((unsigned long long*)&st->counts[a.phase][a.query], stat[0]);
+    if (stat[1]) atomicAdd((unsigned long long*)&st->visits, stat[1]);
+    if (stat[2]) atomicAdd((unsigned long long*)&st->bytes_phase, stat[2]);
+    if (stat[3]) atomicAdd((unsigned long long*)&st->gen_calls, stat[3]);
+    if (stat[4]) atomicAdd((unsigned long long*)&st->bytes_kernel, stat[4]);
     if (timed_out) atomicOr(&st->timed_out, 1u << a.query);
   }
 }

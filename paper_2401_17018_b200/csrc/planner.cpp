@@ -122,6 +122,21 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
       if (q.labels[order[j]] == q.labels[u]) lp.eqmask |= 1u << j;
     }
   }
+  // Independent tail: the smallest T >= 2 such that every level t >= T has
+  // all its backward neighbours before T (no query edge inside the tail) and
+  // the tail's labels are pairwise distinct (no injectivity between tail
+  // vertices).  Given M[0..T) the tail levels' candidate sets are then
+  // independent, so the kernel counts each once and multiplies.
+  auto independent = [&](uint32_t t0) {
+    for (uint32_t t = t0; t < q.n; ++t) {
+      if (p.lv[t].backmask >> t0) return false;
+      for (uint32_t s = t0; s < t; ++s)
+        if (q.labels[order[s]] == q.labels[order[t]]) return false;
+    }
+    return true;
+  };
+  p.tail = q.n >= 3 ? q.n - 1 : 0;
+  while (p.tail > 2 && independent(p.tail - 1)) --p.tail;
   return p;
 }
 
