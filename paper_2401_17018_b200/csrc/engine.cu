@@ -443,7 +443,12 @@ struct bdsm_engine {
     de.G = uint32_t(qs->enc.group_labels.size());
     de.cap = qs->enc.cap;
     for (uint32_t u = 0; u < de.n; ++u) de.qlabel[u] = qs->q.labels[u];
-    for (uint32_t gi = 0; gi < de.G; ++gi) de.glabel[gi] = qs->enc.group_labels[gi];
+    for (uint32_t gi = 0; gi < de.G; ++gi) {
+      de.glabel[gi] = qs->enc.group_labels[gi];
+      const auto r = label_range(de.glabel[gi]);
+      de.glo[gi] = r.first;
+      de.ghi[gi] = r.second;
+    }
     for (uint32_t u = 0; u < de.n; ++u)
       for (uint32_t gi = 0; gi < de.G; ++gi) de.qcnt[u][gi] = qs->enc.qcnt[u * de.G + gi];
     DBuf<DevQueryEnc> one;

@@ -16,6 +16,7 @@ struct DevQueryEnc {
   uint32_t cap;                  // saturation cap
   uint32_t qlabel[kMaxQ];
   uint32_t glabel[kMaxQ];
+  uint32_t glo[kMaxQ], ghi[kMaxQ];  // internal-id range of each group's label (ids are label-ordered)
   uint8_t qcnt[kMaxQ][kMaxQ];    // [u][g]
 };
 

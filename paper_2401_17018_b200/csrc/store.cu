@@ -272,14 +272,45 @@ __device__ __forceinline__ void merged_pos(const uint64_t* seg, uint32_t segn,
   p = i - D + I;
 }
 
+// Saturated neighbour counts of one query's label groups for a sorted list
+// (encode_vertex, src/encoding.cpp:70-87): internal ids are label-ordered, so
+// group g's count is the size of the id range [glo[g], ghi[g]) inside the
+// list — two binary searches (lanes 2g / 2g+1) instead of a label gather per
+// neighbour.  Returns lane g's count of group g.
+__device__ __forceinline__ uint32_t group_counts(const uint32_t* lst, uint32_t d, const DevQueryEnc& qe,
+                                                 uint32_t lane) {
+  const uint32_t gi = lane >> 1;
+  uint32_t bnd = 0;
+  if (gi < qe.G) bnd = lower_bound_u32(lst, d, (lane & 1) ? qe.ghi[gi] : qe.glo[gi]);
+  const uint32_t lo = __shfl_sync(kFull, bnd, (2 * lane) & 31);
+  const uint32_t hi = __shfl_sync(kFull, bnd, (2 * lane + 1) & 31);
+  uint32_t cnt = lane < qe.G ? hi - lo : 0;
+  return cnt > qe.cap ? qe.cap : cnt;
+}
+
+// Candidate row of a vertex with label vl from lane g's saturated counts
+// (encoding_contains, src/encoding.cpp:115-122).
+__device__ __forceinline__ uint32_t row_of(const DevQueryEnc& qe, uint32_t vl, uint32_t cnt, uint32_t lane) {
+  uint32_t row = 0;
+  for (uint32_t u = 0; u < qe.n; ++u) {
+    bool ok = lane >= qe.G || cnt >= qe.qcnt[u][lane];
+    if (__all_sync(kFull, ok) && vl == qe.qlabel[u]) row |= 1u << u;
+  }
+  return row;
+}
+
+constexpr uint32_t kMoveUnroll = 8;  // old elements per lane in flight per sweep step
+
 // K3 (part 2) + K4: one warp per touched vertex.  Insert slots are computed
 // first against the intact old list.  In place (merged list fits the slack)
 // the old elements move in two sweeps — ascending for left-movers, descending
-// for right-movers — and each sweep only overwrites slots whose element has
-// already moved (the merged order is a monotone map of the old order), then
-// the inserts fill their slots.  Relocated lists are merged out of place.
-// The same warp then re-streams the new list to recount per-label neighbour
-// counters and recompute the candidate row of every query (K4).
+// for right-movers — in steps of 32 x kMoveUnroll elements: a step is read
+// completely before it is written, and it only writes slots of its own step
+// or of steps already read (the merged order is a monotone map of the old
+// order and single-kind segments shift in one direction), so hub lists move
+// with kMoveUnroll loads in flight per lane.  Relocated lists are merged out
+// of place.  The same warp then recomputes the candidate row of every query
+// from label-range counts of the new list (K4).
 __global__ void __launch_bounds__(256) k_merge_refresh(
     const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
     const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
@@ -321,60 +352,48 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
     }
     __syncwarp();
-    // 2. move old elements
-    if (reloc) {
-      for (uint32_t i = lane; i < dold; i += 32) {
-        uint32_t a = src[i], p;
-        bool dl;
-        merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
-        if (!dl) {
-          dst[p] = a;
-          if (edst) edst[p] = esrc[i];
-        }
-      }
-    } else if (dold > 0) {
-      // In place only for single-kind segments (k_alloc relocates mixed ones):
-      // delete-only lists move left (ascending sweep), insert-only lists move
-      // right (descending sweep); either sweep writes only to slots already read.
-      uint32_t start = 0;
-      if (lane == 0) start = lower_bound_u32(src, dold, uint32_t(seg[0]));  // below: never moves
+    // 2. move old elements (elements below the first batch key never move)
+    uint32_t start = 0;
+    if (!reloc) {
+      if (lane == 0 && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
       start = __shfl_sync(kFull, start, 0);
-      if (nins == 0) {
-        for (uint32_t base = start; base < dold; base += 32) {  // left-movers, ascending
-          uint32_t i = base + lane, a = 0, p = 0, el = kNone;
-          bool dl = true;
-          if (i < dold) {
-            a = src[i];
-            if (esrc) el = esrc[i];
-            merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
-          }
-          __syncwarp();
-          if (i < dold && !dl && p < i) {
-            dst[p] = a;
-            if (edst) edst[p] = el;
-          }
-          __syncwarp();
-        }
-      } else if (dold > start) {  // right-movers, descending
-        int nch = int((dold - start + 31) / 32);
-        for (int c = nch - 1; c >= 0; --c) {
-          uint32_t i = start + uint32_t(c) * 32 + lane, a = 0, p = 0, el = kNone;
-          bool dl = true;
-          if (i < dold) {
-            a = src[i];
-            if (esrc) el = esrc[i];
-            merged_pos(seg, segn, ins_prefix, s, a, i, p, dl);
-          }
-          __syncwarp();
-          if (i < dold && !dl && p > i) {
-            dst[p] = a;
-            if (edst) edst[p] = el;
-          }
-          __syncwarp();
+    }
+    const bool ascending = reloc || nins == 0;  // left-movers ascend, right-movers descend
+    const uint32_t step = 32 * kMoveUnroll;
+    const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
+    for (uint32_t si = 0; si < nsteps; ++si) {
+      const uint32_t base = start + (ascending ? si : nsteps - 1 - si) * step;
+      uint32_t a[kMoveUnroll], p[kMoveUnroll], el[kMoveUnroll];
+      bool mv[kMoveUnroll];
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        const uint32_t i = base + k * 32 + lane;
+        mv[k] = false;
+        el[k] = kNone;
+        if (i < dold) {
+          a[k] = src[i];
+          if (esrc) el[k] = esrc[i];
         }
       }
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        const uint32_t i = base + k * 32 + lane;
+        if (i < dold) {
+          bool dl;
+          merged_pos(seg, segn, ins_prefix, s, a[k], i, p[k], dl);
+          mv[k] = !dl && (reloc || p[k] != i);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        if (mv[k]) {
+          dst[p[k]] = a[k];
+          if (edst) edst[p[k]] = el[k];
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
     // 3. inserts
     for (uint32_t k = lane; k < segn; k += 32) {
       uint32_t val = svals[s + k];
@@ -393,25 +412,11 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
     // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
+    const uint32_t vl = g.vlabel[x];
     for (uint32_t q = 0; q < nq; ++q) {
       const DevQueryEnc& qe = qenc[q];
-      uint32_t cnt = 0;  // lane g holds group g's count
-      for (uint32_t base = 0; base < dnew; base += 32) {
-        uint32_t i = base + lane;
-        uint32_t lab = i < dnew ? __ldg(g.vlabel + dst[i]) : kNone;
-        for (uint32_t gi = 0; gi < qe.G; ++gi) {
-          uint32_t b = __ballot_sync(kFull, lab == qe.glabel[gi]);
-          if (lane == gi) cnt += __popc(b);
-        }
-      }
-      if (cnt > qe.cap) cnt = qe.cap;
-      uint32_t vl = g.vlabel[x];
-      uint32_t row = 0;
-      for (uint32_t u = 0; u < qe.n; ++u) {
-        bool ok = lane >= qe.G || cnt >= qe.qcnt[u][lane];
-        bool all = __all_sync(kFull, ok);
-        if (all && vl == qe.qlabel[u]) row |= 1u << u;
-      }
+      const uint32_t cnt = group_counts(dst, dnew, qe, lane);
+      const uint32_t row = row_of(qe, vl, cnt, lane);
       if (lane == 0) {
         const uint32_t word = rows[q][x];
         const uint32_t before = word & ~kRowFlags;  // keep the batch flags
@@ -447,23 +452,8 @@ __global__ void __launch_bounds__(256) k_encode_all(DevGraph g, const DevQueryEn
       if (lane == 0) rows[v] = 0;
       continue;
     }
-    uint32_t d = g.deg[v];
-    const uint32_t* lst = g.adj + g.off[v];
-    uint32_t cnt = 0;
-    for (uint32_t base = 0; base < d; base += 32) {
-      uint32_t i = base + lane;
-      uint32_t lab = i < d ? __ldg(g.vlabel + lst[i]) : kNone;
-      for (uint32_t gi = 0; gi < qe.G; ++gi) {
-        uint32_t b = __ballot_sync(kFull, lab == qe.glabel[gi]);
-        if (lane == gi) cnt += __popc(b);
-      }
-    }
-    if (cnt > qe.cap) cnt = qe.cap;
-    uint32_t row = 0;
-    for (uint32_t u = 0; u < qe.n; ++u) {
-      bool ok = lane >= qe.G || cnt >= qe.qcnt[u][lane];
-      if (__all_sync(kFull, ok) && vl == qe.qlabel[u]) row |= 1u << u;
-    }
+    const uint32_t cnt = group_counts(g.adj + g.off[v], g.deg[v], qe, lane);
+    const uint32_t row = row_of(qe, vl, cnt, lane);
     if (lane == 0) rows[v] = row;
   }
 }
