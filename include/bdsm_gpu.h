@@ -158,6 +158,9 @@ BDSM_API const char* bdsm_last_error(void);
 BDSM_API size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, size_t cap);
 BDSM_API bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out /* [V] */);
 BDSM_API int bdsm_engine_order(bdsm_engine* engine, int query, uint32_t edge, uint32_t* out /* [32] */);
+/* First level T of the independent tail of that order: levels > T are counted
+ * once per prefix and multiplied instead of enumerated (no reference counterpart). */
+BDSM_API int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge);
 BDSM_API bdsm_status bdsm_engine_column_sizes(bdsm_engine* engine, int query, uint64_t* out /* [n] */);
 BDSM_API uint64_t bdsm_engine_num_edges(bdsm_engine* engine);
 BDSM_API uint32_t bdsm_engine_num_vertices(bdsm_engine* engine);
@@ -169,6 +172,10 @@ BDSM_API bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query);
  * its cost, in canonical order.  owner = floor(world * prefix / total).
  * Pure host function, used by the engine and by the CPU tests. */
 BDSM_API void bdsm_shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);
+
+/* Diagnostics of -DBDSM_TRACE builds: per-phase matching-kernel trace words
+ * of the last batch (zeros otherwise).  Returns the number of words. */
+BDSM_API size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size_t cap);
 
 BDSM_API const char* bdsm_version(void);
 

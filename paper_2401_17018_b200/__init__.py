@@ -33,7 +33,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libbdsm_b200.so")
+    # BDSM_LIB: an alternative build of the same engine (e.g. -DBDSM_TRACE diagnostics)
+    return os.environ.get("BDSM_LIB") or os.path.join(_HERE, "libbdsm_b200.so")
 
 
 UPDATE_DTYPE = np.dtype([("u", "<u4"), ("v", "<u4"), ("op", "<u4"), ("elab", "<u4")])
@@ -115,6 +116,10 @@ def _load():
     L.bdsm_engine_num_vertices.argtypes = [C.c_void_p]
     L.bdsm_shard_owners.restype = None
     L.bdsm_shard_owners.argtypes = [C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]
+    L.bdsm_engine_debug_trace.restype = C.c_size_t
+    L.bdsm_engine_debug_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.bdsm_engine_tail.restype = C.c_int
+    L.bdsm_engine_tail.argtypes = [C.c_void_p, C.c_int, C.c_uint32]
     L.bdsm_version.restype = C.c_char_p
     L.bdsm_version.argtypes = []
     _lib = L
@@ -288,6 +293,25 @@ class Engine:
         if n < 0:
             _raise(-n, self._h)
         return out[:n].tolist()
+
+    def tail(self, query: int, edge: int) -> int:
+        """First level of the independent tail of (query, edge)'s matching order."""
+        t = lib().bdsm_engine_tail(self._h, query, edge)
+        if t < 0:
+            _raise(-t, self._h)
+        return t
+
+    def debug_trace(self) -> dict:
+        """Per-phase matching-kernel trace of the last batch (-DBDSM_TRACE builds)."""
+        out = np.zeros(24 + 64, np.uint64)
+        lib().bdsm_engine_debug_trace(self._h, _ptr(out), out.size)
+        names = ("busy_ns", "max_item_ns", "max_item", "static_items", "donated_items", "t_first", "t_last",
+                 "mx_chunks", "mx_tail_chunks", "mx_big_leaf", "mx_donations", "mx_anchor_deg")
+        r = {ph: dict(zip(names, out[12 * i: 12 * i + 12].tolist())) for i, ph in enumerate(("neg", "pos"))}
+        for i, ph in enumerate(("neg", "pos")):
+            r[ph]["chunks"] = out[24 + 16 * i: 40 + 16 * i].tolist()
+            r[ph]["setups"] = out[56 + 16 * i: 72 + 16 * i].tolist()
+        return r
 
     def column_sizes(self, query: int) -> List[int]:
         out = np.zeros(32, np.uint64)

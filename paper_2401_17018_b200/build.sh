@@ -6,7 +6,8 @@ NVCC="${NVCC:-nvcc}"
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC
        -Xcompiler -fvisibility=hidden -I"$HERE/../include" --expt-relaxed-constexpr -diag-suppress 177
        ${BDSM_NVCC_EXTRA:-})
-OBJ="$HERE/build"
+OBJ="${BDSM_OBJ:-$HERE/build}"
+OUT="${BDSM_OUT:-$HERE/libbdsm_b200.so}"  # BDSM_OUT: alternative library (e.g. -DBDSM_TRACE diagnostics)
 mkdir -p "$OBJ"
 pids=()
 for f in store match engine; do
@@ -16,9 +17,10 @@ done
 g++ -std=c++17 -O3 -fPIC -fvisibility=hidden -I"$HERE/../include" -I/usr/local/cuda/include \
     -c "$HERE/csrc/planner.cpp" -o "$OBJ/planner.o"
 for p in "${pids[@]}"; do wait "$p" || { cat "$OBJ"/*.ptxas.log; exit 1; }; done
-"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o "$HERE/libbdsm_b200.so" \
+"$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o "$OUT" \
     "$OBJ/store.o" "$OBJ/match.o" "$OBJ/engine.o" "$OBJ/planner.o"
-echo "built $HERE/libbdsm_b200.so"
+echo "built $OUT"
+[ -n "${BDSM_OUT:-}" ] && exit 0
 # `bdsm run` CLI (drop-in for the reference's tools/bdsm.cpp), linked against the C ABI
 g++ -std=c++17 -O2 -I"$HERE/../include" "$HERE/csrc/cli.cpp" "$HERE/csrc/textio.cpp" \
     -L"$HERE" -lbdsm_b200 -Wl,-rpath,'$ORIGIN' -o "$HERE/bdsm"

@@ -44,7 +44,21 @@ struct EdgeProg {
   uint32_t query;                // query index
   uint32_t tail;                 // first level T of the independent tail (levels > T are counted, not enumerated)
   uint32_t order[kMaxQ];
+  uint32_t inval[kMaxQ];         // position j -> independent tail levels whose cached count depends on M[j]
+  uint32_t leafmask;             // tail levels that are leaves of level `tail` (weight f(M[tail]))
+  uint32_t singlemask;           // independent tail levels with one backward neighbour j (weight f(M[j]))
+  uint32_t sig[kMaxQ];           // weighted level t: (order[parent] << 4) | order[t], the weight's memo tag
   LevelProg lv[kMaxQ];
+};
+
+// A distinct leaf signature of a query's programs (EdgeProg::sig): the
+// parent query vertex p = order[T] (candidate bit, label id range) and the
+// leaf's level program (candidate bit, label range, edge label in elab[0]).
+struct LeafSig {
+  uint32_t sig;
+  uint32_t pbit;
+  uint32_t plo, phi;
+  LevelProg leaf;
 };
 
 // Anchor-mapping table entry (map_update_to_query_edges, src/matcher.cpp:42-55).
@@ -147,6 +161,14 @@ struct BatchState {
   uint64_t gen_calls;
   uint64_t bytes_phase;
   uint64_t bytes_kernel;         // 4 B x backward degrees of the GenCandidates calls the kernel made
+  // -DBDSM_TRACE builds only, per phase: busy ns summed over items, longest
+  // item ns, its (kind << 8 | start level), static items, donated items,
+  // first item start / last item end (%globaltimer), and for the longest
+  // item: main-loop chunks, tail chunks, warp-counted leaf misses, donations,
+  // anchor endpoint degrees (deg0 << 32 | deg1)
+  uint64_t trace[2][12];
+  uint64_t trace_chunks[2][kMaxQ];  // -DBDSM_TRACE: 32-candidate chunks filtered per level
+  uint64_t trace_setups[2][kMaxQ];  // -DBDSM_TRACE: GenCandidates setups per level
 };
 
 }  // namespace bdsm_b200

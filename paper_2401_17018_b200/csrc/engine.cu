@@ -79,6 +79,10 @@ struct QueryState {
   DBuf<EdgeProg> progs;
   DBuf<AnchorEdge> anchors;
   std::vector<std::vector<uint32_t>> orders;
+  std::vector<uint32_t> tails;  // EdgeProg::tail per query edge
+  bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
+  DBuf<LeafSig> leafsigs;        // distinct leaf signatures (prefill before each launch)
+  uint32_t n_leafsig = 0;
   uint64_t deadline_ns = 0;  // host-steady-clock based, translated per batch
   double deadline_s = 0;     // seconds since epoch of the host steady clock
   bool solved = true;
@@ -127,6 +131,7 @@ struct bdsm_engine {
   DBuf<DynItem> dyn;           // donated-subtree queue of the matching kernel
   DBuf<QueueState> qstate;
   DBuf<uint32_t> dyn_ready;
+  DBuf<unsigned long long> memo;  // leaf-weight memo of the matching kernel (2^21 words)
   uint32_t epoch = 0;
   DBuf<uint8_t> cub_tmp;
   DBuf<BatchState> d_st;
@@ -483,16 +488,42 @@ struct bdsm_engine {
     QueryState& qs = *queries.at(size_t(qi));
     std::vector<uint64_t> cs = column_sizes(qi);
     qs.orders.clear();
+    qs.tails.clear();
+    qs.has_leaf = false;
+    if (!memo.p) memo.ensure(size_t(1) << 21);
     std::vector<EdgeProg> progs;
     std::vector<AnchorEdge> anchors;
+    std::vector<LeafSig> leafsigs;
     std::vector<std::pair<uint32_t, uint32_t>> ranges(qs.q.n);
     for (uint32_t u = 0; u < qs.q.n; ++u) ranges[u] = label_range(qs.q.labels[u]);
     for (uint32_t e = 0; e < qs.q.edges.size(); ++e) {
       qs.orders.push_back(matching_order(qs.q, e, cs));
       progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back(), ranges));
+      qs.tails.push_back(progs.back().tail);
+      const EdgeProg& ep = progs.back();
+      for (uint32_t t = 0; t < ep.n; ++t) {
+        if (!(((ep.leafmask | ep.singlemask) >> t) & 1u)) continue;
+        bool seen = false;
+        for (const LeafSig& ls : leafsigs) seen |= ls.sig == ep.sig[t];
+        if (seen) continue;
+        const uint32_t pq = ep.order[(ep.leafmask >> t) & 1u ? ep.tail : ep.lv[t].back[0]];
+        LeafSig ls{};
+        ls.sig = ep.sig[t];
+        ls.pbit = 1u << pq;
+        ls.plo = ranges[pq].first;
+        ls.phi = ranges[pq].second;
+        ls.leaf = ep.lv[t];
+        leafsigs.push_back(ls);
+      }
       const QEdge& qe = qs.q.edges[e];
       anchors.push_back({qs.q.labels[qe.a], qs.q.labels[qe.b], qe.label, e});
     }
+    qs.has_leaf = !leafsigs.empty();
+    qs.n_leafsig = uint32_t(leafsigs.size());
+    qs.leafsigs.ensure(std::max<size_t>(leafsigs.size(), 1));
+    if (!leafsigs.empty())
+      CK(cudaMemcpyAsync(qs.leafsigs.p, leafsigs.data(), sizeof(LeafSig) * leafsigs.size(), cudaMemcpyHostToDevice,
+                         stream));
     qs.progs.ensure(std::max<size_t>(progs.size(), 1));
     qs.anchors.ensure(std::max<size_t>(anchors.size(), 1));
     if (!progs.empty()) {
@@ -634,6 +665,8 @@ struct bdsm_engine {
     a.dyn_ready = dyn_ready.p;
     a.dyn_cap = uint32_t(dyn.n);
     a.merge_ratio = 8;
+    a.memo = memo.p;
+    a.memo_mask = uint32_t(memo.n - 1);
     return a;
   }
 
@@ -661,6 +694,11 @@ struct bdsm_engine {
       cub_calls += 3;
       if (qs.q.n > 2) {
         CK(cudaEventRecord(next_kev(), stream));
+        if (qs.has_leaf) {
+          CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+          launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, num_sms, stream);
+          ++launches;
+        }
         launch_wbm(a, num_sms, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
@@ -675,6 +713,7 @@ struct bdsm_engine {
 
   BatchState template_state() {
     BatchState s{};
+    s.trace[0][5] = s.trace[1][5] = ~0ull;
     s.selfloop_min = kNone;
     s.conflict_min = kNone;
     s.pool_top = pool_top;
@@ -1048,6 +1087,15 @@ size_t bdsm_last_batch_errors(bdsm_engine* engine, bdsm_update_error* out, size_
   return engine->last_errors.size();
 }
 
+size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size_t cap) {
+  if (!engine || !engine->h_st) return 0;
+  const size_t n = (sizeof(engine->h_st->trace) + sizeof(engine->h_st->trace_chunks) +
+                    sizeof(engine->h_st->trace_setups)) / sizeof(uint64_t);
+  const uint64_t* t = &engine->h_st->trace[0][0];
+  for (size_t i = 0; i < n && i < cap; ++i) out[i] = t[i];
+  return n;
+}
+
 size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, size_t cap) {
   if (!engine || v >= engine->g.V) return 0;
   size_t d = 0;
@@ -1084,6 +1132,13 @@ bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out) {
     for (uint32_t v = 0; v < engine->g.V; ++v) out[v] = rows[engine->new_of[v]] & ~kRowFlags;
     return BDSM_OK;
   });
+}
+
+int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge) {
+  if (!engine || query < 0 || size_t(query) >= engine->queries.size()) return -int(BDSM_INVALID_ARGUMENT);
+  QueryState& qs = *engine->queries[size_t(query)];
+  if (edge >= qs.tails.size()) return -int(BDSM_INVALID_ARGUMENT);
+  return int(qs.tails[edge]);
 }
 
 int bdsm_engine_order(bdsm_engine* engine, int query, uint32_t edge, uint32_t* out) {

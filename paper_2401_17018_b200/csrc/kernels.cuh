@@ -103,10 +103,13 @@ struct PhaseArgs {
   uint32_t dyn_cap;
   uint32_t epoch;
   uint32_t merge_ratio;          // merge-window intersection when |other| <= ratio x |driver|
+  unsigned long long* memo;      // leaf-weight memo (cleared before each launch)
+  uint32_t memo_mask;
 };
 
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);
 void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s);
 void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s);
+void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, int num_sms, cudaStream_t s);
 
 }  // namespace bdsm_b200

@@ -386,31 +386,311 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
 // (1 + Σ_k Π_{T<s<=k} |C_s|), GenCandidates calls and B_phase bytes the
 // reference tree spends below it, so MatchStats-style
 // counters stay those of the reference tree.
+#ifdef BDSM_TRACE
+__device__ uint32_t (*s_dbg)[2];  // per-block shared counters (set by each block; diagnostic builds only)
+#endif
 struct TailFactor {
   unsigned long long f, v, b, c;
 };
 
+// Weight of a leaf level t of T for the level-T candidate x: the number of
+// its candidates, i.e. neighbours c of x in label(order[t])'s id range with
+// candidate bit order[t], the query edge's label, and — only when x is a
+// same-kind batch endpoint — visible under the lowest-order rule.  (c != x
+// always; no other position shares the label, EdgeProg::leafmask.)  Warp-
+// collective over one x.
+__device__ __forceinline__ unsigned long long leaf_count(const PhaseArgs& a, const LevelProg& lp, uint32_t x,
+                                                         bool x_touched, uint32_t anchor, uint32_t flag,
+                                                         uint32_t lane) {
+  const DevGraph& g = a.g;
+  const uint64_t xo = __ldg(g.off + x);
+  const uint32_t xd = __ldg(g.deg + x);
+  uint32_t lo = 0, hi = xd;
+  if (xd > 32) {
+    uint32_t bnd = 0;
+    if (lane < 2) bnd = lb_u32(g.adj + xo, xd, lane ? lp.vhi : lp.vlo);
+    lo = __shfl_sync(kFull, bnd, 0);
+    hi = __shfl_sync(kFull, bnd, 1);
+  }
+  unsigned long long cnt = 0;
+  constexpr uint32_t U = 4;  // chunks in flight
+  for (uint32_t cur = lo; cur < hi; cur += 32 * U) {
+    uint32_t c[U], rw[U];
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      const uint32_t idx = cur + 32 * k + lane;
+      c[k] = idx < hi ? __ldg(g.adj + xo + idx) : kNone;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) rw[k] = c[k] != kNone ? __ldg(a.rows + c[k]) : 0u;
+    uint32_t n = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      const uint32_t idx = cur + 32 * k + lane;
+      bool ok = (rw[k] & lp.qbit) != 0;
+      if (ok && g.elab) ok = __ldg(g.elab + xo + idx) == lp.elab[0];
+      if (ok && x_touched && (rw[k] & flag)) ok = !hidden_edge(a, x, c[k], anchor);
+      n += ok;
+    }
+    cnt += __reduce_add_sync(kFull, n);
+  }
+  return cnt;
+}
+
+// The same count computed by one lane alone (small neighbour lists: the
+// lanes of a warp count their own candidates concurrently).
+__device__ __forceinline__ unsigned long long leaf_count_lane(const PhaseArgs& a, const LevelProg& lp, uint32_t x,
+                                                              uint64_t xo, uint32_t xd, bool x_touched,
+                                                              uint32_t anchor, uint32_t flag) {
+  const DevGraph& g = a.g;
+  const uint32_t* L = g.adj + xo;
+  uint32_t i = lb_u32(L, xd, lp.vlo);
+  unsigned long long cnt = 0;
+  for (; i < xd; ++i) {
+    const uint32_t c = __ldg(L + i);
+    if (c >= lp.vhi) break;
+    const uint32_t rw = __ldg(a.rows + c);
+    bool ok = (rw & lp.qbit) != 0;
+    if (ok && g.elab) ok = __ldg(g.elab + xo + i) == lp.elab[0];
+    if (ok && x_touched && (rw & flag)) ok = !hidden_edge(a, x, c, anchor);
+    cnt += ok;
+  }
+  return cnt;
+}
+
+constexpr uint32_t kLeafLaneMax = 256;  // lists up to this length are counted per lane
+
+// Leaf weights are memoised without the visibility rule; for a level-T
+// candidate x that is a same-kind batch endpoint the hidden edges are then
+// subtracted: the same-kind updates (x, y) with order < anchor whose y passes
+// the leaf's filter (x's segment of the sorted directed batch keys).
+__device__ __forceinline__ unsigned long long hidden_count(const PhaseArgs& a, const LevelProg& lp, uint32_t x,
+                                                           uint32_t anchor) {
+  const unsigned long long k0 = uint64_t(x) << 32;
+  uint32_t i = lb_u64(a.skeys, a.m_keys, k0);
+  unsigned long long n = 0;
+  for (; i < a.m_keys; ++i) {
+    const unsigned long long k = __ldg(a.skeys + i);
+    if ((k >> 32) != x) break;
+    const uint32_t val = __ldg(a.svals + i);
+    const uint32_t ord = val & 0x7fffffffu;
+    if ((val >> 31) != (a.phase == 0 ? 1u : 0u) || ord >= anchor) continue;  // other kind, or not earlier
+    const uint32_t y = uint32_t(k);
+    if (y < lp.vlo || y >= lp.vhi || !(__ldg(a.rows + y) & lp.qbit)) continue;
+    if (a.g.elab) {
+      const uint32_t el = a.phase == 0 ? __ldg(a.dlab + ord) : a.ups[ord].elab;
+      if (el != lp.elab[0]) continue;
+    }
+    ++n;
+  }
+  return n;
+}
+
+// Launch-wide memo of leaf weights: one 64-bit word per (x, sig) =
+// x << 32 | sig << 24 | weight (weights >= 2^24 are not memoised).  Linear
+// probing, bounded; entries are immutable once written, so a racing second
+// insert of the same key is harmless.
+constexpr int kMemoProbes = 8;
+constexpr unsigned long long kMemoEmpty = ~0ull;
+
+__device__ __forceinline__ bool memo_get(const PhaseArgs& a, uint32_t x, uint32_t sig, unsigned long long* w) {
+  const unsigned long long tag = (uint64_t(x) << 32) | (uint64_t(sig) << 24);
+  uint32_t pos = pair_hash(tag) & a.memo_mask;
+  for (int i = 0; i < kMemoProbes; ++i) {
+    const unsigned long long e = __ldcg(a.memo + pos);
+    if (e == kMemoEmpty) return false;
+    if ((e & ~0xffffffull) == tag) {
+      *w = e & 0xffffffull;
+      return true;
+    }
+    pos = (pos + 1) & a.memo_mask;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void memo_put(const PhaseArgs& a, uint32_t x, uint32_t sig, unsigned long long w) {
+  if (w >= (1ull << 24)) return;
+  const unsigned long long tag = (uint64_t(x) << 32) | (uint64_t(sig) << 24);
+  uint32_t pos = pair_hash(tag) & a.memo_mask;
+  for (int i = 0; i < kMemoProbes; ++i) {
+    const unsigned long long prev = atomicCAS(a.memo + pos, kMemoEmpty, tag | w);
+    if (prev == kMemoEmpty || (prev & ~0xffffffull) == tag) return;
+    pos = (pos + 1) & a.memo_mask;
+  }
+}
+
+// Per-lane leaf weight of level t for the lane's level-T candidate c (lanes
+// with `want`): memo hits answer directly, misses are counted one candidate
+// at a time by the whole warp and memoised (candidates that are same-kind
+// batch endpoints depend on the anchor through the visibility rule and are
+// never memoised).
+__device__ __forceinline__ unsigned long long leaf_weight(const PhaseArgs& a, const EdgeProg& P, uint32_t t,
+                                                          uint32_t c, bool tc, bool want, uint32_t anchor,
+                                                          uint32_t flag, uint32_t lane, unsigned long long* stat) {
+  const uint32_t sig = P.sig[t];
+  const LevelProg& lp = P.lv[t];
+  unsigned long long wgt = 0;
+  bool hit = false;
+  if (want) hit = memo_get(a, c, sig, &wgt);
+  // misses on short lists: every lane counts its own candidate
+  bool big = false;
+  if (want && !hit) {
+    const uint32_t xd = __ldg(a.g.deg + c);
+    if (xd <= kLeafLaneMax) {
+      const uint64_t xo = __ldg(a.g.off + c);
+      wgt = leaf_count_lane(a, lp, c, xo, xd, false, anchor, flag);
+      memo_put(a, c, sig, wgt);
+      atomicAdd(stat + 4, 4ull * xd);  // one GenCandidates call made
+    } else {
+      big = true;
+    }
+  }
+  // misses on long lists: the whole warp counts one candidate at a time
+  uint32_t todo = __ballot_sync(kFull, big);
+  while (todo) {
+    const uint32_t k = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t ck = __shfl_sync(kFull, c, k);
+    const unsigned long long wk = leaf_count(a, lp, ck, false, anchor, flag, lane);
+#ifdef BDSM_TRACE
+    if (lane == 0) ++s_dbg[threadIdx.x >> 5][1];
+#endif
+    if (lane == k) wgt = wk;
+    if (lane == 0) {
+      memo_put(a, ck, sig, wk);
+      stat[4] += 4ull * __ldg(a.g.deg + ck);  // one GenCandidates call made
+    }
+  }
+  if (want && tc) wgt -= hidden_count(a, lp, c, anchor);
+  return wgt;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Leaf-weight prefill (before each matching launch of a query with leaf
+// levels): the weights of every long-list vertex that can be a level-T
+// candidate of a leaf signature — label(order[T]), its candidate bit, not a
+// same-kind batch endpoint — computed by the whole grid up front, so no DFS
+// warp counts a hub's list on its critical path.  Warp per 32 consecutive
+// vertex ids of the label range; qualifying lanes are counted one by one.
+__global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig* __restrict__ sigs, uint32_t nsig) {
+  if (batch_aborted(a.st)) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
+  uint64_t total = 0;
+  for (uint32_t si = 0; si < nsig; ++si) total += (uint64_t(sigs[si].phi - sigs[si].plo) + 31) / 32;
+  for (uint64_t gi = warp; gi < total; gi += nwarps) {
+    uint32_t si = 0;
+    uint64_t bi = gi;
+    while (true) {  // map the global block index to (signature, block)
+      const uint64_t nb = (uint64_t(sigs[si].phi - sigs[si].plo) + 31) / 32;
+      if (bi < nb) break;
+      bi -= nb;
+      ++si;
+    }
+    const LeafSig& ls = sigs[si];
+    const uint32_t x = ls.plo + uint32_t(bi) * 32 + lane;
+    bool want = false;
+    if (x < ls.phi) {
+      const uint32_t rw = __ldg(a.rows + x);
+      want = (rw & ls.pbit) && __ldg(a.g.deg + x) > kLeafLaneMax;
+    }
+    uint32_t todo = __ballot_sync(kFull, want);
+    while (todo) {
+      const uint32_t k = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t xk = __shfl_sync(kFull, x, k);
+      const unsigned long long wk = leaf_count(a, ls.leaf, xk, false, 0, flag, lane);
+      if (lane == 0) memo_put(a, xk, ls.sig, wk);
+    }
+  }
+}
+
+// Tail counts are cached per warp: level t's count depends only on the images
+// of its dependency positions (EdgeProg::lv[t].depmask = backward + same-label
+// positions), so it is recomputed only after one of them was reassigned
+// (`tvalid` bit t cleared through EdgeProg::inval).  With the greedy order
+// most tail levels hang off shallow positions and are counted once per item.
 __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& P, uint32_t T, uint32_t w,
                                             const uint32_t* M, uint32_t (*s_floor)[kMaxQ][kFloorB],
                                             uint32_t (*s_ceil)[kMaxQ][kFloorB], uint32_t touched, uint32_t anchor,
                                             uint32_t flag, uint32_t lane, TailFactor* out,
-                                            unsigned long long* stat) {
+                                            unsigned long long* stat, unsigned long long* tcnt, uint32_t* tdeg,
+                                            uint32_t& tvalid) {
   unsigned long long prod = 1, v = 1, b = 0, c = 0;
   for (uint32_t t = T + 1; t < P.n; ++t) {
-    const LevelProg& lp = P.lv[t];
-    const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t]);
-    __syncwarp();
-    b += prod * 4ull * su.deg_sum;  // one call per visit at level t-1
-    c += prod;
-    if (lane == 0) stat[4] += 4ull * su.deg_sum;
-    unsigned long long cnt = 0;
-    for (uint32_t cur = su.lo; cur < su.hi; cur += 32) {
-      uint32_t cc;
-      bool tc;
-      cnt += __popc(filter_chunk(a, lp, M, s_floor[w][t], s_ceil[w][t], su.drv_off, cur, su.hi, su.drv_b, touched,
-                                 anchor, flag, lane, cc, tc));
+    if ((P.leafmask >> t) & 1u) continue;  // leaves of T: weighted per level-T candidate
+    unsigned long long cnt;
+    uint32_t degsum;
+    if ((tvalid >> t) & 1u) {
+      cnt = tcnt[t];
+      degsum = tdeg[t];
+    } else if ((P.singlemask >> t) & 1u) {
+      // one backward neighbour x = M[j]: the memoised weight of x, minus the
+      // edges the lowest-order rule hides when x is a same-kind batch endpoint
+      const LevelProg& lp = P.lv[t];
+      const uint32_t j = lp.back[0];
+      const uint32_t x = M[j];
+      degsum = __ldg(a.g.deg + x);
+      unsigned long long wx = 0;
+      bool hit = false;
+      if (lane == 0) hit = memo_get(a, x, P.sig[t], &wx);
+      hit = __shfl_sync(kFull, uint32_t(hit), 0) != 0;
+      if (!hit) {
+        wx = leaf_count(a, lp, x, false, anchor, flag, lane);
+        if (lane == 0) {
+          memo_put(a, x, P.sig[t], wx);
+          stat[4] += 4ull * degsum;
+        }
+      }
+      if ((touched >> j) & 1u) {
+        unsigned long long h = 0;
+        if (lane == 0) h = hidden_count(a, lp, x, anchor);
+        wx -= h;
+      }
+      cnt = __shfl_sync(kFull, wx, 0);
+      if (lane == 0) {
+        tcnt[t] = cnt;
+        tdeg[t] = degsum;
+      }
+      tvalid |= 1u << t;
+    } else {
+      const LevelProg& lp = P.lv[t];
+      const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t]);
       __syncwarp();
+#ifdef BDSM_TRACE
+      if (lane == 0) {
+        atomicAdd((unsigned long long*)&a.st->trace_setups[a.phase][t], 1ull);
+        atomicAdd((unsigned long long*)&a.st->trace_chunks[a.phase][t], (unsigned long long)((su.hi - su.lo + 31) / 32));
+      }
+#endif
+      degsum = su.deg_sum;
+      if (lane == 0) stat[4] += 4ull * su.deg_sum;
+      cnt = 0;
+      for (uint32_t cur = su.lo; cur < su.hi; cur += 32) {
+        uint32_t cc;
+        bool tc;
+        cnt += __popc(filter_chunk(a, lp, M, s_floor[w][t], s_ceil[w][t], su.drv_off, cur, su.hi, su.drv_b, touched,
+                                   anchor, flag, lane, cc, tc));
+#ifdef BDSM_TRACE
+        if (lane == 0) ++s_dbg[w][0];
+#endif
+        __syncwarp();
+      }
+      if (lane == 0) {
+        tcnt[t] = cnt;
+        tdeg[t] = degsum;
+      }
+      tvalid |= 1u << t;
     }
+    b += prod * 4ull * degsum;  // one call per visit at level t-1
+    c += prod;
     prod *= cnt;
     v += prod;
     if (prod == 0) break;  // the reference tree has no deeper nodes either
@@ -428,6 +708,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
   __shared__ uint32_t s_ceil[kWarpsPerBlock][kMaxQ][kFloorB];
   __shared__ TailFactor s_tail[kWarpsPerBlock];
+  __shared__ unsigned long long s_tcnt[kWarpsPerBlock][kMaxQ];  // cached tail-level counts
+  __shared__ uint32_t s_tdeg[kWarpsPerBlock][kMaxQ];
+#ifdef BDSM_TRACE
+  __shared__ uint32_t s_dbg_[kWarpsPerBlock][2];
+  s_dbg = s_dbg_;
+#endif
   // per-warp counters (lane 0 updates them; kept out of the register budget)
   __shared__ unsigned long long s_stat[kWarpsPerBlock][5];  // count, visits, bytes, calls, kernel bytes
   if (batch_aborted(a.st)) return;
@@ -500,6 +786,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     kind = __shfl_sync(kFull, kind, 0);
     ref = __shfl_sync(kFull, ref, 0);
     if (kind == 3) break;
+#ifdef BDSM_TRACE
+    const uint64_t t_item = globaltimer();
+    uint32_t it_chunks = 0, it_don = 0;
+    s_dbg[w][0] = s_dbg[w][1] = 0;
+#endif
     uint32_t task_id, lstart, rbegin, rend, ncand = 0;
     if (kind == 1) {
       const Item item = a.items[ref];
@@ -528,6 +819,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     const EdgeProg& P = a.progs[task.prog];
     const uint32_t anchor = task.upd;
     const uint32_t T = P.tail;  // deepest DFS level; deeper levels are counted by tail_factor
+    uint32_t tvalid = 0;        // tail levels whose cached count is current
     if (kind == 1) {
       const bdsm_update_dev up = a.ups[task.upd];
       const uint32_t m0 = task.flip ? up.v : up.u, m1 = task.flip ? up.u : up.v;
@@ -561,7 +853,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         c_cur = c_end = 0;
         c_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
       }
-      if (lstart == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat);
+      if (lstart == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
+                                 s_tcnt[w], s_tdeg[w], tvalid);
     }
     uint32_t l = lstart;
     while (true) {
@@ -647,6 +940,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
                   atomicExch(a.dyn_ready + slot, a.epoch);
                   atomicAdd(&st->donations, 1u);
                 }
+#ifdef BDSM_TRACE
+                ++it_don;
+#endif
                 c_end = __shfl_sync(kFull, r_end, l);  // shrinks when j == l
               }
             }
@@ -654,10 +950,47 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         }
         const uint32_t cur = c_cur;
         c_cur += 32;
+#ifdef BDSM_TRACE
+        if (lane == 0) atomicAdd((unsigned long long*)&st->trace_chunks[a.phase][l], 1ull);
+        ++it_chunks;
+#endif
         uint32_t c;
         bool tc;
         const uint32_t m = filter_chunk(a, P.lv[l], s_M[w], s_floor[w][l], s_ceil[w][l], c_off, cur, c_end, c_drv,
                                         touched, anchor, flag, lane, c, tc);
+        if (l == T && P.leafmask && m) {
+          // last DFS level with leaves of T: per-survivor weights; each lane
+          // walks the tail levels for its own reference-tree counters
+          const bool ok = (m >> lane) & 1u;
+          unsigned long long prod = ok ? 1ull : 0ull, vis = prod, bb = 0, cc = 0;
+          const uint32_t degc = ok ? __ldg(g.deg + c) : 0u;
+          for (uint32_t t = T + 1; t < P.n; ++t) {
+            unsigned long long cnt;
+            uint32_t dsum;
+            if ((P.leafmask >> t) & 1u) {
+              cnt = leaf_weight(a, P, t, c, tc, ok && prod != 0, anchor, flag, lane, stat);
+              dsum = degc;
+            } else {
+              cnt = s_tcnt[w][t];
+              dsum = s_tdeg[w][t];
+            }
+            bb += prod * 4ull * dsum;
+            cc += prod;
+            prod *= cnt;
+            vis += prod;
+          }
+          prod = warp_sum_u64(prod);
+          vis = warp_sum_u64(vis);
+          bb = warp_sum_u64(bb);
+          cc = warp_sum_u64(cc);
+          if (lane == 0) {
+            stat[0] += prod;
+            stat[1] += vis;
+            stat[2] += bb;
+            stat[3] += cc;
+          }
+          continue;
+        }
         if (l == T) {  // last DFS level: every survivor roots the counted tail
           const unsigned long long pm = __popc(m);
           if (pm && lane == 0) {
@@ -679,6 +1012,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         c_mask &= c_mask - 1;
         const uint32_t c = s_cand[w][l][k];
         if (lane == 0) s_M[w][l] = c;
+        tvalid &= ~P.inval[l];
         touched |= ((c_tmask >> k) & 1u) << l;
         if (lane == l) {  // park level l
           r_off = c_off;
@@ -697,6 +1031,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
           stat[2] += 4ull * su.deg_sum;
           stat[3] += 1;
           stat[4] += 4ull * su.deg_sum;
+#ifdef BDSM_TRACE
+          atomicAdd((unsigned long long*)&st->trace_setups[a.phase][l], 1ull);
+#endif
         }
         c_off = su.drv_off;
         c_cur = su.lo;
@@ -704,10 +1041,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         c_mask = 0;
         c_drv = su.drv_b;
         c_tmask = 0;
-        if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat);
+        if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
+                                 s_tcnt[w], s_tdeg[w], tvalid);
       }
     }
     if (lane == 0) atomicSub(&a.q->holders.v, 1u);
+#ifdef BDSM_TRACE
+    if (lane == 0) {
+      const uint64_t t1 = globaltimer(), dt = t1 - t_item;
+      unsigned long long* tr = (unsigned long long*)st->trace[a.phase];
+      atomicAdd(tr + 0, (unsigned long long)dt);
+      const unsigned long long prev = atomicMax(tr + 1, (unsigned long long)dt);
+      if (dt > prev) {  // racy, diagnostic only
+        tr[2] = (kind << 8) | lstart;
+        tr[7] = it_chunks;
+        tr[8] = s_dbg[w][0];
+        tr[9] = s_dbg[w][1];
+        tr[10] = it_don;
+        tr[11] = (uint64_t(__ldg(g.deg + s_M[w][0])) << 32) | __ldg(g.deg + s_M[w][1]);
+      }
+      atomicAdd(tr + (kind == 1 ? 3 : 4), 1ull);
+      atomicMin(tr + 5, (unsigned long long)t_item);
+      atomicMax(tr + 6, (unsigned long long)t1);
+    }
+#endif
     if (timed_out) break;
   }
   __syncwarp();
@@ -732,6 +1089,10 @@ void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s) {
   unsigned blocks = unsigned((uint64_t(a.n_ups) + 255) / 256);
   if (blocks == 0) blocks = 1;
   k_anchor_emit<<<blocks, 256, 0, s>>>(a);
+}
+
+void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, int num_sms, cudaStream_t s) {
+  if (nsig) k_leaf_prefill<<<unsigned(num_sms * 8), 256, 0, s>>>(a, sigs, nsig);
 }
 
 void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s) {

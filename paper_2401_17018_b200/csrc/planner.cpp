@@ -122,21 +122,48 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
       if (q.labels[order[j]] == q.labels[u]) lp.eqmask |= 1u << j;
     }
   }
-  // Independent tail: the smallest T >= 2 such that every level t >= T has
-  // all its backward neighbours before T (no query edge inside the tail) and
-  // the tail's labels are pairwise distinct (no injectivity between tail
-  // vertices).  Given M[0..T) the tail levels' candidate sets are then
-  // independent, so the kernel counts each once and multiplies.
-  auto independent = [&](uint32_t t0) {
-    for (uint32_t t = t0; t < q.n; ++t) {
-      if (p.lv[t].backmask >> t0) return false;
-      for (uint32_t s = t0; s < t; ++s)
-        if (q.labels[order[s]] == q.labels[order[t]]) return false;
+  // Counted tail.  T is the deepest level the kernel enumerates; every level
+  // t > T is counted instead, and must be either
+  //  * independent: all backward neighbours before T and no same-label
+  //    position at or after T — its candidate set depends only on M[0..T),
+  //    so its count is computed once per prefix (cached per warp) and
+  //    multiplied; or
+  //  * a leaf of T: T is its only backward neighbour and its only possible
+  //    same-label position — its count is a function of M[T] alone, the
+  //    per-vertex weight f(M[T]) memoised across the launch.
+  // Tail levels are pairwise non-adjacent (by construction) and carry
+  // pairwise distinct labels, so no injectivity couples them.
+  auto counted = [&](uint32_t T) {
+    for (uint32_t t = T + 1; t < q.n; ++t) {
+      const LevelProg& lp = p.lv[t];
+      const bool indep = (lp.backmask >> T) == 0 && (lp.eqmask >> T) == 0;
+      const bool leaf = lp.backmask == (1u << T) && (lp.eqmask & ~(1u << T)) == 0;
+      if (!indep && !leaf) return false;
+      for (uint32_t s2 = T + 1; s2 < t; ++s2)
+        if (q.labels[order[s2]] == q.labels[order[t]]) return false;
     }
     return true;
   };
   p.tail = q.n >= 3 ? q.n - 1 : 0;
-  while (p.tail > 2 && independent(p.tail - 1)) --p.tail;
+  while (p.tail > 2 && counted(p.tail - 1)) --p.tail;
+  p.leafmask = 0;
+  for (uint32_t t = p.tail + 1; t < q.n; ++t) {
+    const LevelProg& lp = p.lv[t];
+    if ((lp.backmask >> p.tail) != 0) {  // leaf of T: weight memoised per M[T]
+      p.leafmask |= 1u << t;
+      p.sig[t] = (order[p.tail] << 4) | order[t];
+      continue;
+    }
+    const uint32_t dep = lp.backmask | lp.eqmask;  // what level t's candidate set depends on
+    for (uint32_t j = 0; j < q.n; ++j)
+      if ((dep >> j) & 1u) p.inval[j] |= 1u << t;
+    // a single backward neighbour j (and no other same-label position): the
+    // count is the memoised per-vertex weight of M[j], like a leaf of T
+    if (lp.nback == 1 && (lp.eqmask & ~lp.backmask) == 0) {
+      p.singlemask |= 1u << t;
+      p.sig[t] = (order[lp.back[0]] << 4) | order[t];
+    }
+  }
   return p;
 }
 
