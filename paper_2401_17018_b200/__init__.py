@@ -303,14 +303,15 @@ class Engine:
 
     def debug_trace(self) -> dict:
         """Per-phase matching-kernel trace of the last batch (-DBDSM_TRACE builds)."""
-        out = np.zeros(24 + 64, np.uint64)
+        out = np.zeros(32 + 64, np.uint64)
         lib().bdsm_engine_debug_trace(self._h, _ptr(out), out.size)
         names = ("busy_ns", "max_item_ns", "max_item", "static_items", "donated_items", "t_first", "t_last",
-                 "mx_chunks", "mx_tail_chunks", "mx_big_leaf", "mx_donations", "mx_anchor_deg")
-        r = {ph: dict(zip(names, out[12 * i: 12 * i + 12].tolist())) for i, ph in enumerate(("neg", "pos"))}
+                 "mx_chunks", "mx_tail_chunks", "mx_big_leaf", "mx_donations", "mx_anchor_deg",
+                 "mx_cy_donate", "mx_cy_filter", "mx_cy_leaf", "mx_cy_setup")
+        r = {ph: dict(zip(names, out[16 * i: 16 * i + 16].tolist())) for i, ph in enumerate(("neg", "pos"))}
         for i, ph in enumerate(("neg", "pos")):
-            r[ph]["chunks"] = out[24 + 16 * i: 40 + 16 * i].tolist()
-            r[ph]["setups"] = out[56 + 16 * i: 72 + 16 * i].tolist()
+            r[ph]["chunks"] = out[32 + 16 * i: 48 + 16 * i].tolist()
+            r[ph]["setups"] = out[64 + 16 * i: 80 + 16 * i].tolist()
         return r
 
     def column_sizes(self, query: int) -> List[int]:

@@ -165,8 +165,9 @@ struct BatchState {
   // item ns, its (kind << 8 | start level), static items, donated items,
   // first item start / last item end (%globaltimer), and for the longest
   // item: main-loop chunks, tail chunks, warp-counted leaf misses, donations,
-  // anchor endpoint degrees (deg0 << 32 | deg1)
-  uint64_t trace[2][12];
+  // anchor endpoint degrees (deg0 << 32 | deg1), SM cycles spent donating,
+  // filtering chunks, weighting leaves, in setups (incl. tail factors)
+  uint64_t trace[2][16];
   uint64_t trace_chunks[2][kMaxQ];  // -DBDSM_TRACE: 32-candidate chunks filtered per level
   uint64_t trace_setups[2][kMaxQ];  // -DBDSM_TRACE: GenCandidates setups per level
 };

@@ -596,7 +596,7 @@ struct bdsm_engine {
     cost_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
     size_t hcap = 1024;
-    while (hcap < 4 * cap_n) hcap <<= 1;  // >= 2x the 2|dB| directed keys
+    while (hcap < 8 * cap_n) hcap <<= 1;  // >= 2x the 2|dB| directed keys + <= 2|dB| segment heads
     hkeys.ensure(hcap);
     hvals.ensure(hcap);
     batch_cap = cap_n;

@@ -212,6 +212,7 @@ __device__ __forceinline__ uint32_t dyn_reserve(QueueState* q, uint32_t cap) {
   return t;
 }
 
+constexpr uint32_t kSplitMin = 2;  // driver entries a parked range needs to be split for donation
 constexpr int kFloorB = 8;  // backward lists per level with a tracked search floor
 
 // Membership of each lane's candidate c in the sorted list L[0, n), for
@@ -466,8 +467,19 @@ constexpr uint32_t kLeafLaneMax = 256;  // lists up to this length are counted p
 // the leaf's filter (x's segment of the sorted directed batch keys).
 __device__ __forceinline__ unsigned long long hidden_count(const PhaseArgs& a, const LevelProg& lp, uint32_t x,
                                                            uint32_t anchor) {
-  const unsigned long long k0 = uint64_t(x) << 32;
-  uint32_t i = lb_u64(a.skeys, a.m_keys, k0);
+  // x's segment start from the visibility table's (x, kNone) entry
+  const unsigned long long hk = (uint64_t(x) << 32) | kNone;
+  uint32_t pos = pair_hash(hk) & a.hmask;
+  uint32_t i = a.m_keys;
+  while (true) {
+    const unsigned long long k = __ldg(a.hkeys + pos);
+    if (k == hk) {
+      i = __ldg(a.hvals + pos);
+      break;
+    }
+    if (k == kEmptyKey) break;
+    pos = (pos + 1) & a.hmask;
+  }
   unsigned long long n = 0;
   for (; i < a.m_keys; ++i) {
     const unsigned long long k = __ldg(a.skeys + i);
@@ -726,6 +738,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   if ((threadIdx.x & 31) < 5) stat[threadIdx.x & 31] = 0;
   __syncwarp();
   uint32_t dtick = 0;
+  unsigned long long tt_pref = 0;  // prefetched donation-demand poll
   bool timed_out = false;
   bool static_done = false;
   uint32_t ticket = kNone;  // lane 0: outstanding ticket of this warp
@@ -789,6 +802,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
 #ifdef BDSM_TRACE
     const uint64_t t_item = globaltimer();
     uint32_t it_chunks = 0, it_don = 0;
+    long long cy_don = 0, cy_filter = 0, cy_leaf = 0, cy_setup = 0, cy0 = 0;
     s_dbg[w][0] = s_dbg[w][1] = 0;
 #endif
     uint32_t task_id, lstart, rbegin, rend, ncand = 0;
@@ -875,27 +889,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         // (upper half of the remaining driver range, or of the remaining
         // candidates of an already-fetched chunk); the deadline is polled on
         // the same cadence.
-        if (((++dtick) & 7u) == 0) {
-          if (a.deadline_ns && (dtick & 255u) == 0 &&
+        {
+          if (a.deadline_ns && ((++dtick) & 255u) == 0 &&
               __shfl_sync(kFull, uint32_t(globaltimer() > a.deadline_ns), 0)) {
             timed_out = true;
             break;
           }
-          // demand: tickets handed out beyond the slots reserved so far
-          const unsigned long long tt =
-              *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
+          // demand: tickets handed out beyond the slots reserved so far.  The
+          // poll is issued one chunk fetch ahead so its L2 round trip overlaps
+          // the chunk's filtering.
+          const unsigned long long tt = tt_pref;
+          tt_pref = *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
           if (int32_t(uint32_t(tt) - uint32_t(tt >> 32)) > 0) {
             if (lane == l) {  // park the current level: the stack now covers [lstart, l]
               r_cur = c_cur;
               r_end = c_end;
               r_mask = 0;
             }
-            bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= 64;
+            bool can_r = lane >= lstart && lane <= l && r_end > r_cur && (r_end - r_cur) >= kSplitMin;
             bool can_m = lane >= lstart && lane < l && __popc(r_mask) >= 2;
             uint32_t cb = __ballot_sync(kFull, can_r || can_m);
             if (cb) {
               uint32_t j = __ffs(cb) - 1;
               bool by_range = (__ballot_sync(kFull, can_r) >> j) & 1u;
+#ifdef BDSM_TRACE
+              cy0 = clock64();
+#endif
               uint32_t slot = 0;
               if (lane == 0) slot = dyn_reserve(a.q, a.dyn_cap);
               slot = __shfl_sync(kFull, slot, 0);
@@ -943,8 +962,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
 #ifdef BDSM_TRACE
                 ++it_don;
 #endif
-                c_end = __shfl_sync(kFull, r_end, l);  // shrinks when j == l
               }
+#ifdef BDSM_TRACE
+              cy_don += clock64() - cy0;
+#endif
+              c_end = __shfl_sync(kFull, r_end, l);  // shrinks when j == l
             }
           }
         }
@@ -956,8 +978,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
 #endif
         uint32_t c;
         bool tc;
+#ifdef BDSM_TRACE
+        cy0 = clock64();
+#endif
         const uint32_t m = filter_chunk(a, P.lv[l], s_M[w], s_floor[w][l], s_ceil[w][l], c_off, cur, c_end, c_drv,
                                         touched, anchor, flag, lane, c, tc);
+#ifdef BDSM_TRACE
+        cy_filter += clock64() - cy0;
+        cy0 = clock64();
+#endif
         if (l == T && P.leafmask && m) {
           // last DFS level with leaves of T: per-survivor weights; each lane
           // walks the tail levels for its own reference-tree counters
@@ -989,6 +1018,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
             stat[2] += bb;
             stat[3] += cc;
           }
+#ifdef BDSM_TRACE
+          cy_leaf += clock64() - cy0;
+#endif
           continue;
         }
         if (l == T) {  // last DFS level: every survivor roots the counted tail
@@ -1026,6 +1058,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         ++l;
         // GenCandidates for level l: driver = smallest backward list, range =
         // its label sub-range
+#ifdef BDSM_TRACE
+        cy0 = clock64();
+#endif
         const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l]);
         if (lane == 0) {
           stat[2] += 4ull * su.deg_sum;
@@ -1043,6 +1078,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         c_tmask = 0;
         if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
                                  s_tcnt[w], s_tdeg[w], tvalid);
+#ifdef BDSM_TRACE
+        cy_setup += clock64() - cy0;
+#endif
       }
     }
     if (lane == 0) atomicSub(&a.q->holders.v, 1u);
@@ -1058,6 +1096,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         tr[8] = s_dbg[w][0];
         tr[9] = s_dbg[w][1];
         tr[10] = it_don;
+        tr[12] = cy_don;
+        tr[13] = cy_filter;
+        tr[14] = cy_leaf;
+        tr[15] = cy_setup;
         tr[11] = (uint64_t(__ldg(g.deg + s_M[w][0])) << 32) | __ldg(g.deg + s_M[w][1]);
       }
       atomicAdd(tr + (kind == 1 ? 3 : 4), 1ull);

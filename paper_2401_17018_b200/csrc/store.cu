@@ -200,15 +200,19 @@ __global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* 
     insflag[j] = is_del ? 0u : 1u;
     if (src < V)
       for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? kRowDelFlag : kRowInsFlag);
-    // visibility table: linear probing (duplicates only in rejected batches)
-    uint32_t pos = pair_hash(k) & hmask;
-    for (uint32_t probe = 0; probe <= hmask; ++probe) {
-      unsigned long long prev = atomicCAS(hkeys + pos, kEmptyKey, (unsigned long long)k);
-      if (prev == kEmptyKey || prev == k) {
-        hvals[pos] = val;
-        break;
+    // visibility table: linear probing (duplicates only in rejected batches);
+    // segment heads also map (src, kNone) -> the segment's first index
+    for (int pass = 0; pass < (h ? 2 : 1); ++pass) {
+      const unsigned long long key = pass ? ((uint64_t(src) << 32) | kNone) : (unsigned long long)k;
+      uint32_t pos = pair_hash(key) & hmask;
+      for (uint32_t probe = 0; probe <= hmask; ++probe) {
+        unsigned long long prev = atomicCAS(hkeys + pos, kEmptyKey, key);
+        if (prev == kEmptyKey || prev == key) {
+          hvals[pos] = pass ? j : val;
+          break;
+        }
+        pos = (pos + 1) & hmask;
       }
-      pos = (pos + 1) & hmask;
     }
   }
 }

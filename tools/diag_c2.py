@@ -47,7 +47,9 @@ def main():
                       f"static {t['static_items']} donated {t['donated_items']}")
                 dg = t["mx_anchor_deg"]
                 print(f"      longest item: chunks {t['mx_chunks']} tail chunks {t['mx_tail_chunks']} "
-                      f"big leaf misses {t['mx_big_leaf']} donations {t['mx_donations']} anchor deg {dg >> 32}/{dg & 0xffffffff}")
+                      f"big leaf misses {t['mx_big_leaf']} donations {t['mx_donations']} anchor deg {dg >> 32}/{dg & 0xffffffff} "
+                      f"us: donate {t['mx_cy_donate']/1965:.0f} filter {t['mx_cy_filter']/1965:.0f} "
+                      f"leaf {t['mx_cy_leaf']/1965:.0f} setup {t['mx_cy_setup']/1965:.0f}")
                 print(f"      chunks/level {t['chunks'][:len(wl.qlabels)]} setups/level {t['setups'][:len(wl.qlabels)]}")
 
 
