@@ -282,10 +282,32 @@ def ours(args, world, rank, local):
 
     statsA = []
     dev_ms = []
+    nccl_totals = []
+    use_nccl = world > 1 and __import__("torch.distributed").distributed.get_backend() == "nccl"
     with ClockSampler(local if not os.environ.get("CUDA_VISIBLE_DEVICES") else 0) as clk:
         for i in range(args.warmup, nb):
             flush.zero_()
             barrier()
+            if use_nccl:
+                # multi-GPU step: NCCL broadcast of the batch
+                # from rank 0, each rank applies it to its replica and counts its
+                # share of the work units, NCCL all-reduce of the counts; device
+                # time from CUDA events around the whole step
+                import torch.distributed as dist
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                dist.broadcast(dev_batches[i], src=0)
+                torch.cuda.current_stream().synchronize()
+                r = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
+                cnt = torch.tensor([r.positive[0], r.negative[0]], dtype=torch.int64, device=dev)
+                dist.all_reduce(cnt)
+                ev1.record()
+                ev1.synchronize()
+                dev_ms.append(ev0.elapsed_time(ev1))
+                statsA.append(r.stats)
+                countsA.append((r.positive[0], r.negative[0]))  # this rank's share
+                nccl_totals.append(tuple(cnt.tolist()))
+                continue
             r = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
             dev_ms.append(r.stats["ms_device"])
             statsA.append(r.stats)
@@ -311,6 +333,8 @@ def ours(args, world, rank, local):
     value = updates / (tot_dev / 1e3)
     e2e_value = updates / (tot_e2e / 1e3)
     parity_ok = flatA == flatB
+    if nccl_totals:  # the in-step NCCL all-reduce agrees with the end-of-run sum
+        parity_ok = parity_ok and [c for pn in nccl_totals for c in pn] == flatA[2 * args.warmup:]
 
     # roofline of the dominant kernel (mean over the timed steps)
     peak, peak_kind = peaks()

@@ -173,6 +173,16 @@ BDSM_API bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query);
  * Pure host function, used by the engine and by the CPU tests. */
 BDSM_API void bdsm_shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);
 
+/* Bounded match materialisation (the reference's match vectors, for
+ * --dump-matches, src/bench.cpp:484-491): with cap > 0 every later batch also
+ * records up to `cap` matches per (query, phase); 0 returns to counts only. */
+BDSM_API bdsm_status bdsm_engine_collect_matches(bdsm_engine* engine, uint64_t cap);
+/* Matches of the last batch for (query, phase: 0 negative, 1 positive), in
+ * external ids, query vertex order, sorted ascending (src/matcher.cpp:365-366);
+ * copies up to `cap` matches (num_vertices words each) and returns the total
+ * number of matches (> collected when the engine's cap was exceeded), or -status. */
+BDSM_API int64_t bdsm_engine_matches(bdsm_engine* engine, int query, int phase, uint32_t* out, size_t cap);
+
 /* Diagnostics of -DBDSM_TRACE builds: per-phase matching-kernel trace words
  * of the last batch (zeros otherwise).  Returns the number of words. */
 BDSM_API size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size_t cap);

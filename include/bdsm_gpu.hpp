@@ -151,6 +151,18 @@ class Engine {
     out.resize(n);
     return out;
   }
+  // Bounded match materialisation for later batches (0: counts only).
+  void collect_matches(std::uint64_t cap) { check(bdsm_engine_collect_matches(e_, cap)); }
+  // Matches of the last batch for (query, phase 0 negative / 1 positive),
+  // flattened num_vertices words each, sorted; throws when they were truncated.
+  std::vector<std::uint32_t> matches(int query, int phase, std::uint32_t num_vertices) {
+    std::int64_t total = bdsm_engine_matches(e_, query, phase, nullptr, 0);
+    if (total < 0) check(bdsm_status(-total));
+    std::vector<std::uint32_t> out(std::size_t(total) * num_vertices);
+    std::int64_t again = bdsm_engine_matches(e_, query, phase, out.data(), std::size_t(total));
+    if (again < 0) check(bdsm_status(-again));
+    return out;
+  }
   std::uint32_t vertex_count() const { return bdsm_engine_num_vertices(e_); }
   std::uint64_t edge_count() const { return bdsm_engine_num_edges(e_); }
   std::size_t query_count() const { return nq_; }

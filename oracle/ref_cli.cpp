@@ -8,7 +8,8 @@
 // by tests/golden/make_cli_golden.sh to produce the CLI fixtures the B200
 // CLI is checked against.
 //
-//   ref_cli GRAPH (q:FILE | g:cat,size,count) (s:FILE | s:rate,mode,batches[,k]) SEED OUTDIR
+//   ref_cli GRAPH (q:FILE | g:cat,size,count) (s:FILE | s:rate,mode,batches[,k]) SEED OUTDIR [dump]
+//   (dump: --dump-matches, matches_batch<i>.txt in OUTDIR)
 #include <filesystem>
 #include <fstream>
 #include <iostream>
@@ -30,7 +31,7 @@ std::vector<std::string> csv(const std::string& s) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc != 6) {
+  if (argc != 6 && argc != 7) {
     std::cerr << "usage: ref_cli GRAPH q:FILE|g:cat,size,count s:FILE|s:rate,mode,batches[,k] SEED OUT\n";
     return 2;
   }
@@ -76,6 +77,7 @@ int main(int argc, char** argv) {
     bdsm::PipelineConfig config;
     config.match.coalesce = false;
     config.query_categories = cats;
+    if (argc == 7) config.dump_matches_dir = out;
     bdsm::RunReport report = bdsm::run_pipeline(g, queries, stream, config);
     bdsm::emit_report(report, out);
     std::size_t pos = 0, neg = 0, unsolved = 0;

@@ -118,6 +118,10 @@ def _load():
     L.bdsm_shard_owners.argtypes = [C.c_void_p, C.c_size_t, C.c_uint32, C.c_void_p]
     L.bdsm_engine_debug_trace.restype = C.c_size_t
     L.bdsm_engine_debug_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.bdsm_engine_collect_matches.restype = C.c_int
+    L.bdsm_engine_collect_matches.argtypes = [C.c_void_p, C.c_uint64]
+    L.bdsm_engine_matches.restype = C.c_int64
+    L.bdsm_engine_matches.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]
     L.bdsm_engine_tail.restype = C.c_int
     L.bdsm_engine_tail.argtypes = [C.c_void_p, C.c_int, C.c_uint32]
     L.bdsm_version.restype = C.c_char_p
@@ -293,6 +297,24 @@ class Engine:
         if n < 0:
             _raise(-n, self._h)
         return out[:n].tolist()
+
+    def collect_matches(self, cap: int) -> None:
+        """Materialise up to `cap` matches per (query, phase) for later batches (0: counts only)."""
+        r = lib().bdsm_engine_collect_matches(self._h, cap)
+        if r != 0:
+            _raise(r, self._h)
+
+    def matches(self, query: int, positive: bool) -> np.ndarray:
+        """The last batch's matches of `query` (external ids, query vertex order, sorted)."""
+        n = self.query_sizes[query]
+        total = lib().bdsm_engine_matches(self._h, query, 1 if positive else 0, None, 0)
+        if total < 0:
+            _raise(int(-total), self._h)
+        out = np.zeros((total, n), np.uint32)
+        got = lib().bdsm_engine_matches(self._h, query, 1 if positive else 0, _ptr(out), total)
+        if got < 0:
+            _raise(int(-got), self._h)
+        return out
 
     def tail(self, query: int, edge: int) -> int:
         """First level of the independent tail of (query, edge)'s matching order."""

@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -186,9 +187,8 @@ int run(const Args& args) {
   if (args.coalesce != "on" && args.coalesce != "off") throw std::invalid_argument("--coalesce wants on|off");
   if (args.coalesce == "on")
     std::cerr << "note: coalesced search is not exact in the reference (SURVEY.md F1); running the exact search\n";
-  if (!args.dump_plan.empty() || args.dump_matches)
-    throw std::runtime_error(std::string(args.dump_matches ? "--dump-matches" : "--dump-plan") +
-                             " is not supported by the GPU build (counts only)");
+  if (!args.dump_plan.empty())
+    throw std::runtime_error("--dump-plan is not supported by the GPU build (plan_to_json is a debug dump)");
 
   bdsm::text::Graph g = bdsm::text::load_graph_file(args.graph);
   if (args.generate_only) return generate(args, g);
@@ -227,6 +227,10 @@ int run(const Args& args) {
     throw std::runtime_error("need --stream or --gen-stream");
   }
 
+  // --dump-matches: bounded materialisation (BDSM_DUMP_CAP matches per query and phase)
+  const char* capenv = std::getenv("BDSM_DUMP_CAP");
+  const std::uint64_t dump_cap = capenv ? std::strtoull(capenv, nullptr, 10) : (1ull << 22);
+  if (args.dump_matches) engine.collect_matches(dump_cap);
   std::vector<int> qid(queries.size());
   for (std::size_t i = 0; i < queries.size(); ++i) {
     auto t0 = Clock::now();
@@ -279,6 +283,24 @@ int run(const Args& args) {
       if (double(del) / double(std::max<std::uint64_t>(tot, 1)) > 0.25) {
         engine.replan(qid[i]);
         q.plan_cols = now;
+      }
+    }
+    if (args.dump_matches) {  // src/bench.cpp:484-491 (format_match, src/matcher.cpp:391-398)
+      mkdirs(args.out);
+      std::ofstream mf(join(args.out, "matches_batch" + std::to_string(bi) + ".txt"));
+      for (std::size_t i = 0; i < queries.size(); ++i) {
+        if (!queries[i].solved) continue;
+        const std::uint32_t n = std::uint32_t(queries[i].q.labels.size());
+        for (int phase : {1, 0}) {
+          const std::vector<std::uint32_t> m = engine.matches(qid[i], phase, n);
+          if (m.size() / std::max<std::uint32_t>(n, 1) > dump_cap)
+            throw std::runtime_error("too many matches to dump (raise BDSM_DUMP_CAP)");
+          for (std::size_t k = 0; k + n <= m.size(); k += n) {
+            mf << (phase ? '+' : '-');
+            for (std::uint32_t u = 0; u < n; ++u) mf << " u" << u << ":v" << m[k + u];
+            mf << '\n';
+          }
+        }
       }
     }
     deltas.push_back(d);

@@ -23,7 +23,34 @@ struct DevGraph {
   const uint32_t* adj;
   const uint32_t* elab;    // parallel to adj, or nullptr when no edge labels exist
   const uint32_t* vlabel;
+  // Label index: loff[v * (nlab + 1) + k] = position in v's list of the first
+  // neighbour of label class >= k (ids are label-ordered), so a label
+  // sub-range is two loads instead of two binary searches; nullptr when the
+  // graph has more than kMaxLabelIndex label classes.
+  const uint32_t* loff;
+  uint32_t nlab;
 };
+
+constexpr uint32_t kMaxLabelIndex = 64;
+
+#ifdef __CUDACC__
+// Label sub-range [lo, hi) of label class `cls` (id range [vlo, vhi)) in x's
+// sorted list lst[0, d): from the label index when present, else by binary
+// search.  `which` 0 -> lo, 1 -> hi.
+__device__ __forceinline__ uint32_t label_bound(const DevGraph& g, uint32_t x, const uint32_t* lst, uint32_t d,
+                                                uint32_t cls, uint32_t vlo, uint32_t vhi, uint32_t which) {
+  if (cls == kNone) return 0;
+  if (g.loff) return __ldg(g.loff + uint64_t(x) * (g.nlab + 1) + cls + which);
+  const uint32_t key = which ? vhi : vlo;
+  uint32_t lo = 0, hi = d;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(lst + mid) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+#endif
 
 // Matching program of one (query, anchor edge): the matching order and, per
 // level l >= 2, the backward neighbours (positions j < l adjacent to order[l]),
@@ -32,6 +59,7 @@ struct DevGraph {
 struct LevelProg {
   uint32_t qbit;                 // 1 << order[l] (candidate-row bit)
   uint32_t vlo, vhi;             // internal-id range of label(order[l]) (ids are label-ordered)
+  uint32_t lcls;                 // label class index of label(order[l]) (kNone: absent from the graph)
   uint32_t backmask;             // positions j < l adjacent to order[l]
   uint32_t eqmask;               // positions j < l with label(order[j]) == label(order[l])
   uint32_t nback;

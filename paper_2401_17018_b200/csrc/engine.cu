@@ -81,6 +81,8 @@ struct QueryState {
   std::vector<std::vector<uint32_t>> orders;
   std::vector<uint32_t> tails;  // EdgeProg::tail per query edge
   bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
+  DBuf<uint32_t> mbuf[2];        // materialised matches per phase (bdsm_engine_collect_matches)
+  DBuf<unsigned long long> mcount;
   DBuf<LeafSig> leafsigs;        // distinct leaf signatures (prefill before each launch)
   uint32_t n_leafsig = 0;
   uint64_t deadline_ns = 0;  // host-steady-clock based, translated per batch
@@ -108,6 +110,7 @@ struct bdsm_engine {
 
   DBuf<uint64_t> off;
   DBuf<uint32_t> deg, cap, adj, elab, vlabel;
+  DBuf<uint32_t> loff, class_lo;  // label index (DevGraph::loff) and label-class start ids
 
   std::vector<std::unique_ptr<QueryState>> queries;
   DBuf<DevQueryEnc> d_qenc;
@@ -132,6 +135,34 @@ struct bdsm_engine {
   DBuf<QueueState> qstate;
   DBuf<uint32_t> dyn_ready;
   DBuf<unsigned long long> memo;  // leaf-weight memo of the matching kernel (2^21 words)
+  uint64_t collect_cap = 0;        // matches materialised per (query, phase); 0 = counts only
+
+  // Matches of the last batch for (query, phase) in external ids, query vertex
+  // order, sorted (the reference sorts its match vectors, src/matcher.cpp:365-366).
+  size_t fetch_matches(int qi, int phase, std::vector<uint32_t>& out) {
+    QueryState& qs = *queries.at(size_t(qi));
+    out.clear();
+    if (!collect_cap || !qs.mcount.p) return 0;
+    unsigned long long cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, qs.mcount.p + phase, sizeof(cnt), cudaMemcpyDeviceToHost, stream));
+    sync();
+    const size_t got = size_t(std::min<unsigned long long>(cnt, collect_cap));
+    const uint32_t n = qs.q.n;
+    out.resize(got * n);
+    if (got) CK(cudaMemcpyAsync(out.data(), qs.mbuf[phase].p, 4ull * got * n, cudaMemcpyDeviceToHost, stream));
+    sync();
+    for (auto& x : out) x = old_of[x];
+    std::vector<size_t> idx(got);
+    for (size_t i = 0; i < got; ++i) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](size_t p, size_t q) {
+      return std::lexicographical_compare(out.begin() + p * n, out.begin() + (p + 1) * n, out.begin() + q * n,
+                                          out.begin() + (q + 1) * n);
+    });
+    std::vector<uint32_t> sorted(got * n);
+    for (size_t i = 0; i < got; ++i) std::copy_n(out.begin() + idx[i] * n, n, sorted.begin() + i * n);
+    out.swap(sorted);
+    return size_t(cnt);
+  }
   uint32_t epoch = 0;
   DBuf<uint8_t> cub_tmp;
   DBuf<BatchState> d_st;
@@ -175,6 +206,8 @@ struct bdsm_engine {
     v.adj = g.adj;
     v.elab = g.elab;
     v.vlabel = g.vlabel;
+    v.loff = g.loff;
+    v.nlab = g.nlab;
     return v;
   }
 
@@ -225,6 +258,35 @@ struct bdsm_engine {
     if (V) CK(cudaMemcpyAsync(d_new_of.p, new_of.data(), 4ull * V, cudaMemcpyHostToDevice, stream));
     build_internal(&internal);
     orig_desc = nullptr;
+    build_label_index();
+  }
+
+  // Label index over the label classes (label_ranges order); disabled for
+  // graphs with more than kMaxLabelIndex classes.
+  void build_label_index() {
+    const uint32_t nl = uint32_t(label_ranges.size());
+    g.nlab = nl;
+    loff.release();
+    std::vector<uint32_t> lo(std::max<uint32_t>(nl, 1), 0);
+    for (uint32_t k = 0; k < nl; ++k) lo[k] = label_ranges[k].second.first;
+    class_lo.ensure(lo.size());
+    CK(cudaMemcpyAsync(class_lo.p, lo.data(), 4 * lo.size(), cudaMemcpyHostToDevice, stream));
+    if (nl > kMaxLabelIndex || g.V == 0) {
+      refresh_graph_view();
+      sync();
+      return;
+    }
+    loff.ensure(uint64_t(g.V) * (nl + 1));
+    refresh_graph_view();
+    launch_label_index(g, num_sms, stream);
+    sync();
+  }
+
+  uint32_t label_class(uint32_t label) const {
+    auto it = std::lower_bound(label_ranges.begin(), label_ranges.end(), label,
+                               [](const auto& e, uint32_t l) { return e.first < l; });
+    if (it == label_ranges.end() || it->first != label) return kNone;
+    return uint32_t(it - label_ranges.begin());
   }
 
   std::pair<uint32_t, uint32_t> label_range(uint32_t label) const {
@@ -340,6 +402,8 @@ struct bdsm_engine {
     g.adj = adj.p;
     g.elab = has_elab ? elab.p : nullptr;
     g.vlabel = vlabel.p;
+    g.loff = loff.n ? loff.p : nullptr;
+    g.class_lo = class_lo.p;
   }
 
   [[noreturn]] void throw_build_error(const bdsm_graph_desc* d, uint32_t bad) {
@@ -495,10 +559,14 @@ struct bdsm_engine {
     std::vector<AnchorEdge> anchors;
     std::vector<LeafSig> leafsigs;
     std::vector<std::pair<uint32_t, uint32_t>> ranges(qs.q.n);
-    for (uint32_t u = 0; u < qs.q.n; ++u) ranges[u] = label_range(qs.q.labels[u]);
+    std::vector<uint32_t> classes(qs.q.n);
+    for (uint32_t u = 0; u < qs.q.n; ++u) {
+      ranges[u] = label_range(qs.q.labels[u]);
+      classes[u] = label_class(qs.q.labels[u]);
+    }
     for (uint32_t e = 0; e < qs.q.edges.size(); ++e) {
       qs.orders.push_back(matching_order(qs.q, e, cs));
-      progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back(), ranges));
+      progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back(), ranges, classes));
       qs.tails.push_back(progs.back().tail);
       const EdgeProg& ep = progs.back();
       for (uint32_t t = 0; t < ep.n; ++t) {
@@ -551,6 +619,38 @@ struct bdsm_engine {
     CK(cudaMemcpyAsync(d_rows.p, rows.data(), sizeof(uint32_t*) * nq, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_colsize.p, cols.data(), sizeof(uint64_t*) * nq, cudaMemcpyHostToDevice, stream));
     sync();
+    apply_l2_window();
+  }
+
+  // L2 access-policy window (experiment switch BDSM_L2_WINDOW=rows|memo):
+  // persisting L2 lines for the candidate rows of query 0 or the weight memo.
+  void apply_l2_window() {
+    const char* env = getenv("BDSM_L2_WINDOW");
+    if (!env || queries.empty()) return;
+    void* base = nullptr;
+    size_t bytes = 0;
+    if (!strcmp(env, "rows")) {
+      base = queries[0]->rows.p;
+      bytes = 4ull * g.V;
+    } else if (!strcmp(env, "memo") && memo.p) {
+      base = memo.p;
+      bytes = 8ull * memo.n;
+    }
+    if (!base) return;
+    int max_persist = 0, max_window = 0;
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
+    const size_t win = std::min<size_t>(bytes, size_t(max_window));
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, size_t(max_persist))));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = base;
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio = std::min(1.0f, float(max_persist) / float(win));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    fprintf(stderr, "[bdsm] L2 window %s: %zu bytes (max window %d, max persisting %d)\n", env, win, max_window,
+            max_persist);
   }
 
   // --------------------------------------------------------------- batches --
@@ -667,6 +767,9 @@ struct bdsm_engine {
     a.merge_ratio = 8;
     a.memo = memo.p;
     a.memo_mask = uint32_t(memo.n - 1);
+    a.match_out = nullptr;
+    a.match_count = nullptr;
+    a.match_cap = 0;
     return a;
   }
 
@@ -686,15 +789,24 @@ struct bdsm_engine {
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_task_counts.p, task_off.p, int(n + 1), stream));
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_counts.p, item_off.p, int(n + 1), stream));
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_cost.p, cost_off.p, int(n + 1), stream));
-      launch_anchor_emit(a, stream);
+      if (!(collect_cap && qs.q.n <= 2)) launch_anchor_emit(a, stream);
       // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
       CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
       a.epoch = ++epoch;
       launches += 2;
       cub_calls += 3;
+      if (collect_cap) {  // --dump-matches: materialise this (query, phase)'s matches
+        qs.mbuf[phase].ensure(collect_cap * qs.q.n);
+        qs.mcount.ensure(2);
+        CK(cudaMemsetAsync(qs.mcount.p + phase, 0, sizeof(unsigned long long), stream));
+        a.match_out = qs.mbuf[phase].p;
+        a.match_count = qs.mcount.p + phase;
+        a.match_cap = collect_cap;
+      }
+      if (qs.q.n <= 2 && collect_cap) launch_anchor_emit(a, stream);  // 2-vertex matches are the anchors
       if (qs.q.n > 2) {
         CK(cudaEventRecord(next_kev(), stream));
-        if (qs.has_leaf) {
+        if (qs.has_leaf && !collect_cap) {
           CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
           launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, num_sms, stream);
           ++launches;
@@ -1132,6 +1244,28 @@ bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out) {
     for (uint32_t v = 0; v < engine->g.V; ++v) out[v] = rows[engine->new_of[v]] & ~kRowFlags;
     return BDSM_OK;
   });
+}
+
+bdsm_status bdsm_engine_collect_matches(bdsm_engine* engine, uint64_t cap) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  engine->collect_cap = cap;
+  return BDSM_OK;
+}
+
+int64_t bdsm_engine_matches(bdsm_engine* engine, int query, int phase, uint32_t* out, size_t cap) {
+  if (!engine || query < 0 || size_t(query) >= engine->queries.size() || phase < 0 || phase > 1)
+    return -int64_t(BDSM_INVALID_ARGUMENT);
+  int64_t r = 0;
+  bdsm_status st = guarded([&] {
+    std::vector<uint32_t> m;
+    const size_t cnt = engine->fetch_matches(query, phase, m);
+    const uint32_t n = engine->queries[size_t(query)]->q.n;
+    const size_t have = n ? m.size() / n : 0;
+    if (out) std::copy_n(m.begin(), std::min(have, cap) * n, out);
+    r = int64_t(cnt);
+    return BDSM_OK;
+  });
+  return st == BDSM_OK ? r : -int64_t(st);
 }
 
 int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge) {

@@ -30,6 +30,9 @@ struct DevGraphMut {
   uint32_t* elab;
   uint32_t* vlabel;
   uint64_t pool_size;
+  uint32_t* loff;                // label index (see DevGraph), or nullptr
+  uint32_t nlab;
+  const uint32_t* class_lo;      // first internal id of each label class [nlab]
 };
 
 // ---- store.cu: build ------------------------------------------------------
@@ -64,6 +67,7 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           uint64_t* const* colsize, BatchState* st, int num_sms, cudaStream_t s);
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);
+void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s);
 
 // ---- match.cu ---------------------------------------------------------------
 struct PhaseArgs {
@@ -105,6 +109,9 @@ struct PhaseArgs {
   uint32_t merge_ratio;          // merge-window intersection when |other| <= ratio x |driver|
   unsigned long long* memo;      // leaf-weight memo (cleared before each launch)
   uint32_t memo_mask;
+  uint32_t* match_out;           // non-null: materialise matches ([match_cap][n], query vertex order)
+  unsigned long long* match_count;
+  unsigned long long match_cap;
 };
 
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);

@@ -76,8 +76,9 @@ __device__ __forceinline__ void level2_range(const EdgeProg& p, uint32_t m0, uin
   const uint32_t drv = level2_driver(p, m0, m1, g, &pos);
   const uint32_t* lst = g.adj + g.off[drv];
   const uint32_t d = g.deg[drv];
-  const uint32_t lo = lb_u32(lst, d, p.lv[2].vlo);
-  const uint32_t hi = p.lv[2].vhi > p.lv[2].vlo ? lb_u32(lst, d, p.lv[2].vhi) : lo;
+  const LevelProg& lp = p.lv[2];
+  const uint32_t lo = label_bound(g, drv, lst, d, lp.lcls, lp.vlo, lp.vhi, 0);
+  const uint32_t hi = label_bound(g, drv, lst, d, lp.lcls, lp.vlo, lp.vhi, 1);
   *base = lo;
   *len = hi - lo;
 }
@@ -142,6 +143,14 @@ __global__ void k_anchor_emit(PhaseArgs a) {
       if (a.qn <= 2) {
         uint32_t owner = a.shard_world > 1 ? uint32_t((unsigned __int128)c * a.shard_world / total_cost) : 0;
         if (owner == a.shard_rank) ++direct;
+        if (owner == a.shard_rank && a.match_out) {  // materialise the 2-vertex match
+          const EdgeProg& p = a.progs[prog];
+          const unsigned long long k = atomicAdd(a.match_count, 1ull);
+          if (k < a.match_cap) {
+            a.match_out[k * 2 + p.order[0]] = flip ? up.v : up.u;
+            a.match_out[k * 2 + p.order[1]] = flip ? up.u : up.v;
+          }
+        }
         a.tasks[t++] = Task{i, prog, flip, 0, 0};
         c += 1;
         return;
@@ -290,7 +299,7 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   uint32_t bnd = 0;
   if (lane < 2 * nb) {
     if (bd <= 32) bnd = (lane & 1) ? bd : 0u;
-    else bnd = lb_u32(g.adj + bo, bd, (lane & 1) ? lp.vhi : lp.vlo);
+    else bnd = label_bound(g, M[lp.back[lb_list]], g.adj + bo, bd, lp.lcls, lp.vlo, lp.vhi, lane & 1);
   }
   const uint32_t f = __shfl_sync(kFull, bnd, (2 * lane) & 31);
   const uint32_t c = __shfl_sync(kFull, bnd, (2 * lane + 1) & 31);
@@ -409,7 +418,7 @@ __device__ __forceinline__ unsigned long long leaf_count(const PhaseArgs& a, con
   uint32_t lo = 0, hi = xd;
   if (xd > 32) {
     uint32_t bnd = 0;
-    if (lane < 2) bnd = lb_u32(g.adj + xo, xd, lane ? lp.vhi : lp.vlo);
+    if (lane < 2) bnd = label_bound(g, x, g.adj + xo, xd, lp.lcls, lp.vlo, lp.vhi, lane);
     lo = __shfl_sync(kFull, bnd, 0);
     hi = __shfl_sync(kFull, bnd, 1);
   }
@@ -445,11 +454,11 @@ __device__ __forceinline__ unsigned long long leaf_count_lane(const PhaseArgs& a
                                                               uint32_t anchor, uint32_t flag) {
   const DevGraph& g = a.g;
   const uint32_t* L = g.adj + xo;
-  uint32_t i = lb_u32(L, xd, lp.vlo);
+  uint32_t i = label_bound(g, x, L, xd, lp.lcls, lp.vlo, lp.vhi, 0);
+  const uint32_t end = label_bound(g, x, L, xd, lp.lcls, lp.vlo, lp.vhi, 1);
   unsigned long long cnt = 0;
-  for (; i < xd; ++i) {
+  for (; i < end; ++i) {
     const uint32_t c = __ldg(L + i);
-    if (c >= lp.vhi) break;
     const uint32_t rw = __ldg(a.rows + c);
     bool ok = (rw & lp.qbit) != 0;
     if (ok && g.elab) ok = __ldg(g.elab + xo + i) == lp.elab[0];
@@ -714,6 +723,11 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
 #ifndef BDSM_WBM_MIN_BLOCKS
 #define BDSM_WBM_MIN_BLOCKS 4  // resident 256-thread CTAs per SM the register budget must allow
 #endif
+// kEmit: bounded match materialisation (the reference's Match vectors,
+// src/matcher.cpp:169-217, for --dump-matches): the whole order is
+// enumerated (no counted tail) and every complete match is written in query
+// vertex order to a.match_out.
+template <bool kEmit>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wbm(PhaseArgs a) {
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
@@ -832,7 +846,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     const Task task = a.tasks[task_id];
     const EdgeProg& P = a.progs[task.prog];
     const uint32_t anchor = task.upd;
-    const uint32_t T = P.tail;  // deepest DFS level; deeper levels are counted by tail_factor
+    const uint32_t T = kEmit ? P.n - 1 : P.tail;  // deepest DFS level; deeper levels are counted by tail_factor
     uint32_t tvalid = 0;        // tail levels whose cached count is current
     if (kind == 1) {
       const bdsm_update_dev up = a.ups[task.upd];
@@ -987,7 +1001,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         cy_filter += clock64() - cy0;
         cy0 = clock64();
 #endif
-        if (l == T && P.leafmask && m) {
+        if (kEmit && l == T && m) {  // write every survivor's full match (query vertex order)
+          const uint32_t pm = __popc(m);
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(a.match_count, (unsigned long long)pm);
+          base = __shfl_sync(kFull, base, 0);
+          if ((m >> lane) & 1u) {
+            const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+            if (k < a.match_cap) {
+              uint32_t* out = a.match_out + k * P.n;
+              for (uint32_t j = 0; j < T; ++j) out[P.order[j]] = s_M[w][j];
+              out[P.order[T]] = c;
+            }
+          }
+        }
+        if (!kEmit && l == T && P.leafmask && m) {
           // last DFS level with leaves of T: per-survivor weights; each lane
           // walks the tail levels for its own reference-tree counters
           const bool ok = (m >> lane) & 1u;
@@ -1141,10 +1169,11 @@ void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s) {
   // persistent: as many resident CTAs as the SMs hold
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm, kWarpsPerBlock * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<false>, kWarpsPerBlock * 32, 0);
     if (per_sm <= 0) per_sm = 1;
   }
-  k_wbm<<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
+  if (a.match_out) k_wbm<true><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
+  else k_wbm<false><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
 }
 
 }  // namespace bdsm_b200

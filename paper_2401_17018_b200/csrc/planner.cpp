@@ -100,7 +100,8 @@ std::vector<uint32_t> matching_order(const HostQuery& q, uint32_t e,
 }
 
 EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order,
-                       const std::vector<std::pair<uint32_t, uint32_t>>& label_range) {
+                       const std::vector<std::pair<uint32_t, uint32_t>>& label_range,
+                       const std::vector<uint32_t>& label_class) {
   EdgeProg p{};
   p.n = q.n;
   p.query = query_index;
@@ -111,6 +112,7 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
     lp.qbit = 1u << u;
     lp.vlo = label_range[u].first;
     lp.vhi = label_range[u].second;
+    lp.lcls = label_class[u];
     lp.nback = 0;
     for (uint32_t j = 0; j < l; ++j) {
       if (q.adjacent(order[j], u)) {

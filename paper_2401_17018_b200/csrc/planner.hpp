@@ -52,7 +52,8 @@ std::vector<uint32_t> matching_order(const HostQuery& q, uint32_t e,
 // Device program for one (query, edge) from its order.  label_range[u] is
 // the internal-id range [lo, hi) holding query vertex u's label.
 EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vector<uint32_t>& order,
-                       const std::vector<std::pair<uint32_t, uint32_t>>& label_range);
+                       const std::vector<std::pair<uint32_t, uint32_t>>& label_range,
+                       const std::vector<uint32_t>& label_class);
 
 // Canonical split of work units over ranks: owner = floor(world * prefix / total).
 void shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);

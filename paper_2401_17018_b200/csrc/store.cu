@@ -415,6 +415,10 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
+    // label index of the new list
+    if (g.loff)
+      for (uint32_t k = lane; k <= g.nlab; k += 32)
+        g.loff[uint64_t(x) * (g.nlab + 1) + k] = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
     // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
     const uint32_t vl = g.vlabel[x];
     for (uint32_t q = 0; q < nq; ++q) {
@@ -459,6 +463,20 @@ __global__ void __launch_bounds__(256) k_encode_all(DevGraph g, const DevQueryEn
     const uint32_t cnt = group_counts(g.adj + g.off[v], g.deg[v], qe, lane);
     const uint32_t row = row_of(qe, vl, cnt, lane);
     if (lane == 0) rows[v] = row;
+  }
+}
+
+// Label index of every vertex (DevGraph::loff): warp per vertex, lane k
+// finds label class k's first position by binary search.
+__global__ void __launch_bounds__(256) k_label_index(DevGraphMut g) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t v = warp; v < g.V; v += nwarps) {
+    const uint32_t d = g.deg[v];
+    const uint32_t* lst = g.adj + g.off[v];
+    for (uint32_t k = lane; k <= g.nlab; k += 32)
+      g.loff[v * (g.nlab + 1) + k] = k < g.nlab ? lower_bound_u32(lst, d, g.class_lo[k]) : d;
   }
 }
 
@@ -545,6 +563,9 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);
+}
+void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s) {
+  if (g.loff && g.V) k_label_index<<<unsigned(num_sms * 16), 256, 0, s>>>(g);
 }
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s) {
   k_column_sizes<<<blocks_for(V), kThreads, 0, s>>>(rows, V, n, out);

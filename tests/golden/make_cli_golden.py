@@ -47,13 +47,14 @@ def random_graph(path, V, E, L, seed, elabels=0):
     write(path, lines)
 
 
-def run_case(name, graph, qspec, sspec, seed):
+def run_case(name, graph, qspec, sspec, seed, dump=True):
     d = os.path.join(OUT, name)
     ref_out = os.path.join(d, "ref")
     shutil.rmtree(ref_out, ignore_errors=True)
-    r = subprocess.run([REF_CLI, graph, qspec, sspec, str(seed), ref_out], capture_output=True, text=True)
+    r = subprocess.run([REF_CLI, graph, qspec, sspec, str(seed), ref_out] + (["dump"] if dump else []),
+                       capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    meta = {"qspec": qspec, "sspec": sspec, "seed": seed, "summary": r.stdout.strip()}
+    meta = {"qspec": qspec, "sspec": sspec, "seed": seed, "summary": r.stdout.strip(), "dump_matches": dump}
     for f in ("latency.csv", "stages.csv", "utilization.csv"):
         os.remove(os.path.join(ref_out, f))  # timing-dependent, headers are checked in tests
     with open(os.path.join(d, "case.json"), "w") as f:
@@ -78,17 +79,17 @@ def main():
                  "s:" + os.path.join(d, s + ".txt"), 1)
     # generated workloads through the reference's own generators
     cases = [
-        ("gen_sparse_mixed", 400, 2400, 3, 0, "g:sparse,5,3", "s:0.05,mixed,4", 5),
-        ("gen_tree_insert", 300, 1500, 2, 0, "g:tree,4,2", "s:0.08,insert,3", 11),
-        ("gen_dense_delete", 200, 1800, 2, 0, "g:dense,4,2", "s:0.05,delete,2", 3),
-        ("gen_kcore_mixed", 300, 2000, 3, 0, "g:sparse,4,2", "s:0.05,mixed,3,4", 21),
-        ("gen_elabel_mixed", 250, 1500, 2, 2, "g:sparse,4,2", "s:0.06,mixed,3", 8),
+        ("gen_sparse_mixed", 400, 2400, 3, 0, "g:sparse,5,3", "s:0.05,mixed,4", 5, True),
+        ("gen_tree_insert", 300, 1500, 2, 0, "g:tree,4,2", "s:0.08,insert,3", 11, False),
+        ("gen_dense_delete", 200, 1800, 2, 0, "g:dense,4,2", "s:0.05,delete,2", 3, True),
+        ("gen_kcore_mixed", 300, 2000, 3, 0, "g:sparse,4,2", "s:0.05,mixed,3,4", 21, True),
+        ("gen_elabel_mixed", 250, 1500, 2, 2, "g:sparse,4,2", "s:0.06,mixed,3", 8, True),
     ]
-    for name, V, E, L, EL, q, s, seed in cases:
+    for name, V, E, L, EL, q, s, seed, dump in cases:
         d = os.path.join(OUT, name)
         os.makedirs(d)
         random_graph(os.path.join(d, "g.txt"), V, E, L, seed, EL)
-        run_case(name, os.path.join(d, "g.txt"), q, s, seed)
+        run_case(name, os.path.join(d, "g.txt"), q, s, seed, dump)
     # relative paths in case.json
     for name in os.listdir(OUT):
         p = os.path.join(OUT, name, "case.json")

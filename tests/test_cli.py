@@ -4,8 +4,9 @@ oracle/ref_cli.cpp: run_pipeline with coalesce off).
 
 CPU: the seeded generators (`bdsm generate`) reproduce the reference's
 generate_queries / generate_stream byte for byte; flag errors.
-GPU: `bdsm run` writes the reference's deltas.csv and summary line, and the
-report CSV headers of emit_report (src/bench.cpp:566-591).
+GPU: `bdsm run` writes the reference's deltas.csv, summary line and
+--dump-matches files, and the report CSV headers of emit_report
+(src/bench.cpp:566-591).
 """
 import json
 import os
@@ -87,10 +88,17 @@ def test_cli_errors(tmp_path):
 def test_cli_run_matches_reference(name, tmp_path):
     meta = case(name)
     out = str(tmp_path / "out")
-    r = subprocess.run([CLI, "run"] + cli_args(name, meta, out), capture_output=True, text=True, timeout=300)
+    dump = ["--dump-matches"] if meta.get("dump_matches") else []
+    r = subprocess.run([CLI, "run"] + cli_args(name, meta, out) + dump, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == meta["summary"].replace("OUT/", out + "/")
-    assert read(os.path.join(out, "deltas.csv")) == read(os.path.join(GOLD, name, "ref", "deltas.csv"))
+    ref = os.path.join(GOLD, name, "ref")
+    assert read(os.path.join(out, "deltas.csv")) == read(os.path.join(ref, "deltas.csv"))
+    # --dump-matches: the materialised match sets, file for file (src/bench.cpp:484-491)
+    dumps = sorted(f for f in os.listdir(ref) if f.startswith("matches_batch"))
+    assert bool(dumps) == bool(dump)
+    for f in dumps:
+        assert read(os.path.join(out, f)) == read(os.path.join(ref, f)), f
     assert read(os.path.join(out, "latency.csv")).startswith("query_id,category,size,seconds,solved\n")
     assert read(os.path.join(out, "stages.csv")).startswith("batch,preprocess_s,match_s,ratio\n")
     assert read(os.path.join(out, "utilization.csv")).startswith("worker,busy_seconds,total_seconds,fraction\n")
