@@ -159,6 +159,7 @@ def main():
     ap.add_argument("--cpu-time-cap", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--l2-hot-mb", type=int, default=0, help="K8 hot-list L2 persistence budget (0: off)")
     args = ap.parse_args()
 
     world, rank, local = dist_env()
@@ -245,10 +246,10 @@ def ours(args, world, rank, local):
 
     t0 = time.time()
     engA = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
-                     chunk=args.chunk)
+                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb)
     engA.add_query(wl.qlabels, wl.qedges)
     engB = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
-                     chunk=args.chunk)
+                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb)
     engB.add_query(wl.qlabels, wl.qedges)
     log(f"engines built in {time.time() - t0:.1f}s")
 

@@ -53,7 +53,8 @@ class _QueryDesc(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("group_bits", C.c_uint32), ("coalesce", C.c_uint32), ("device", C.c_int32),
                 ("shard_rank", C.c_uint32), ("shard_world", C.c_uint32), ("slack", C.c_float),
-                ("pool_reserve", C.c_float), ("chunk", C.c_uint32)]
+                ("pool_reserve", C.c_float), ("chunk", C.c_uint32), ("zero_copy", C.c_uint32),
+                ("l2_hot_mb", C.c_uint32)]
 
 
 class _UpdateError(C.Structure):
@@ -212,14 +213,15 @@ class Engine:
 
     def __init__(self, vertex_labels, src, dst, edge_labels=None, *, group_bits: int = 2, device: int = 0,
                  shard_rank: int = 0, shard_world: int = 1, slack: float = 0.25, pool_reserve: float = 0.5,
-                 chunk: int = 64):
+                 chunk: int = 64, zero_copy: bool = False, l2_hot_mb: int = 0):
         L = lib()
         self._vl = _u32(vertex_labels)
         s, d = _u32(src), _u32(dst)
         el = None if edge_labels is None else _u32(edge_labels)
         desc = _GraphDesc(len(self._vl), self._vl.ctypes.data, len(s), s.ctypes.data, d.ctypes.data,
                           None if el is None else el.ctypes.data)
-        opts = _Options(group_bits, 0, device, shard_rank, shard_world, slack, pool_reserve, chunk)
+        opts = _Options(group_bits, 0, device, shard_rank, shard_world, slack, pool_reserve, chunk,
+                        1 if zero_copy else 0, l2_hot_mb)
         h = C.c_void_p()
         st = L.bdsm_engine_create(C.byref(desc), C.byref(opts), C.byref(h))
         if st != 0:

@@ -48,21 +48,36 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  T* host = nullptr;    // zero-copy: mapped pinned host allocation behind p
+  bool mapped = false;  // allocate as mapped pinned host memory (graphs beyond HBM)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (host) cudaFreeHost(host);
+    else if (p) cudaFree(p);
     p = nullptr;
+    host = nullptr;
     n = 0;
   }
   void ensure(size_t want) {
     if (want <= n && p) return;
     release();
     size_t alloc = std::max<size_t>(want, 1);
-    CK(cudaMalloc(&p, alloc * sizeof(T)));
+    if (mapped) {
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&host), alloc * sizeof(T), cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&p), host, 0));
+    } else {
+      CK(cudaMalloc(&p, alloc * sizeof(T)));
+    }
     n = alloc;
+  }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(host, o.host);
+    std::swap(mapped, o.mapped);
   }
   void ensure_grow(size_t want) {  // amortised growth
     if (want <= n && p) return;
@@ -136,6 +151,36 @@ struct bdsm_engine {
   DBuf<uint32_t> dyn_ready;
   DBuf<unsigned long long> memo;  // leaf-weight memo of the matching kernel (2^21 words)
   uint64_t collect_cap = 0;        // matches materialised per (query, phase); 0 = counts only
+
+  // K8 hot-list L2 persistence (opts.l2_hot_mb > 0).  Every kHotPeriod batches
+  // the hottest lists (random-walk visit counts, decayed) are packed into an
+  // arena at the pool's bump pointer and the engine stream gets a persisting
+  // access-policy window over it.
+  static constexpr uint64_t kHotPeriod = 8;
+  DBuf<uint32_t> heat;
+  DBuf<unsigned long long> hot_hist;
+  bool heat_init = false;
+  uint64_t batches_done = 0;
+  void hot_pack_maybe() {
+    if (!opts.l2_hot_mb || batches_done == 0 || batches_done % kHotPeriod) return;
+    int max_persist = 0, max_window = 0;
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
+    const uint64_t budget =
+        std::min<uint64_t>({uint64_t(opts.l2_hot_mb) << 20, uint64_t(max_window), uint64_t(max_persist)});
+    if (budget < 4096 || g.pool_size - pool_top < 2 * (budget / 4)) return;  // no room: skip this period
+    hot_hist.ensure(34);
+    launch_hot_pack(g, heat.p, hot_hist.p, budget, d_st.p, num_sms, stream);
+    launches += 4;
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(budget)));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = g.adj + pool_top;
+    attr.accessPolicyWindow.num_bytes = size_t(budget);
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  }
 
   // Matches of the last batch for (query, phase) in external ids, query vertex
   // order, sorted (the reference sorts its match vectors, src/matcher.cpp:365-366).
@@ -458,15 +503,15 @@ struct bdsm_engine {
     reserve = std::max(reserve, 2 * extra_need);
     uint64_t size = used + reserve;
     DBuf<uint32_t> nadj, nelab;
+    nadj.mapped = adj.mapped;
+    nelab.mapped = elab.mapped;
     nadj.ensure(size);
     if (has_elab) nelab.ensure(size);
     launch_compact(g, noff.p, ncap.p, nadj.p, has_elab ? nelab.p : nullptr, stream);
     sync();
-    std::swap(adj.p, nadj.p);
-    std::swap(adj.n, nadj.n);
+    adj.swap(nadj);
     if (has_elab) {
-      std::swap(elab.p, nelab.p);
-      std::swap(elab.n, nelab.n);
+      elab.swap(nelab);
     }
     std::swap(off.p, noff.p);
     std::swap(off.n, noff.n);
@@ -619,39 +664,8 @@ struct bdsm_engine {
     CK(cudaMemcpyAsync(d_rows.p, rows.data(), sizeof(uint32_t*) * nq, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_colsize.p, cols.data(), sizeof(uint64_t*) * nq, cudaMemcpyHostToDevice, stream));
     sync();
-    apply_l2_window();
   }
 
-  // L2 access-policy window (experiment switch BDSM_L2_WINDOW=rows|memo):
-  // persisting L2 lines for the candidate rows of query 0 or the weight memo.
-  void apply_l2_window() {
-    const char* env = getenv("BDSM_L2_WINDOW");
-    if (!env || queries.empty()) return;
-    void* base = nullptr;
-    size_t bytes = 0;
-    if (!strcmp(env, "rows")) {
-      base = queries[0]->rows.p;
-      bytes = 4ull * g.V;
-    } else if (!strcmp(env, "memo") && memo.p) {
-      base = memo.p;
-      bytes = 8ull * memo.n;
-    }
-    if (!base) return;
-    int max_persist = 0, max_window = 0;
-    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
-    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
-    const size_t win = std::min<size_t>(bytes, size_t(max_window));
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, size_t(max_persist))));
-    cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = base;
-    attr.accessPolicyWindow.num_bytes = win;
-    attr.accessPolicyWindow.hitRatio = std::min(1.0f, float(max_persist) / float(win));
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    CK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-    fprintf(stderr, "[bdsm] L2 window %s: %zu bytes (max window %d, max persisting %d)\n", env, win, max_window,
-            max_persist);
-  }
 
   // --------------------------------------------------------------- batches --
   size_t cub_bytes_for(size_t n) {
@@ -883,6 +897,7 @@ struct bdsm_engine {
       CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
       const uint32_t m = uint32_t(2 * n);
       const uint32_t nq = uint32_t(queries.size());
+      if (attempt == 0) hot_pack_maybe();
       launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
                      stream);
       {
@@ -919,6 +934,15 @@ struct bdsm_engine {
       cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);
+      if (opts.l2_hot_mb) {  // K8 estimator: walks from this batch's touched vertices
+        heat.ensure(g.V);
+        if (!heat_init) {
+          CK(cudaMemsetAsync(heat.p, 0, 4ull * g.V, stream));
+          heat_init = true;
+        }
+        launch_hot_walks(heads.p, skeys.p, d_st.p, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
+        ++launches;
+      }
       launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
       ++launches;
       CK(cudaEventRecord(ev[4], stream));
@@ -926,6 +950,9 @@ struct bdsm_engine {
       CK(cudaEventRecord(ev[5], stream));
       sync();
       const BatchState& b = *h_st;
+      // the hot-list arena (K8) is reserved even when the batch is then rejected
+      // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
+      if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
       if (b.selfloop_min != kNone || b.conflict_min != kNone) {
         bdsm_update bad{};
         uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
@@ -968,6 +995,7 @@ struct bdsm_engine {
     }
     const BatchState& b = *h_st;
     pool_top = b.pool_top;
+    ++batches_done;
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       bool dead = (b.timed_out >> qi) & 1u;
       if (dead) queries[qi]->solved = false;
@@ -1136,6 +1164,9 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     if (o.shard_rank >= o.shard_world) throw std::invalid_argument("shard_rank must be < shard_world");
     if (o.chunk % 32 != 0) throw std::invalid_argument("chunk must be a multiple of 32");
     e->opts = o;
+    // zero-copy tier (north_star item 4): the adjacency pool in mapped pinned
+    // host memory, for graphs whose lists exceed one GPU's HBM
+    e->adj.mapped = e->elab.mapped = o.zero_copy != 0;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (ndev == 0) throw CudaFailure("no CUDA device");

@@ -68,6 +68,10 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s);
+void launch_hot_walks(const uint32_t* heads, const uint64_t* skeys, const BatchState* st, DevGraph g,
+                      uint32_t* heat, uint32_t walks, uint32_t depth, uint32_t seed, int num_sms, cudaStream_t s);
+void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, unsigned long long budget,
+                     BatchState* st, int num_sms, cudaStream_t s);
 
 // ---- match.cu ---------------------------------------------------------------
 struct PhaseArgs {

@@ -466,6 +466,99 @@ __global__ void __launch_bounds__(256) k_encode_all(DevGraph g, const DevQueryEn
   }
 }
 
+// ---- K8: hot-list estimator, packing into an L2-persisting arena ----------
+// (north_star item 4; no reference counterpart).  Random walks
+// from the batch's touched vertices estimate which adjacency lists the next
+// batches' DFS will read; the hottest lists (by visits, within a byte budget)
+// are copied contiguously into an arena of the pool that an access-policy
+// window marks persisting in L2.  Performance only: list contents never change.
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void k_hot_walks(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+                            const BatchState* st, DevGraph g, uint32_t* heat, uint32_t walks, uint32_t depth,
+                            uint32_t seed) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  const uint64_t total = uint64_t(st->n_touched) * walks;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t v = uint32_t(skeys[heads[i / walks]] >> 32);
+    uint32_t h = mix32(seed ^ uint32_t(i * 0x9e3779b9u));
+    atomicAdd(heat + v, 1u);
+    for (uint32_t s = 0; s < depth; ++s) {
+      const uint32_t d = g.deg[v];
+      if (!d) break;
+      h = mix32(h + s);
+      v = g.adj[g.off[v] + h % d];
+      atomicAdd(heat + v, 1u);
+    }
+  }
+}
+
+// Bytes of lists per heat bucket (bucket = bit length of the heat).
+__global__ void k_hot_hist(DevGraph g, const uint32_t* __restrict__ heat, unsigned long long* hist) {
+  __shared__ unsigned long long sh[33];
+  if (threadIdx.x < 33) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.V; v += gridDim.x * blockDim.x) {
+    const uint32_t h = heat[v];
+    if (h) atomicAdd(&sh[32 - __clz(h)], 4ull * g.deg[v]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 33 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
+}
+
+// Threshold bucket: the hottest buckets whose lists fit the budget.
+__global__ void k_hot_select(unsigned long long* hist, unsigned long long budget) {
+  if (threadIdx.x != 0) return;
+  unsigned long long acc = 0;
+  uint32_t tb = 33;
+  for (int b = 32; b >= 1; --b) {
+    if (acc + hist[b] > budget) break;
+    acc += hist[b];
+    tb = uint32_t(b);
+  }
+  hist[33] = tb;  // read by k_hot_pack
+}
+
+// Warp per hot vertex: copy the list (and labels) to the arena slot reserved
+// from the pool bump pointer, repoint off/cap; decay every vertex's heat.
+__global__ void k_hot_pack(DevGraphMut g, uint32_t* heat, const unsigned long long* hist, BatchState* st) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t tb = uint32_t(hist[33]);
+  for (uint64_t v = warp; v < g.V; v += nwarps) {
+    const uint32_t h = heat[v];
+    const uint32_t d = g.deg[v];
+    const bool hot = h && (32 - __clz(h)) >= tb && d >= 32;
+    __syncwarp();
+    if (lane == 0) heat[v] = h >> 1;
+    if (!hot) continue;
+    const uint32_t c = (d + 3) & ~3u;  // no slack: the next insert relocates it out of the arena
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
+    slot = __shfl_sync(kFull, slot, 0);
+    if (slot + c > g.pool_size) continue;  // pool exhausted: leave it in place
+    const uint64_t o = g.off[v];
+    for (uint32_t i = lane; i < d; i += 32) g.adj[slot + i] = g.adj[o + i];
+    if (g.elab)
+      for (uint32_t i = lane; i < d; i += 32) g.elab[slot + i] = g.elab[o + i];
+    __syncwarp();
+    if (lane == 0) {
+      g.off[v] = slot;
+      g.cap[v] = c;
+    }
+  }
+}
+
 // Label index of every vertex (DevGraph::loff): warp per vertex, lane k
 // finds label class k's first position by binary search.
 __global__ void __launch_bounds__(256) k_label_index(DevGraphMut g) {
@@ -563,6 +656,18 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);
+}
+void launch_hot_walks(const uint32_t* heads, const uint64_t* skeys, const BatchState* st, DevGraph g,
+                      uint32_t* heat, uint32_t walks, uint32_t depth, uint32_t seed, int num_sms, cudaStream_t s) {
+  k_hot_walks<<<unsigned(num_sms * 4), kThreads, 0, s>>>(heads, skeys, st, g, heat, walks, depth, seed);
+}
+void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, unsigned long long budget,
+                     BatchState* st, int num_sms, cudaStream_t s) {
+  cudaMemsetAsync(hist, 0, 34 * sizeof(unsigned long long), s);
+  DevGraph v{g.V, g.off, g.deg, g.cap, g.adj, g.elab, g.vlabel, g.loff, g.nlab};
+  k_hot_hist<<<unsigned(num_sms * 8), kThreads, 0, s>>>(v, heat, hist);
+  k_hot_select<<<1, 32, 0, s>>>(hist, budget);
+  k_hot_pack<<<unsigned(num_sms * 16), kThreads, 0, s>>>(g, heat, hist, st);
 }
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s) {
   if (g.loff && g.V) k_label_index<<<unsigned(num_sms * 16), 256, 0, s>>>(g);

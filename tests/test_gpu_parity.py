@@ -110,3 +110,66 @@ def test_gpu_work_split_sums_to_reference(world):
             rs = [e.match_batch(b) for e in engines]
             assert sum(r.positive[0] for r in rs) == exp["pos"], inst["name"]
             assert sum(r.negative[0] for r in rs) == exp["neg"], inst["name"]
+
+
+def _random_stream(seed, V=2500, E=20000, L=3, nb=12, bsz=300):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    vl = rng.integers(0, L, V).astype(np.uint32)
+    hubs = rng.integers(0, V, 20)
+    pairs = set()
+    while len(pairs) < E:
+        a = int(hubs[rng.integers(0, 20)]) if rng.random() < 0.2 else int(rng.integers(0, V))
+        b = int(rng.integers(0, V))
+        if a != b:
+            pairs.add((min(a, b), max(a, b)))
+    present = set(pairs)
+    edges = sorted(pairs)
+    batches = []
+    for _ in range(nb):
+        batch, used = [], set()
+        plist = sorted(present)
+        while len(batch) < bsz:
+            if rng.random() < 0.34:
+                k = plist[int(rng.integers(0, len(plist)))]
+                op = 1
+            else:
+                a, b = (int(x) for x in rng.integers(0, V, 2))
+                k = (min(a, b), max(a, b))
+                op = 0
+                if a == b or k in present:
+                    continue
+            if k in used:
+                continue
+            used.add(k)
+            batch.append((op, k[0], k[1]))
+        for op, a, b in batch:
+            (present.discard if op else present.add)((a, b))
+        batches.append(batch)
+    return vl, edges, batches
+
+
+@pytest.mark.parametrize("opts", [{"zero_copy": True}, {"l2_hot_mb": 1}])
+def test_storage_options_do_not_change_counts(opts):
+    """Zero-copy adjacency pool (mapped pinned host memory) and K8 hot-list
+    packing into an L2-persisting arena (every 8 batches, so batches 9-12 read
+    packed lists) are storage/performance choices only: counts equal the
+    CPU restatement (pinned to the reference) on every batch."""
+    import sys
+    import os
+    import paper_2401_17018_b200 as bd
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    from oracle_py import Oracle
+    vl, edges, batches = _random_stream(11)
+    eu = [a for a, _ in edges]
+    ev = [b for _, b in edges]
+    q = ([0, 1, 2, 0, 1], [(0, 1), (1, 2), (2, 0), (2, 3), (3, 4)])
+    e = bd.Engine(vl, eu, ev, **opts)
+    e.add_query(*q)
+    o = Oracle(vl, eu, ev)
+    o.add_query(*q)
+    for bi, b in enumerate(batches):
+        r = e.match_batch(b)
+        exp = o.apply_batch(b)
+        assert (r.positive[0], r.negative[0]) == (exp[0][0], exp[1][0]), (bi, opts)
+    e.close()
