@@ -151,6 +151,13 @@ struct bdsm_engine {
   DBuf<uint32_t> dyn_ready;
   DBuf<unsigned long long> memo;  // leaf-weight memo of the matching kernel (2^21 words)
   uint64_t collect_cap = 0;        // matches materialised per (query, phase); 0 = counts only
+  // matching-kernel tuning knobs (BDSM_TUNE_BACKOFF / BDSM_TUNE_MERGE env overrides, for sweeps)
+  uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
+  uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
+  static uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = getenv(name);
+    return v ? uint32_t(strtoul(v, nullptr, 10)) : dflt;
+  }
 
   // K8 hot-list L2 persistence (opts.l2_hot_mb > 0).  Every kHotPeriod batches
   // the hottest lists (random-walk visit counts, decayed) are packed into an
@@ -778,7 +785,8 @@ struct bdsm_engine {
     a.dyn = dyn.p;
     a.dyn_ready = dyn_ready.p;
     a.dyn_cap = uint32_t(dyn.n);
-    a.merge_ratio = 8;
+    a.merge_ratio = tune_merge_ratio;
+    a.backoff_max = tune_backoff;
     a.memo = memo.p;
     a.memo_mask = uint32_t(memo.n - 1);
     a.match_out = nullptr;
@@ -1150,14 +1158,14 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     o.group_bits = 2;
     o.slack = 0.25f;
     o.pool_reserve = 0.5f;
-    o.chunk = 64;
+    o.chunk = 32;
     o.shard_world = 1;
     if (opts) {
       o = *opts;
       if (o.group_bits == 0) o.group_bits = 2;
       if (o.slack <= 0) o.slack = 0.25f;
       if (o.pool_reserve <= 0) o.pool_reserve = 0.5f;
-      if (o.chunk == 0) o.chunk = 64;
+      if (o.chunk == 0) o.chunk = 32;
       if (o.shard_world == 0) o.shard_world = 1;
     }
     if (o.coalesce) throw std::invalid_argument("coalesced search is not supported: it is not exact in the reference (SURVEY.md F1)");

@@ -111,6 +111,7 @@ struct PhaseArgs {
   uint32_t dyn_cap;
   uint32_t epoch;
   uint32_t merge_ratio;          // merge-window intersection when |other| <= ratio x |driver|
+  uint32_t backoff_max;          // idle warps' longest sleep between donation polls (ns)
   unsigned long long* memo;      // leaf-weight memo (cleared before each launch)
   uint32_t memo_mask;
   uint32_t* match_out;           // non-null: materialise matches ([match_cap][n], query vertex order)

@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
             }
           }
           __nanosleep(backoff);
-          if (backoff < 4096) backoff *= 2;
+          if (backoff < a.backoff_max) backoff *= 2;
         }
       }
     }
