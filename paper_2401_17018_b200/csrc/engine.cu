@@ -141,8 +141,7 @@ struct bdsm_engine {
   DBuf<uint64_t> new_off;
   DBuf<unsigned long long> hkeys;  // visibility table of the batch
   DBuf<uint32_t> hvals;
-  DBuf<uint32_t> upd_counts, upd_task_counts, item_off, task_off;
-  DBuf<uint64_t> upd_cost, cost_off;
+  DBuf<AnchorCount> upd_cnt, upd_off;
   DBuf<Task> tasks;
   DBuf<Item> items;
   size_t max_items = 0;
@@ -164,6 +163,20 @@ struct bdsm_engine {
   // arena at the pool's bump pointer and the engine stream gets a persisting
   // access-policy window over it.
   static constexpr uint64_t kHotPeriod = 8;
+  // Hub list for the leaf-weight prefill, refreshed every kHubPeriod batches.
+  static constexpr uint64_t kHubPeriod = 16;
+  DBuf<uint32_t> hub_ids, n_hubs;
+  DBuf<uint8_t> hub_tmp;
+  uint64_t hubs_at = ~0ull;
+  void refresh_hubs() {
+    if (hubs_at != ~0ull && batches_done - hubs_at < kHubPeriod) return;
+    hub_ids.ensure(std::max<uint32_t>(g.V, 1));
+    n_hubs.ensure(1);
+    const size_t tmp = select_hubs_tmp_bytes(g.V);
+    hub_tmp.ensure(std::max<size_t>(tmp, 1));
+    launch_select_hubs(g.deg, g.V, 256, hub_ids.p, n_hubs.p, hub_tmp.p, hub_tmp.n, stream);
+    hubs_at = batches_done;
+  }
   DBuf<uint32_t> heat;
   DBuf<unsigned long long> hot_hist;
   bool heat_init = false;
@@ -685,7 +698,10 @@ struct bdsm_engine {
     CK(cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, int(m + 1), stream));
     CK(cub::DeviceScan::ExclusiveSum(nullptr, d, (uint64_t*)nullptr, (uint64_t*)nullptr, int(n + 1), stream));
     CK(cub::DeviceScan::ExclusiveSum(nullptr, e, (uint32_t*)nullptr, (uint32_t*)nullptr, int(n + 1), stream));
-    return std::max({a, b, c, d, e});
+    size_t f = 0;
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, f, (AnchorCount*)nullptr, (AnchorCount*)nullptr, AnchorCountSum(),
+                                      AnchorCount{0, 0, 0}, int(n + 1), stream));
+    return std::max({a, b, c, d, e, f});
   }
 
   size_t batch_cap = 0;
@@ -709,12 +725,8 @@ struct bdsm_engine {
     ipos.ensure(m);
     new_off.ensure(m);
     new_cap.ensure(m);
-    upd_counts.ensure(cap_n + 1);
-    upd_task_counts.ensure(cap_n + 1);
-    item_off.ensure(cap_n + 1);
-    task_off.ensure(cap_n + 1);
-    upd_cost.ensure(cap_n + 1);
-    cost_off.ensure(cap_n + 1);
+    upd_cnt.ensure(cap_n + 1);
+    upd_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
     size_t hcap = 1024;
     while (hcap < 8 * cap_n) hcap <<= 1;  // >= 2x the 2|dB| directed keys + <= 2|dB| segment heads
@@ -770,12 +782,8 @@ struct bdsm_engine {
     a.chunk = opts.chunk;
     a.shard_rank = opts.shard_rank;
     a.shard_world = std::max<uint32_t>(opts.shard_world, 1);
-    a.upd_counts = upd_counts.p;
-    a.upd_task_counts = upd_task_counts.p;
-    a.upd_cost = upd_cost.p;
-    a.item_off = item_off.p;
-    a.task_off = task_off.p;
-    a.cost_off = cost_off.p;
+    a.upd_cnt = upd_cnt.p;
+    a.upd_off = upd_off.p;
     a.tasks = tasks.p;
     a.items = items.p;
     a.max_items = uint32_t(std::min<size_t>(max_items, 0xffffffffu));
@@ -808,15 +816,14 @@ struct bdsm_engine {
       }
       launch_anchor_count(a, stream);
       size_t tmp = cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_task_counts.p, task_off.p, int(n + 1), stream));
-      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_counts.p, item_off.p, int(n + 1), stream));
-      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, upd_cost.p, cost_off.p, int(n + 1), stream));
+      CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(), AnchorCount{0, 0, 0},
+                                        int(n + 1), stream));
       if (!(collect_cap && qs.q.n <= 2)) launch_anchor_emit(a, stream);
       // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
       CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
       a.epoch = ++epoch;
       launches += 2;
-      cub_calls += 3;
+      cub_calls += 1;
       if (collect_cap) {  // --dump-matches: materialise this (query, phase)'s matches
         qs.mbuf[phase].ensure(collect_cap * qs.q.n);
         qs.mcount.ensure(2);
@@ -830,7 +837,8 @@ struct bdsm_engine {
         CK(cudaEventRecord(next_kev(), stream));
         if (qs.has_leaf && !collect_cap) {
           CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
-          launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, num_sms, stream);
+          refresh_hubs();
+          launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
           ++launches;
         }
         launch_wbm(a, num_sms, stream);

@@ -74,6 +74,17 @@ void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, un
                      BatchState* st, int num_sms, cudaStream_t s);
 
 // ---- match.cu ---------------------------------------------------------------
+// Per-update anchor counts (K5 pass 1) and their exclusive scan (one CUB scan).
+struct AnchorCount {
+  uint32_t tasks, items;
+  uint64_t cost;
+};
+struct AnchorCountSum {
+  __host__ __device__ AnchorCount operator()(const AnchorCount& x, const AnchorCount& y) const {
+    return AnchorCount{x.tasks + y.tasks, x.items + y.items, x.cost + y.cost};
+  }
+};
+
 struct PhaseArgs {
   DevGraph g;
   const bdsm_update_dev* ups;
@@ -94,12 +105,8 @@ struct PhaseArgs {
   uint32_t qn;                   // query vertex count
   uint32_t chunk;
   uint32_t shard_rank, shard_world;
-  uint32_t* upd_counts;          // [n_ups + 1] items per update (scan input)
-  uint32_t* upd_task_counts;     // [n_ups + 1]
-  uint64_t* upd_cost;            // [n_ups + 1] driver mass per update (scan input)
-  uint32_t* item_off;            // exclusive scans
-  uint32_t* task_off;
-  uint64_t* cost_off;
+  AnchorCount* upd_cnt;          // [n_ups + 1] per-update anchors / items / driver mass (scan input)
+  AnchorCount* upd_off;          // its exclusive scan
   Task* tasks;
   Item* items;
   uint32_t max_items;
@@ -122,6 +129,10 @@ struct PhaseArgs {
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);
 void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s);
 void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s);
-void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, int num_sms, cudaStream_t s);
+void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, const uint32_t* hubs,
+                         const uint32_t* n_hubs, int num_sms, cudaStream_t s);
+void launch_select_hubs(const uint32_t* deg, uint32_t V, uint32_t min_deg, uint32_t* hubs, uint32_t* n_hubs,
+                        void* tmp, size_t tmp_bytes, cudaStream_t s);
+size_t select_hubs_tmp_bytes(uint32_t V);
 
 }  // namespace bdsm_b200

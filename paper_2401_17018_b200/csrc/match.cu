@@ -117,28 +117,28 @@ __global__ void k_anchor_count(PhaseArgs a) {
         cost += d;
       });
     }
-    a.upd_task_counts[i] = nt;
-    a.upd_counts[i] = ni;
-    a.upd_cost[i] = cost;
+    a.upd_cnt[i] = AnchorCount{nt, ni, cost};
   }
 }
 
 __global__ void k_anchor_emit(PhaseArgs a) {
   if (batch_aborted(a.st)) return;
-  const uint64_t total_cost = a.cost_off[a.n_ups];
-  const uint32_t total_items = a.item_off[a.n_ups];
+  const AnchorCount tot = a.upd_off[a.n_ups];
+  const uint64_t total_cost = tot.cost;
+  const uint32_t total_items = tot.items;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.st->n_tasks[a.phase] = a.task_off[a.n_ups];
+    a.st->n_tasks[a.phase] = tot.tasks;
     a.st->n_items[a.phase] = total_items;
-    atomicAdd((unsigned long long*)&a.st->tasks_total, (unsigned long long)a.task_off[a.n_ups]);
+    atomicAdd((unsigned long long*)&a.st->tasks_total, (unsigned long long)tot.tasks);
     if (total_items > a.max_items) a.st->overflow = a.phase == 0 ? 2 : 3;  // host regrows, reruns
   }
   if (total_items > a.max_items) return;
   uint64_t direct = 0;    // 2-vertex queries: every anchor is a match
   uint64_t bytes = 0, calls = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ups; i += gridDim.x * blockDim.x) {
-    uint32_t t = a.task_off[i], it = a.item_off[i];
-    uint64_t c = a.cost_off[i];
+    const AnchorCount off = a.upd_off[i];
+    uint32_t t = off.tasks, it = off.items;
+    uint64_t c = off.cost;
     for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up) {
       if (a.qn <= 2) {
         uint32_t owner = a.shard_world > 1 ? uint32_t((unsigned __int128)c * a.shard_world / total_cost) : 0;
@@ -593,34 +593,31 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 }
 
 // Leaf-weight prefill (before each matching launch of a query with leaf
-// levels): the weights of every long-list vertex that can be a level-T
-// candidate of a leaf signature — label(order[T]), its candidate bit, not a
-// same-kind batch endpoint — computed by the whole grid up front, so no DFS
-// warp counts a hub's list on its critical path.  Warp per 32 consecutive
-// vertex ids of the label range; qualifying lanes are counted one by one.
-__global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig* __restrict__ sigs, uint32_t nsig) {
+// levels): the weights of every long-list vertex that can be a weighted
+// parent of a leaf signature — label(parent), its candidate bit — computed by
+// the whole grid up front, so no DFS warp counts a hub's list on its critical
+// path.  The candidates come from the engine's hub list (ids with > 256
+// neighbours, refreshed every few batches; a stale list only means a lazy
+// count later).  Warp per (signature, 32 hubs); qualifying lanes are counted
+// one by one by the whole warp.
+__global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig* __restrict__ sigs, uint32_t nsig,
+                                                      const uint32_t* __restrict__ hubs,
+                                                      const uint32_t* __restrict__ n_hubs) {
   if (batch_aborted(a.st)) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
-  uint64_t total = 0;
-  for (uint32_t si = 0; si < nsig; ++si) total += (uint64_t(sigs[si].phi - sigs[si].plo) + 31) / 32;
-  for (uint64_t gi = warp; gi < total; gi += nwarps) {
-    uint32_t si = 0;
-    uint64_t bi = gi;
-    while (true) {  // map the global block index to (signature, block)
-      const uint64_t nb = (uint64_t(sigs[si].phi - sigs[si].plo) + 31) / 32;
-      if (bi < nb) break;
-      bi -= nb;
-      ++si;
-    }
-    const LeafSig& ls = sigs[si];
-    const uint32_t x = ls.plo + uint32_t(bi) * 32 + lane;
+  const uint32_t nh = *n_hubs;
+  const uint64_t nblk = (uint64_t(nh) + 31) / 32;
+  for (uint64_t gi = warp; gi < nblk * nsig; gi += nwarps) {
+    const LeafSig& ls = sigs[gi / nblk];
+    const uint64_t hi = (gi % nblk) * 32 + lane;
     bool want = false;
-    if (x < ls.phi) {
-      const uint32_t rw = __ldg(a.rows + x);
-      want = (rw & ls.pbit) && __ldg(a.g.deg + x) > kLeafLaneMax;
+    uint32_t x = 0;
+    if (hi < nh) {
+      x = __ldg(hubs + hi);
+      want = x >= ls.plo && x < ls.phi && (__ldg(a.rows + x) & ls.pbit) && __ldg(a.g.deg + x) > kLeafLaneMax;
     }
     uint32_t todo = __ballot_sync(kFull, want);
     while (todo) {
@@ -1161,8 +1158,9 @@ void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s) {
   k_anchor_emit<<<blocks, 256, 0, s>>>(a);
 }
 
-void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, int num_sms, cudaStream_t s) {
-  if (nsig) k_leaf_prefill<<<unsigned(num_sms * 8), 256, 0, s>>>(a, sigs, nsig);
+void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, const uint32_t* hubs,
+                         const uint32_t* n_hubs, int num_sms, cudaStream_t s) {
+  if (nsig) k_leaf_prefill<<<unsigned(num_sms * 8), 256, 0, s>>>(a, sigs, nsig, hubs, n_hubs);
 }
 
 void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s) {

@@ -9,6 +9,8 @@
 // adjacency"; the PMA density rules are not carried over.
 #include "kernels.cuh"
 
+#include <cub/cub.cuh>
+
 namespace bdsm_b200 {
 
 namespace {
@@ -668,6 +670,23 @@ void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, un
   k_hot_hist<<<unsigned(num_sms * 8), kThreads, 0, s>>>(v, heat, hist);
   k_hot_select<<<1, 32, 0, s>>>(hist, budget);
   k_hot_pack<<<unsigned(num_sms * 16), kThreads, 0, s>>>(g, heat, hist, st);
+}
+struct DegAbove {
+  const uint32_t* deg;
+  uint32_t min_deg;
+  __host__ __device__ bool operator()(uint32_t v) const { return deg[v] > min_deg; }
+};
+// Hub list (ascending ids with more than min_deg neighbours) for the leaf prefill.
+size_t select_hubs_tmp_bytes(uint32_t V) {
+  size_t tmp = 0;
+  cub::DeviceSelect::If(nullptr, tmp, cub::CountingInputIterator<uint32_t>(0), (uint32_t*)nullptr,
+                        (uint32_t*)nullptr, int(V), DegAbove{nullptr, 0});
+  return tmp;
+}
+void launch_select_hubs(const uint32_t* deg, uint32_t V, uint32_t min_deg, uint32_t* hubs, uint32_t* n_hubs,
+                        void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  cub::DeviceSelect::If(tmp, tmp_bytes, cub::CountingInputIterator<uint32_t>(0), hubs, n_hubs, int(V),
+                        DegAbove{deg, min_deg}, s);
 }
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s) {
   if (g.loff && g.V) k_label_index<<<unsigned(num_sms * 16), 256, 0, s>>>(g);
