@@ -393,7 +393,13 @@ def ours(args, world, rank, local):
                       "dfs_visits": s["dfs_visits"], "tasks": s["tasks"], "items": s["work_items"],
                       "touched": s["touched"], "relocations": s["relocations"]} for s in statsA],
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and wl.meta["E"] > 500_000_000:
+        # the reference's PMA alone needs ~69 GB at the
+        # Friendster shape plus sort keys and an edge hash set
+        line["cpu_baseline"] = {"value": None, "unit": "updates/s", "cores": os.cpu_count(), "kind": "reference",
+                                "sample": "not run: the reference's graph build needs > 100 GB of host RAM at "
+                                          f"{wl.meta['E']} edges (SURVEY.md §8(d))"}
+    elif world == 1 and not args.no_cpu_baseline:
         tmp = tempfile.mkdtemp(prefix="bdsm_cpu_")
         path = os.path.join(tmp, "workload.bin")
         W.write_file(wl, path)

@@ -43,6 +43,9 @@ CONFIGS = {
     "C3": dict(kind="chunglu", V=3_100_000, E=117_000_000, L=16, qsize=8, qcat="dense", batch=100_000,
                mode="mixed", dmax=33_000, gamma=2.2,
                desc="Orkut-shaped synthetic (3.1M V, 117M E), 8-vertex dense query, 100K-update batch"),
+    "C4": dict(kind="chunglu_lean", V=65_000_000, E=1_800_000_000, L=16, qsize=6, qcat="sparse",
+               batch=1_000_000, mode="mixed", dmax=5_214, gamma=2.5,
+               desc="Friendster-shaped synthetic (65M V, 1.8B E, 16 labels), 6-vertex query, 1M-update batch"),
     "C5": dict(kind="chunglu", V=1_000_000, E=10_000_000, L=1, qsize=5, qcat="clique", batch=10_000,
                mode="mixed", dmax=5_000, gamma=2.3,
                desc="Batch-size sweep with unlabelled 5-vertex clique query"),
@@ -137,6 +140,101 @@ def chung_lu_graph(V: int, E: int, seed: int, device, dmax: int, gamma: float):
     return V, torch.minimum(a, b), torch.maximum(a, b)
 
 
+def chung_lu_keys(V: int, E: int, seed: int, device, dmax: int, gamma: float, chunk: int = 1 << 27):
+    """Memory-lean Chung-Lu for billion-edge shapes (C4): the same weight
+    sequence and one guaranteed edge per vertex as chung_lu_graph, sampled in
+    chunks straight into undirected keys (min << 32 | max); duplicates and
+    self-loops dropped, topped up until >= E, then a uniformly random surplus
+    removed, so exactly E edges.  Returns the sorted int64 keys (one array of
+    8 B per edge instead of the per-step copies of the small-shape path)."""
+    g = _gen(seed, device)
+    alpha = 1.0 / (gamma - 1.0)
+    i = torch.arange(V, dtype=torch.float64, device=device)
+    w = (i + 1.0) ** (-alpha)
+    del i
+    target = 2.0 * E / V
+    for _ in range(50):
+        w = w * (target * V / float(w.sum()))
+        w = torch.clamp(w, max=float(dmax))
+        if abs(float(w.sum()) / V - target) < 1e-3 * target:
+            break
+    cdf = torch.cumsum(w, 0)
+    cdf = cdf / cdf[-1]
+    del w
+    perm = torch.randperm(V, generator=g, device=device)
+
+    def keys_of(u, v):
+        u, v = perm[u], perm[v]
+        keep = u != v
+        u, v = u[keep], v[keep]
+        return (torch.minimum(u, v) << 32) | torch.maximum(u, v)
+
+    def draw(n):
+        r = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        return torch.clamp(torch.searchsorted(cdf, r), max=V - 1)
+
+    base_u = torch.arange(V, device=device)
+    base_v = draw(V)
+    base_v = torch.where(base_v == base_u, (base_v + 1) % V, base_v)
+    parts = [keys_of(base_u, base_v)]
+    del base_u, base_v
+    want = int((E - V) * 1.03) + 4096
+    while want > 0:
+        c = min(chunk, want)
+        parts.append(keys_of(draw(c), draw(c)))
+        want -= c
+    keys = torch.unique(torch.cat(parts))
+    del parts
+    while keys.numel() < E:  # top up
+        more = []
+        need = int((E - keys.numel()) * 1.5) + 4096
+        while need > 0:
+            c = min(chunk, need)
+            more.append(keys_of(draw(c), draw(c)))
+            need -= c
+        extra = torch.unique(torch.cat(more))
+        pos = torch.clamp(torch.searchsorted(keys, extra), max=keys.numel() - 1)
+        extra = extra[keys[pos] != extra]
+        keys = torch.sort(torch.cat([keys, extra])).values
+    surplus = keys.numel() - E
+    if surplus > 0:  # drop a uniformly random surplus
+        drop = torch.empty(0, dtype=torch.int64, device=device)
+        while drop.numel() < surplus:
+            drop = torch.unique(torch.cat([drop, torch.randint(0, keys.numel(), (2 * surplus + 16,), generator=g,
+                                                               device=device)]))
+        drop = drop[torch.randperm(drop.numel(), generator=g, device=device)[:surplus]]
+        keep = torch.ones(keys.numel(), dtype=torch.bool, device=device)
+        keep[drop] = False
+        keys = keys[keep]
+    return V, keys
+
+
+class _KeysGraph:
+    """Neighbour queries and degrees straight from the sorted undirected keys
+    (billion-edge shapes, where the directed CSR copy would not fit)."""
+
+    def __init__(self, keys: torch.Tensor, V: int):
+        self.keys = keys
+        self.V = V
+        deg = torch.zeros(V, dtype=torch.int64, device=keys.device)
+        step = 1 << 28
+        for s in range(0, keys.numel(), step):
+            k = keys[s:s + step]
+            deg += torch.bincount(k >> 32, minlength=V) + torch.bincount(k & 0xFFFFFFFF, minlength=V)
+        self.deg = deg
+        self.off_h = None
+
+    def degree(self, u: int) -> int:
+        return int(self.deg[u])
+
+    def neighbors(self, u: int) -> np.ndarray:
+        lo = int(torch.searchsorted(self.keys, torch.tensor([u << 32], device=self.keys.device)))
+        hi = int(torch.searchsorted(self.keys, torch.tensor([(u + 1) << 32], device=self.keys.device)))
+        up = self.keys[lo:hi] & 0xFFFFFFFF
+        down = self.keys[(self.keys & 0xFFFFFFFF) == u] >> 32
+        return torch.sort(torch.cat([up, down])).values.cpu().numpy()
+
+
 @dataclass
 class Workload:
     name: str
@@ -166,6 +264,9 @@ class _HostCSR:
         self.deg = counts
         self.off_h = self.off.cpu().numpy()
 
+    def degree(self, u: int) -> int:
+        return int(self.off_h[u + 1] - self.off_h[u])
+
     def neighbors(self, u: int) -> np.ndarray:
         lo, hi = int(self.off_h[u]), int(self.off_h[u + 1])
         return (self.keys[lo:hi] & 0xFFFFFFFF).cpu().numpy()
@@ -179,7 +280,7 @@ def extract_query(csr: _HostCSR, labels: np.ndarray, size: int, category: str, s
     V = len(labels)
     for _ in range(attempts):
         start = int(rng.integers(0, V))
-        if csr.off_h[start + 1] == csr.off_h[start]:
+        if csr.degree(start) == 0:
             continue
         members = [start]
         mset = {start}
@@ -227,18 +328,25 @@ def extract_query(csr: _HostCSR, labels: np.ndarray, size: int, category: str, s
     raise RuntimeError(f"could not extract a {category} query of size {size}")
 
 
-def make_stream(a: torch.Tensor, b: torch.Tensor, labels_t: torch.Tensor, V: int, nbatches: int,
-                batch: int, mode: str, seed: int) -> List[np.ndarray]:
+def make_stream(a: Optional[torch.Tensor], b: Optional[torch.Tensor], labels_t: torch.Tensor, V: int,
+                nbatches: int, batch: int, mode: str, seed: int,
+                keys: Optional[torch.Tensor] = None) -> List[np.ndarray]:
     """Mixed/insert/delete batches with the reference's sampling semantics
     (src/bench.cpp:222-287), vectorised: candidates are drawn in bulk and the
-    first valid ones in draw order are taken."""
-    device = a.device
+    first valid ones in draw order are taken.  `keys` (sorted undirected
+    min << 32 | max) replaces a, b for billion-edge shapes."""
+    device = labels_t.device
     g = _gen(seed, device)
-    keys = torch.sort((a << 32) | b).values  # current undirected edge set, sorted
-    la, lb = labels_t[a], labels_t[b]
+    if keys is None:
+        keys = torch.sort((a << 32) | b).values  # current undirected edge set, sorted
     L = int(labels_t.max()) + 1
     lp = torch.zeros(L * L, dtype=torch.bool, device=device)
-    lp[torch.minimum(la, lb) * L + torch.maximum(la, lb)] = True  # label pairs present in G
+    step = 1 << 28
+    for s0 in range(0, keys.numel(), step):  # label pairs present in G
+        k = keys[s0:s0 + step]
+        la, lb = labels_t[k >> 32], labels_t[k & 0xFFFFFFFF]
+        lp[torch.minimum(la, lb) * L + torch.maximum(la, lb)] = True
+        del la, lb
     out = []
     emitted = 0
     for _ in range(nbatches):
@@ -313,14 +421,18 @@ def build(name: str, nbatches: int, seed_graph: int = 1, seed_query: int = 7, se
     if device is None:
         device = "cuda" if torch.cuda.is_available() else "cpu"
     V, E = cfg["V"] // scale_down, cfg["E"] // scale_down
+    keys = None
     if cfg["kind"] == "rmat":
         scale = max(4, int(np.log2(V)))
         V, a, b = rmat_graph(scale, E, seed_graph, device)
+    elif cfg["kind"] == "chunglu_lean":
+        V, keys = chung_lu_keys(V, E, seed_graph, device, max(16, cfg["dmax"] // scale_down), cfg["gamma"])
+        a = b = None
     else:
         V, a, b = chung_lu_graph(V, E, seed_graph, device, max(16, cfg["dmax"] // scale_down), cfg["gamma"])
     lg = _gen(seed_graph + 1, device)
     labels_t = torch.randint(0, cfg["L"], (V,), generator=lg, device=device)
-    csr = _HostCSR(a, b, V)
+    csr = _HostCSR(a, b, V) if keys is None else _KeysGraph(keys, V)
     labels = labels_t.cpu().numpy().astype(np.uint32)
     if cfg["qcat"] == "clique":
         n = cfg["qsize"]
@@ -333,14 +445,26 @@ def build(name: str, nbatches: int, seed_graph: int = 1, seed_query: int = 7, se
     else:
         ql, qe = extract_query(csr, labels, cfg["qsize"], cfg["qcat"], seed_query)
     bsz = batch or cfg["batch"]
-    batches = make_stream(a, b, labels_t, V, nbatches, bsz, cfg["mode"], seed_stream)
+    batches = make_stream(a, b, labels_t, V, nbatches, bsz, cfg["mode"], seed_stream, keys=keys)
     deg = csr.deg
-    meta = {"V": V, "E": int(a.numel()), "L": cfg["L"], "d_max": int(deg.max()), "d_mean": float(deg.float().mean()),
+    meta = {"V": V, "E": int(a.numel()) if keys is None else int(keys.numel()), "L": cfg["L"], "d_max": int(deg.max()), "d_mean": float(deg.float().mean()),
             "isolated": int((deg == 0).sum()), "batch": bsz, "mode": cfg["mode"], "generator": cfg["kind"],
             "seeds": {"graph": seed_graph, "query": seed_query, "stream": seed_stream}, "desc": cfg["desc"]}
-    wl = Workload(name, V, labels, a.cpu().numpy().astype(np.uint32), b.cpu().numpy().astype(np.uint32),
-                  ql, qe, batches, meta)
+    if keys is not None:  # u32 endpoint arrays, converted in slices
+        src = np.empty(keys.numel(), np.uint32)
+        dst = np.empty(keys.numel(), np.uint32)
+        step = 1 << 28
+        for s0 in range(0, keys.numel(), step):
+            k = keys[s0:s0 + step]
+            src[s0:s0 + k.numel()] = (k >> 32).to(torch.int32).cpu().numpy().view(np.uint32)
+            dst[s0:s0 + k.numel()] = (k & 0xFFFFFFFF).to(torch.int32).cpu().numpy().view(np.uint32)
+        del keys
+    else:
+        src, dst = a.cpu().numpy().astype(np.uint32), b.cpu().numpy().astype(np.uint32)
+    wl = Workload(name, V, labels, src, dst, ql, qe, batches, meta)
     del csr
+    if torch.cuda.is_available():
+        torch.cuda.empty_cache()
     return wl
 
 
