@@ -582,6 +582,7 @@ struct bdsm_engine {
       const auto r = label_range(de.glabel[gi]);
       de.glo[gi] = r.first;
       de.ghi[gi] = r.second;
+      de.gcls[gi] = label_class(de.glabel[gi]);
     }
     for (uint32_t u = 0; u < de.n; ++u)
       for (uint32_t gi = 0; gi < de.G; ++gi) de.qcnt[u][gi] = qs->enc.qcnt[u * de.G + gi];

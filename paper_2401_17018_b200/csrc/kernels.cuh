@@ -17,6 +17,7 @@ struct DevQueryEnc {
   uint32_t qlabel[kMaxQ];
   uint32_t glabel[kMaxQ];
   uint32_t glo[kMaxQ], ghi[kMaxQ];  // internal-id range of each group's label (ids are label-ordered)
+  uint32_t gcls[kMaxQ];          // label class index of each group's label (kNone: absent from the graph)
   uint8_t qcnt[kMaxQ][kMaxQ];    // [u][g]
 };
 

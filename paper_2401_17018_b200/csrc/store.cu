@@ -349,7 +349,10 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
     uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
     uint32_t* edst = g.elab ? g.elab + noff : nullptr;
 
-    // 1. insert slots against the intact old list
+    // 1. insert slots against the intact old list; lane 31 meanwhile finds the
+    // first position that can move (elements below the first batch key never move)
+    uint32_t start = 0;
+    if (lane == 31 && !reloc && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
     for (uint32_t k = lane; k < segn; k += 32) {
       if (svals[s + k] >> 31) continue;  // delete
       uint32_t y = uint32_t(seg[k]);
@@ -358,12 +361,8 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
     }
     __syncwarp();
-    // 2. move old elements (elements below the first batch key never move)
-    uint32_t start = 0;
-    if (!reloc) {
-      if (lane == 0 && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
-      start = __shfl_sync(kFull, start, 0);
-    }
+    // 2. move old elements
+    start = __shfl_sync(kFull, start, 31);
     const bool ascending = reloc || nins == 0;  // left-movers ascend, right-movers descend
     const uint32_t step = 32 * kMoveUnroll;
     const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
@@ -417,15 +416,28 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
-    // label index of the new list
+    // label index of the new list (lane k: class k's first position)
+    uint32_t lpos = 0;
     if (g.loff)
-      for (uint32_t k = lane; k <= g.nlab; k += 32)
-        g.loff[uint64_t(x) * (g.nlab + 1) + k] = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
+      for (uint32_t k = lane; k <= g.nlab; k += 32) {
+        lpos = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
+        g.loff[uint64_t(x) * (g.nlab + 1) + k] = lpos;
+      }
+    const bool from_index = g.loff && g.nlab < 32;  // the whole index sits in lanes 0..nlab
     // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
     const uint32_t vl = g.vlabel[x];
     for (uint32_t q = 0; q < nq; ++q) {
       const DevQueryEnc& qe = qenc[q];
-      const uint32_t cnt = group_counts(dst, dnew, qe, lane);
+      uint32_t cnt;
+      if (from_index) {  // group g's count = the size of its label class's range
+        const uint32_t cls = lane < qe.G ? qe.gcls[lane] : kNone;
+        const uint32_t lo = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls);
+        const uint32_t hi = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls + 1);
+        cnt = cls == kNone ? 0 : hi - lo;
+        if (cnt > qe.cap) cnt = qe.cap;
+      } else {
+        cnt = group_counts(dst, dnew, qe, lane);
+      }
       const uint32_t row = row_of(qe, vl, cnt, lane);
       if (lane == 0) {
         const uint32_t word = rows[q][x];
