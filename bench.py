@@ -297,7 +297,7 @@ def ours(args, world, rank, local):
                 import torch.distributed as dist
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record()
-                dist.broadcast(dev_batches[i], src=0)
+                dist.broadcast(dev_batches[i].view(torch.int32), src=0)
                 torch.cuda.current_stream().synchronize()
                 r = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
                 cnt = torch.tensor([r.positive[0], r.negative[0]], dtype=torch.int64, device=dev)

@@ -29,9 +29,16 @@ struct DevGraph {
   // graph has more than kMaxLabelIndex label classes.
   const uint32_t* loff;
   uint32_t nlab;
+  // Hub membership bitmaps: hub_slot[v] = bitmap index of a high-degree vertex
+  // (kNone otherwise); bitmap h holds bit y set iff y is a neighbour, so a
+  // membership test in a hub's list is one load instead of a binary search.
+  const uint32_t* hub_slot;
+  const uint32_t* bitmaps;
+  uint64_t bm_words;       // words per bitmap ((V + 31) / 32)
 };
 
 constexpr uint32_t kMaxLabelIndex = 64;
+constexpr uint32_t kBitmapMinDeg = 1024;  // lists this long get a membership bitmap (within the budget)
 
 #ifdef __CUDACC__
 // Label sub-range [lo, hi) of label class `cls` (id range [vlo, vhi)) in x's

@@ -126,6 +126,8 @@ struct bdsm_engine {
   DBuf<uint64_t> off;
   DBuf<uint32_t> deg, cap, adj, elab, vlabel;
   DBuf<uint32_t> loff, class_lo;  // label index (DevGraph::loff) and label-class start ids
+  DBuf<uint32_t> hub_slot, bitmaps;  // hub membership bitmaps (DevGraph::hub_slot)
+  uint64_t bm_words = 0;
 
   std::vector<std::unique_ptr<QueryState>> queries;
   DBuf<DevQueryEnc> d_qenc;
@@ -273,6 +275,9 @@ struct bdsm_engine {
     v.vlabel = g.vlabel;
     v.loff = g.loff;
     v.nlab = g.nlab;
+    v.hub_slot = g.hub_slot;
+    v.bitmaps = g.bitmaps;
+    v.bm_words = g.bm_words;
     return v;
   }
 
@@ -324,6 +329,7 @@ struct bdsm_engine {
     build_internal(&internal);
     orig_desc = nullptr;
     build_label_index();
+    build_bitmaps();
   }
 
   // Label index over the label classes (label_ranges order); disabled for
@@ -344,6 +350,43 @@ struct bdsm_engine {
     loff.ensure(uint64_t(g.V) * (nl + 1));
     refresh_graph_view();
     launch_label_index(g, num_sms, stream);
+    sync();
+  }
+
+  // Membership bitmaps for the highest-degree vertices (>= kBitmapMinDeg
+  // neighbours; BDSM_BITMAP_MINDEG overrides, tests use it to exercise the
+  // path on small graphs), as many as fit the budget (BDSM_BITMAP_MB, default 2048).
+  // The set is fixed at build; the merge keeps each bitmap in step with its list.
+  void build_bitmaps() {
+    hub_slot.release();
+    bitmaps.release();
+    if (g.V == 0) return;
+    const uint64_t words = (uint64_t(g.V) + 31) / 32;
+    const uint64_t budget = uint64_t(env_u32("BDSM_BITMAP_MB", 2048)) << 20;
+    const uint64_t maxh = budget / (4 * words);
+    if (maxh == 0) return;
+    std::vector<uint32_t> d(g.V);
+    CK(cudaMemcpyAsync(d.data(), g.deg, 4ull * g.V, cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::vector<uint32_t> hubs;
+    const uint32_t min_deg = env_u32("BDSM_BITMAP_MINDEG", kBitmapMinDeg);
+    for (uint32_t v = 0; v < g.V; ++v)
+      if (d[v] >= min_deg) hubs.push_back(v);
+    if (hubs.empty()) return;
+    std::sort(hubs.begin(), hubs.end(), [&](uint32_t a, uint32_t b) { return d[a] != d[b] ? d[a] > d[b] : a < b; });
+    if (hubs.size() > maxh) hubs.resize(maxh);
+    std::vector<uint32_t> slot(g.V, kNone);
+    for (uint32_t i = 0; i < hubs.size(); ++i) slot[hubs[i]] = i;
+    hub_slot.ensure(g.V);
+    CK(cudaMemcpyAsync(hub_slot.p, slot.data(), 4ull * g.V, cudaMemcpyHostToDevice, stream));
+    bitmaps.ensure(words * hubs.size());
+    CK(cudaMemsetAsync(bitmaps.p, 0, 4ull * words * hubs.size(), stream));
+    bm_words = words;
+    DBuf<uint32_t> dh;
+    dh.ensure(hubs.size());
+    CK(cudaMemcpyAsync(dh.p, hubs.data(), 4ull * hubs.size(), cudaMemcpyHostToDevice, stream));
+    refresh_graph_view();
+    launch_build_bitmaps(g, dh.p, uint32_t(hubs.size()), stream);
     sync();
   }
 
@@ -469,6 +512,9 @@ struct bdsm_engine {
     g.vlabel = vlabel.p;
     g.loff = loff.n ? loff.p : nullptr;
     g.class_lo = class_lo.p;
+    g.hub_slot = hub_slot.n ? hub_slot.p : nullptr;
+    g.bitmaps = bitmaps.p;
+    g.bm_words = bm_words;
   }
 
   [[noreturn]] void throw_build_error(const bdsm_graph_desc* d, uint32_t bad) {

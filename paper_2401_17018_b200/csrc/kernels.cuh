@@ -34,6 +34,9 @@ struct DevGraphMut {
   uint32_t* loff;                // label index (see DevGraph), or nullptr
   uint32_t nlab;
   const uint32_t* class_lo;      // first internal id of each label class [nlab]
+  const uint32_t* hub_slot;      // membership bitmaps (see DevGraph), or nullptr
+  uint32_t* bitmaps;
+  uint64_t bm_words;
 };
 
 // ---- store.cu: build ------------------------------------------------------
@@ -69,6 +72,7 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s);
+void launch_build_bitmaps(DevGraphMut g, const uint32_t* hubs, uint32_t nhubs, cudaStream_t s);
 void launch_hot_walks(const uint32_t* heads, const uint64_t* skeys, const BatchState* st, DevGraph g,
                       uint32_t* heat, uint32_t walks, uint32_t depth, uint32_t seed, int num_sms, cudaStream_t s);
 void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, unsigned long long budget,

@@ -349,6 +349,13 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
     if (b == dpos) continue;
     if (!__any_sync(kFull, ok)) break;
     const uint32_t x = M[lp.back[b]];
+    if (g.hub_slot && !g.elab) {  // hub list: one bitmap load instead of a search
+      const uint32_t hs = __ldg(g.hub_slot + x);
+      if (hs != kNone) {
+        if (ok) ok = (__ldg(g.bitmaps + uint64_t(hs) * g.bm_words + (c >> 5)) >> (c & 31)) & 1u;
+        continue;
+      }
+    }
     const uint64_t xo = __ldg(g.off + x);
     const uint32_t xd = __ldg(g.deg + x);
     // search window: label sub-range [floor, ceil), the floor advancing

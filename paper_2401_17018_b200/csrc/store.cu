@@ -416,6 +416,18 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
+    // membership bitmap of a hub: set inserted, clear deleted neighbours
+    if (g.hub_slot) {
+      const uint32_t hs = g.hub_slot[x];
+      if (hs != kNone) {
+        uint32_t* bm = g.bitmaps + uint64_t(hs) * g.bm_words;
+        for (uint32_t k = lane; k < segn; k += 32) {
+          const uint32_t y = uint32_t(seg[k]);
+          if (svals[s + k] >> 31) atomicAnd(bm + (y >> 5), ~(1u << (y & 31)));
+          else atomicOr(bm + (y >> 5), 1u << (y & 31));
+        }
+      }
+    }
     // label index of the new list (lane k: class k's first position)
     uint32_t lpos = 0;
     if (g.loff)
@@ -678,7 +690,7 @@ void launch_hot_walks(const uint32_t* heads, const uint64_t* skeys, const BatchS
 void launch_hot_pack(DevGraphMut g, uint32_t* heat, unsigned long long* hist, unsigned long long budget,
                      BatchState* st, int num_sms, cudaStream_t s) {
   cudaMemsetAsync(hist, 0, 34 * sizeof(unsigned long long), s);
-  DevGraph v{g.V, g.off, g.deg, g.cap, g.adj, g.elab, g.vlabel, g.loff, g.nlab};
+  DevGraph v{g.V, g.off, g.deg, g.cap, g.adj, g.elab, g.vlabel, g.loff, g.nlab, g.hub_slot, g.bitmaps, g.bm_words};
   k_hot_hist<<<unsigned(num_sms * 8), kThreads, 0, s>>>(v, heat, hist);
   k_hot_select<<<1, 32, 0, s>>>(hist, budget);
   k_hot_pack<<<unsigned(num_sms * 16), kThreads, 0, s>>>(g, heat, hist, st);
@@ -699,6 +711,24 @@ void launch_select_hubs(const uint32_t* deg, uint32_t V, uint32_t min_deg, uint3
                         void* tmp, size_t tmp_bytes, cudaStream_t s) {
   cub::DeviceSelect::If(tmp, tmp_bytes, cub::CountingInputIterator<uint32_t>(0), hubs, n_hubs, int(V),
                         DegAbove{deg, min_deg}, s);
+}
+// Warp per hub: set the bit of every neighbour.
+__global__ void k_build_bitmaps(DevGraphMut g, const uint32_t* __restrict__ hubs, uint32_t nhubs) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t h = warp; h < nhubs; h += nwarps) {
+    const uint32_t v = hubs[h];
+    uint32_t* bm = g.bitmaps + uint64_t(g.hub_slot[v]) * g.bm_words;
+    const uint32_t* lst = g.adj + g.off[v];
+    for (uint32_t i = lane; i < g.deg[v]; i += 32) {
+      const uint32_t y = lst[i];
+      atomicOr(bm + (y >> 5), 1u << (y & 31));
+    }
+  }
+}
+void launch_build_bitmaps(DevGraphMut g, const uint32_t* hubs, uint32_t nhubs, cudaStream_t s) {
+  if (nhubs) k_build_bitmaps<<<blocks_for(uint64_t(nhubs) * 32), kThreads, 0, s>>>(g, hubs, nhubs);
 }
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s) {
   if (g.loff && g.V) k_label_index<<<unsigned(num_sms * 16), 256, 0, s>>>(g);

@@ -173,3 +173,17 @@ def test_storage_options_do_not_change_counts(opts):
         exp = o.apply_batch(b)
         assert (r.positive[0], r.negative[0]) == (exp[0][0], exp[1][0]), (bi, opts)
     e.close()
+
+
+def test_hub_bitmaps_do_not_change_counts(monkeypatch):
+    """Membership bitmaps (normally for lists >= 1024) forced onto every
+    vertex with >= 4 neighbours, so the golden suites run the bitmap
+    membership tests and their maintenance by the merge."""
+    monkeypatch.setenv("BDSM_BITMAP_MINDEG", "4")
+    for suite in ("streams", "skewed", "matcher_random"):
+        for inst in gu.load(suite):
+            e, batches = _engine(inst)
+            for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
+                r = e.match_batch(b)
+                assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (suite, inst["name"], bi)
+            e.close()
