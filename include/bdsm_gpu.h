@@ -160,6 +160,13 @@ BDSM_API const char* bdsm_last_error(void);
 BDSM_API size_t bdsm_engine_neighbors(bdsm_engine* engine, uint32_t v, uint32_t* out, size_t cap);
 BDSM_API bdsm_status bdsm_engine_rows(bdsm_engine* engine, int query, uint32_t* out /* [V] */);
 BDSM_API int bdsm_engine_order(bdsm_engine* engine, int query, uint32_t edge, uint32_t* out /* [32] */);
+/* Host-only planner (no device): the matching order of `query` anchored at
+ * query edge `edge` for the given candidate column sizes — build_query_plan's
+ * per-edge order with coalescing off (src/query_analysis.cpp:295-363,
+ * :437-441) — into order[num_vertices], and optionally the counted-tail level.
+ * Returns num_vertices or -status. */
+BDSM_API int bdsm_plan_order(const bdsm_query_desc* query, const uint64_t* column_sizes, uint32_t edge,
+                             uint32_t* order, uint32_t* tail);
 /* First level T of the independent tail of that order: levels > T are counted
  * once per prefix and multiplied instead of enumerated (no reference counterpart). */
 BDSM_API int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge);

@@ -180,8 +180,33 @@ def ref():
             C.c_uint32, _u32p, C.c_uint64, _u32p, _u32p, C.c_void_p,
             C.c_uint32, _u32p, C.c_uint32, _u32p, _u32p, C.c_void_p,
             C.c_uint64, _u32p, _u32p, _u8p, C.c_void_p, _u64p, _u64p, C.c_char_p, C.c_size_t]
+        L.ref_plan_orders.restype = C.c_int
+        L.ref_plan_orders.argtypes = [
+            C.c_uint32, _u32p, C.c_uint64, _u32p, _u32p, C.c_void_p,
+            C.c_uint32, _u32p, C.c_uint32, _u32p, _u32p, C.c_void_p, C.c_uint32, _u32p, _u64p,
+            C.c_char_p, C.c_size_t]
         _ref = L
     return _ref
+
+
+def ref_plan_orders(vlabels, eu, ev, elab, qlabels, qedges, group_bits: int = 2):
+    """The UNMODIFIED reference's plan with coalescing off: (orders per query
+    edge, candidate column sizes it was built from)."""
+    vl, eu, ev = _arr(vlabels), _arr(eu), _arr(ev)
+    el = None if elab is None else _arr(elab)
+    ql = _arr(qlabels)
+    qa = _arr([e[0] for e in qedges])
+    qb = _arr([e[1] for e in qedges])
+    qlab = _arr([NONE if (len(e) < 3 or e[2] is None or e[2] < 0) else e[2] for e in qedges])
+    orders = np.zeros(32 * max(len(qa), 1), np.uint32)
+    cols = np.zeros(max(len(ql), 1), np.uint64)
+    err = C.create_string_buffer(512)
+    r = ref().ref_plan_orders(len(vl), vl, len(eu), eu, ev, _opt_ptr(el), len(ql), ql, len(qa), qa, qb,
+                              _opt_ptr(qlab), group_bits, orders, cols, err, 512)
+    if r != 0:
+        raise OracleError(r, err.value.decode())
+    n = len(ql)
+    return [orders[32 * e: 32 * e + n].tolist() for e in range(len(qa))], cols[:n].tolist()
 
 
 def ref_run_stream(vlabels, eu, ev, elab, qlabels, qedges, batches: Sequence, workers: int = 1,

@@ -101,6 +101,38 @@ QueryPlan make_plan(const QueryGraph& q, const CandidateTable& table, int plan_m
 
 extern "C" {
 
+// The reference's per-edge matching orders, generate_matching_order
+// (src/query_analysis.cpp:358-363) for every query edge (plan_mode 0 above:
+// the plan the restatement and the GPU engine implement; build_query_plan
+// additionally re-orders the edges of k-degenerated coalescing groups with a
+// zone and join tail, :375-435, which only feeds the coalesced search, SURVEY
+// F1): orders_out[e * 32 + i] and the candidate column sizes (colsizes_out[u]).
+// Returns 0, or 2 / 3 on invalid_argument / other exceptions.
+int ref_plan_orders(std::uint32_t nv, const std::uint32_t* vlabels, std::uint64_t ne, const std::uint32_t* eu,
+                    const std::uint32_t* ev, const std::uint32_t* elab, std::uint32_t qn,
+                    const std::uint32_t* qlabels, std::uint32_t qm, const std::uint32_t* qa,
+                    const std::uint32_t* qb, const std::uint32_t* qlab, std::uint32_t group_bits,
+                    std::uint32_t* orders_out, std::uint64_t* colsizes_out, char* err, std::size_t errcap) {
+  try {
+    LabeledGraph g = make_graph(nv, vlabels, ne, eu, ev, elab);
+    QueryGraph q = make_query(qn, qlabels, qm, qa, qb, qlab);
+    auto enc = QueryEncodingState::initialize(g, q, group_bits);
+    QueryPlan plan = make_plan(q, enc.table, 0);
+    for (std::size_t e = 0; e < plan.edge_plans.size(); ++e)
+      if (plan.edge_plans[e].order)
+        for (std::size_t i = 0; i < plan.edge_plans[e].order->order.size(); ++i)
+        orders_out[e * 32 + i] = plan.edge_plans[e].order->order[i];
+    for (std::size_t u = 0; u < plan.column_sizes.size(); ++u) colsizes_out[u] = plan.column_sizes[u];
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    set_err(err, errcap, e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    set_err(err, errcap, e.what());
+    return 3;
+  }
+}
+
 // Status: 0 ok, 1 BatchError (err_index = first failing update, in batch
 // err_batch), 2 std::invalid_argument, 3 other exception.
 //

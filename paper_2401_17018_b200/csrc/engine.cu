@@ -1362,6 +1362,32 @@ int64_t bdsm_engine_matches(bdsm_engine* engine, int query, int phase, uint32_t*
   return st == BDSM_OK ? r : -int64_t(st);
 }
 
+int bdsm_plan_order(const bdsm_query_desc* query, const uint64_t* column_sizes, uint32_t edge, uint32_t* order,
+                    uint32_t* tail) {
+  int r = -int(BDSM_INVALID_ARGUMENT);
+  bdsm_status st = guarded([&]() -> bdsm_status {
+    if (!query || !column_sizes || !order) throw std::invalid_argument("null argument");
+    std::vector<uint32_t> labels(query->vertex_labels, query->vertex_labels + query->num_vertices);
+    std::vector<QEdge> edges;
+    for (uint32_t i = 0; i < query->num_edges; ++i)
+      edges.push_back({query->a[i], query->b[i], query->edge_labels ? query->edge_labels[i] : kNone});
+    HostQuery q(std::move(labels), std::move(edges));
+    if (!q.connected()) throw std::invalid_argument("disconnected query graph");
+    if (edge >= q.edges.size()) throw std::invalid_argument("query edge out of range");
+    std::vector<uint64_t> cs(column_sizes, column_sizes + q.n);
+    const std::vector<uint32_t> o = matching_order(q, edge, cs);
+    for (size_t i = 0; i < o.size(); ++i) order[i] = o[i];
+    if (tail) {
+      std::vector<std::pair<uint32_t, uint32_t>> ranges(q.n, {0, 0});
+      std::vector<uint32_t> classes(q.n, kNone);
+      *tail = q.n <= uint32_t(kMaxQ) ? build_program(q, 0, o, ranges, classes).tail : 0;
+    }
+    r = int(o.size());
+    return BDSM_OK;
+  });
+  return st == BDSM_OK ? r : -int(st);
+}
+
 int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge) {
   if (!engine || query < 0 || size_t(query) >= engine->queries.size()) return -int(BDSM_INVALID_ARGUMENT);
   QueryState& qs = *engine->queries[size_t(query)];
