@@ -323,14 +323,20 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
                                                  uint32_t* floor_l, const uint32_t* ceil_l, uint64_t c_off,
                                                  uint32_t cur, uint32_t end2, uint32_t dpos, uint32_t touched,
                                                  uint32_t anchor, uint32_t flag, uint32_t lane, uint32_t& c_out,
-                                                 bool& tc_out) {
+                                                 bool& tc_out, bool have_pf = false, uint32_t pf_c = 0,
+                                                 uint32_t pf_rw = 0) {
   const DevGraph& g = a.g;
   const uint32_t idx = cur + lane;
   bool ok = idx < end2;
   uint32_t c = 0xffffffffu;
-  if (ok) c = __ldg(g.adj + c_off + idx);
   uint32_t rw = 0;
-  if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
+  if (have_pf) {  // driver entry and its row were prefetched while the previous chunk was weighted
+    c = pf_c;
+    rw = pf_rw;
+  } else {
+    if (ok) c = __ldg(g.adj + c_off + idx);
+    if (ok) rw = __ldg(a.rows + c);  // candidate bits + batch-endpoint flags
+  }
   ok = ok && (rw & lp.qbit) != 0;
   if (ok && g.elab) ok = __ldg(g.elab + c_off + idx) == lp.elab[dpos];
   if (ok) {  // injectivity: only same-label positions can collide
@@ -725,7 +731,7 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
 }
 
 #ifndef BDSM_WBM_MIN_BLOCKS
-#define BDSM_WBM_MIN_BLOCKS 4  // resident 256-thread CTAs per SM the register budget must allow
+#define BDSM_WBM_MIN_BLOCKS 2  // resident 256-thread CTAs per SM the register budget must allow (sweep: 2 beats 3, 4)
 #endif
 // kEmit: bounded match materialisation (the reference's Match vectors,
 // src/matcher.cpp:169-217, for --dump-matches): the whole order is
@@ -757,6 +763,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
   __syncwarp();
   uint32_t dtick = 0;
   unsigned long long tt_pref = 0;  // prefetched donation-demand poll
+  uint32_t pf_c = 0, pf_rw = 0, pf_pos = kNone;  // prefetched next chunk of the last DFS level
   bool timed_out = false;
   bool static_done = false;
   uint32_t ticket = kNone;  // lane 0: outstanding ticket of this warp
@@ -852,6 +859,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
     const uint32_t anchor = task.upd;
     const uint32_t T = kEmit ? P.n - 1 : P.tail;  // deepest DFS level; deeper levels are counted by tail_factor
     uint32_t tvalid = 0;        // tail levels whose cached count is current
+    pf_pos = kNone;
     if (kind == 1) {
       const bdsm_update_dev up = a.ups[task.upd];
       const uint32_t m0 = task.flip ? up.v : up.u, m1 = task.flip ? up.u : up.v;
@@ -894,6 +902,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         if (c_cur >= c_end) {
           if (l == lstart) break;
           --l;  // backtrack: restore the parked state of level l
+          pf_pos = kNone;
           c_off = __shfl_sync(kFull, r_off, l);
           c_cur = __shfl_sync(kFull, r_cur, l);
           c_end = __shfl_sync(kFull, r_end, l);
@@ -1000,7 +1009,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
         cy0 = clock64();
 #endif
         const uint32_t m = filter_chunk(a, P.lv[l], s_M[w], s_floor[w][l], s_ceil[w][l], c_off, cur, c_end, c_drv,
-                                        touched, anchor, flag, lane, c, tc);
+                                        touched, anchor, flag, lane, c, tc, pf_pos == cur, pf_c, pf_rw);
+        pf_pos = kNone;
+        // last DFS level: the next chunk's driver entries are loaded now, their
+        // rows after this chunk's weights, so both round trips overlap the work
+        const bool prefetch = l == T && c_cur < c_end;
+        if (prefetch) pf_c = c_cur + lane < c_end ? __ldg(g.adj + c_off + c_cur + lane) : kNone;
 #ifdef BDSM_TRACE
         cy_filter += clock64() - cy0;
         cy0 = clock64();
@@ -1053,6 +1067,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
 #ifdef BDSM_TRACE
           cy_leaf += clock64() - cy0;
 #endif
+          if (prefetch) {
+            pf_rw = pf_c != kNone ? __ldg(a.rows + pf_c) : 0u;
+            pf_pos = c_cur;
+          }
           continue;
         }
         if (l == T) {  // last DFS level: every survivor roots the counted tail
@@ -1064,6 +1082,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
             stat[2] += pm * tf.b;
             stat[3] += pm * tf.c;
           }
+          if (prefetch) {
+            pf_rw = pf_c != kNone ? __ldg(a.rows + pf_c) : 0u;
+            pf_pos = c_cur;
+          }
           continue;
         }
         if (lane == 0) stat[1] += __popc(m);
@@ -1074,6 +1096,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wb
       } else {
         const uint32_t k = __ffs(c_mask) - 1;
         c_mask &= c_mask - 1;
+        pf_pos = kNone;
         const uint32_t c = s_cand[w][l][k];
         if (lane == 0) s_M[w][l] = c;
         tvalid &= ~P.inval[l];
