@@ -230,6 +230,9 @@ __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, ui
   }
 }
 
+constexpr uint32_t kBigList = 4096;        // lists this long are merged by a whole CTA (k_merge_big)
+constexpr uint32_t kBigFlag = 0x80000000u;  // new_cap[t]: the list is merged by k_merge_big
+
 __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, uint32_t nt, uint32_t m) {
   return t + 1 < nt ? heads[t + 1] : m;
 }
@@ -246,15 +249,18 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
     uint32_t x = uint32_t(skeys[s] >> 32);
     uint32_t nins = ins_prefix[e] - ins_prefix[s];
     uint32_t ndel = (e - s) - nins;
-    uint32_t dnew = g.deg[x] + nins - ndel;
+    const uint32_t dold = g.deg[x];
+    uint32_t dnew = dold + nins - ndel;
+    // top bit: the pre-batch list is long (merged by k_merge_big, not k_merge_refresh)
+    const uint32_t big = dold >= kBigList ? kBigFlag : 0u;
     if (dnew > g.cap[x] || (nins && ndel)) {  // overflow, or a mixed segment (see merge)
       uint32_t c = slack_cap(dnew, slack);
       new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
-      new_cap[t] = c;
+      new_cap[t] = c | big;
       atomicAdd((unsigned long long*)&st->relocations, 1ull);
     } else {
       new_off[t] = g.off[x];
-      new_cap[t] = 0;  // in place
+      new_cap[t] = big;  // in place
     }
   }
 }
@@ -305,6 +311,65 @@ __device__ __forceinline__ uint32_t row_of(const DevQueryEnc& qe, uint32_t vl, u
   return row;
 }
 
+// After a list's merge (warp-collective): keep its membership bitmap in step,
+// rewrite its label index, and recompute every query's candidate row from the
+// label-range counts of the new list (K4).
+__device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const uint32_t* dst, uint32_t dnew,
+                                              const uint64_t* seg, uint32_t segn, const uint32_t* segvals,
+                                              const DevQueryEnc* __restrict__ qenc, uint32_t nq,
+                                              uint32_t* const* rows, uint64_t* const* colsize, uint32_t lane) {
+    // membership bitmap of a hub: set inserted, clear deleted neighbours
+    if (g.hub_slot) {
+      const uint32_t hs = g.hub_slot[x];
+      if (hs != kNone) {
+        uint32_t* bm = g.bitmaps + uint64_t(hs) * g.bm_words;
+        for (uint32_t k = lane; k < segn; k += 32) {
+          const uint32_t y = uint32_t(seg[k]);
+          if (segvals[k] >> 31) atomicAnd(bm + (y >> 5), ~(1u << (y & 31)));
+          else atomicOr(bm + (y >> 5), 1u << (y & 31));
+        }
+      }
+    }
+    // label index of the new list (lane k: class k's first position)
+    uint32_t lpos = 0;
+    if (g.loff)
+      for (uint32_t k = lane; k <= g.nlab; k += 32) {
+        lpos = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
+        g.loff[uint64_t(x) * (g.nlab + 1) + k] = lpos;
+      }
+    const bool from_index = g.loff && g.nlab < 32;  // the whole index sits in lanes 0..nlab
+    // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
+    const uint32_t vl = g.vlabel[x];
+    for (uint32_t q = 0; q < nq; ++q) {
+      const DevQueryEnc& qe = qenc[q];
+      uint32_t cnt;
+      if (from_index) {  // group g's count = the size of its label class's range
+        const uint32_t cls = lane < qe.G ? qe.gcls[lane] : kNone;
+        const uint32_t lo = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls);
+        const uint32_t hi = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls + 1);
+        cnt = cls == kNone ? 0 : hi - lo;
+        if (cnt > qe.cap) cnt = qe.cap;
+      } else {
+        cnt = group_counts(dst, dnew, qe, lane);
+      }
+      const uint32_t row = row_of(qe, vl, cnt, lane);
+      if (lane == 0) {
+        const uint32_t word = rows[q][x];
+        const uint32_t before = word & ~kRowFlags;  // keep the batch flags
+        if (before != row) {
+          rows[q][x] = row | (word & kRowFlags);
+          uint32_t diff = before ^ row;
+          while (diff) {
+            uint32_t u = __ffs(diff) - 1;
+            diff &= diff - 1;
+            atomicAdd((unsigned long long*)(colsize[q] + u),
+                      (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
+          }
+        }
+      }
+    }
+  }
+
 constexpr uint32_t kMoveUnroll = 8;  // old elements per lane in flight per sweep step
 
 // K3 (part 2) + K4: one warp per touched vertex.  Insert slots are computed
@@ -342,7 +407,9 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
     const uint64_t ooff = g.off[x];
     const uint32_t nins = ins_prefix[e] - ins_prefix[s];
     const uint32_t dnew = dold + nins - (segn - nins);
-    const bool reloc = new_cap[t] != 0;
+    if (new_cap[t] & kBigFlag) continue;  // k_merge_big: a whole CTA per long list
+    const uint32_t ncap = new_cap[t];
+    const bool reloc = ncap != 0;
     const uint64_t noff = new_off[t];
     uint32_t* src = g.adj + ooff;
     uint32_t* dst = g.adj + noff;
@@ -412,62 +479,116 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       g.deg[x] = dnew;
       if (reloc) {
         g.off[x] = noff;
-        g.cap[x] = new_cap[t];
+        g.cap[x] = ncap;
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
-    // membership bitmap of a hub: set inserted, clear deleted neighbours
-    if (g.hub_slot) {
-      const uint32_t hs = g.hub_slot[x];
-      if (hs != kNone) {
-        uint32_t* bm = g.bitmaps + uint64_t(hs) * g.bm_words;
-        for (uint32_t k = lane; k < segn; k += 32) {
-          const uint32_t y = uint32_t(seg[k]);
-          if (svals[s + k] >> 31) atomicAnd(bm + (y >> 5), ~(1u << (y & 31)));
-          else atomicOr(bm + (y >> 5), 1u << (y & 31));
-        }
-      }
-    }
-    // label index of the new list (lane k: class k's first position)
-    uint32_t lpos = 0;
-    if (g.loff)
-      for (uint32_t k = lane; k <= g.nlab; k += 32) {
-        lpos = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
-        g.loff[uint64_t(x) * (g.nlab + 1) + k] = lpos;
-      }
-    const bool from_index = g.loff && g.nlab < 32;  // the whole index sits in lanes 0..nlab
-    // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
-    const uint32_t vl = g.vlabel[x];
-    for (uint32_t q = 0; q < nq; ++q) {
-      const DevQueryEnc& qe = qenc[q];
-      uint32_t cnt;
-      if (from_index) {  // group g's count = the size of its label class's range
-        const uint32_t cls = lane < qe.G ? qe.gcls[lane] : kNone;
-        const uint32_t lo = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls);
-        const uint32_t hi = __shfl_sync(kFull, lpos, cls == kNone ? 0 : cls + 1);
-        cnt = cls == kNone ? 0 : hi - lo;
-        if (cnt > qe.cap) cnt = qe.cap;
-      } else {
-        cnt = group_counts(dst, dnew, qe, lane);
-      }
-      const uint32_t row = row_of(qe, vl, cnt, lane);
-      if (lane == 0) {
-        const uint32_t word = rows[q][x];
-        const uint32_t before = word & ~kRowFlags;  // keep the batch flags
-        if (before != row) {
-          rows[q][x] = row | (word & kRowFlags);
-          uint32_t diff = before ^ row;
-          while (diff) {
-            uint32_t u = __ffs(diff) - 1;
-            diff &= diff - 1;
-            atomicAdd((unsigned long long*)(colsize[q] + u),
-                      (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
-          }
-        }
-      }
-    }
+    finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, lane);
   }
   if (lane == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+}
+
+// The same merge for lists of >= kBigList entries, one CTA per list: each
+// sweep step moves 256 threads x kMoveUnroll elements (read completely, then
+// written, with a CTA barrier between), so an 18K-neighbour hub moves in a
+// handful of steps instead of ~75 warp steps; warp 0 then finishes the vertex.
+__global__ void __launch_bounds__(256) k_merge_big(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+    const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
+    const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
+    const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
+    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
+  __shared__ uint32_t s_start;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t nt = st->n_touched;
+  uint64_t bytes = 0;
+  for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    const uint64_t* seg = skeys + s;
+    const uint32_t segn = e - s;
+    const uint32_t x = uint32_t(seg[0] >> 32);
+    if (!(new_cap[t] & kBigFlag)) continue;  // uniform across the CTA
+    const uint32_t ncap = new_cap[t] & ~kBigFlag;
+    const uint32_t dold = g.deg[x];
+    const uint64_t ooff = g.off[x];
+    const uint32_t nins = ins_prefix[e] - ins_prefix[s];
+    const uint32_t dnew = dold + nins - (segn - nins);
+    const bool reloc = ncap != 0;
+    const uint64_t noff = new_off[t];
+    uint32_t* src = g.adj + ooff;
+    uint32_t* dst = g.adj + noff;
+    uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
+    uint32_t* edst = g.elab ? g.elab + noff : nullptr;
+    if (tid == 0) s_start = reloc ? 0u : lower_bound_u32(src, dold, uint32_t(seg[0]));
+    for (uint32_t k = tid; k < segn; k += blockDim.x) {
+      if (svals[s + k] >> 31) continue;
+      const uint32_t y = uint32_t(seg[k]);
+      const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+      ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - (k - ib));
+    }
+    __syncthreads();
+    const uint32_t start = s_start;
+    const bool ascending = reloc || nins == 0;
+    const uint32_t step = blockDim.x * kMoveUnroll;
+    const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
+    for (uint32_t si = 0; si < nsteps; ++si) {
+      const uint32_t base = start + (ascending ? si : nsteps - 1 - si) * step;
+      uint32_t a[kMoveUnroll], p[kMoveUnroll], el[kMoveUnroll];
+      bool mv[kMoveUnroll];
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        const uint32_t i = base + k * blockDim.x + tid;
+        mv[k] = false;
+        el[k] = kNone;
+        if (i < dold) {
+          a[k] = src[i];
+          if (esrc) el[k] = esrc[i];
+        }
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        const uint32_t i = base + k * blockDim.x + tid;
+        if (i < dold) {
+          bool dl;
+          merged_pos(seg, segn, ins_prefix, s, a[k], i, p[k], dl);
+          mv[k] = !dl && (reloc || p[k] != i);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+        if (mv[k]) {
+          dst[p[k]] = a[k];
+          if (edst) edst[p[k]] = el[k];
+        }
+      }
+      __syncthreads();
+    }
+    for (uint32_t k = tid; k < segn; k += blockDim.x) {
+      const uint32_t val = svals[s + k];
+      if (val >> 31) continue;
+      const uint32_t pp = ipos[s + k];
+      dst[pp] = uint32_t(seg[k]);
+      if (edst) edst[pp] = ups[val & 0x7fffffffu].elab;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      if (tid == 0) {
+        g.deg[x] = dnew;
+        if (reloc) {
+          g.off[x] = noff;
+          g.cap[x] = ncap;
+        }
+      }
+      __syncwarp();
+      finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, lane);
+      bytes += 4ull * (uint64_t(dold) + dnew);
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
 }
 
 // Full encode (QueryEncodingState::initialize, src/matcher.cpp:10-18):
@@ -679,6 +800,9 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st);
+  uint64_t bb = std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 4);
+  k_merge_big<<<unsigned(bb), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+                                          nq, rows, colsize, st);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);

@@ -188,3 +188,57 @@ def test_hub_bitmaps_do_not_change_counts(monkeypatch):
                 r = e.match_batch(b)
                 assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (suite, inst["name"], bi)
             e.close()
+
+
+def test_long_list_merge_matches_restatement():
+    """Lists of >= 4096 entries are merged by a whole CTA (k_merge_big), in
+    place (delete-only / insert-only) or relocated (mixed): a 5000-neighbour
+    hub receiving inserts and deletes over several batches, checked against
+    the CPU restatement batch by batch, plus its final neighbour list."""
+    import os
+    import sys
+    import numpy as np
+    import paper_2401_17018_b200 as bd
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    from oracle_py import Oracle
+    rng = np.random.default_rng(5)
+    V, L = 7000, 3
+    vl = rng.integers(0, L, V).astype(np.uint32)
+    hub = 0
+    pairs = {(0, v) for v in range(1, 5001)}
+    while len(pairs) < 20000:
+        a, b = (int(x) for x in rng.integers(1, V, 2))
+        if a != b:
+            pairs.add((min(a, b), max(a, b)))
+    present = set(pairs)
+    edges = sorted(pairs)
+    q = ([0, 1, 2, 1], [(0, 1), (1, 2), (2, 0), (0, 3)])
+    e = bd.Engine(vl, [a for a, _ in edges], [b for _, b in edges])
+    e.add_query(*q)
+    o = Oracle(vl, [a for a, _ in edges], [b for _, b in edges])
+    o.add_query(*q)
+    kinds = ["delete", "insert", "mixed", "mixed", "delete", "insert"]
+    for bi, kind in enumerate(kinds):
+        batch, used = [], set()
+        hub_nb = sorted(b for a, b in present if a == hub)
+        while len(batch) < 200:
+            if kind == "delete" or (kind == "mixed" and len(batch) % 2):
+                k = (hub, hub_nb[int(rng.integers(0, len(hub_nb)))])
+                op = 1
+            else:
+                v = int(rng.integers(1, V))
+                k = (hub, v)
+                op = 0
+                if k in present:
+                    continue
+            if k in used:
+                continue
+            used.add(k)
+            batch.append((op, k[0], k[1]))
+        for op, a, b in batch:
+            (present.discard if op else present.add)((a, b))
+        r = e.match_batch(batch)
+        exp = o.apply_batch(batch)
+        assert (r.positive[0], r.negative[0]) == (exp[0][0], exp[1][0]), (bi, kind)
+    assert e.neighbors(hub) == sorted(b for a, b in present if a == hub)
+    e.close()
