@@ -177,6 +177,7 @@ struct bdsm_engine {
     const size_t tmp = select_hubs_tmp_bytes(g.V);
     hub_tmp.ensure(std::max<size_t>(tmp, 1));
     launch_select_hubs(g.deg, g.V, 256, hub_ids.p, n_hubs.p, hub_tmp.p, hub_tmp.n, stream);
+    ++cub_calls;
     hubs_at = batches_done;
   }
   DBuf<uint32_t> heat;
@@ -993,7 +994,7 @@ struct bdsm_engine {
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, num_sms, stream);
       CK(cudaEventRecord(m1, stream));
-      launches += 4;  // prepare, post_sort, alloc, merge_refresh
+      launches += 5;  // prepare, post_sort, alloc, merge_refresh, merge_big
       cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);
