@@ -96,6 +96,7 @@ struct QueryState {
   std::vector<std::vector<uint32_t>> orders;
   std::vector<uint32_t> tails;  // EdgeProg::tail per query edge
   bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
+  uint32_t prev_items[2] = {0, 0};  // work items of the last batch per phase (kernel variant choice)
   DBuf<uint32_t> mbuf[2];        // materialised matches per phase (bdsm_engine_collect_matches)
   DBuf<unsigned long long> mcount;
   DBuf<LeafSig> leafsigs;        // distinct leaf signatures (prefill before each launch)
@@ -165,6 +166,7 @@ struct bdsm_engine {
   // arena at the pool's bump pointer and the engine stream gets a persisting
   // access-policy window over it.
   static constexpr uint64_t kHotPeriod = 8;
+  static constexpr uint32_t kThroughputItems = 20000;  // above: the 4-CTA matching-kernel variant
   // Hub list for the leaf-weight prefill, refreshed every kHubPeriod batches.
   static constexpr uint64_t kHubPeriod = 16;
   DBuf<uint32_t> hub_ids, n_hubs;
@@ -889,7 +891,8 @@ struct bdsm_engine {
           launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
           ++launches;
         }
-        launch_wbm(a, num_sms, stream);
+        // variant by the previous batch's work items of this (query, phase)
+        launch_wbm(a, num_sms, qs.prev_items[phase] > kThroughputItems, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
       }
@@ -1060,6 +1063,10 @@ struct bdsm_engine {
     const BatchState& b = *h_st;
     pool_top = b.pool_top;
     ++batches_done;
+    for (auto& q : queries) {  // BatchState keeps the last query's item counts per phase
+      q->prev_items[0] = b.n_items[0];
+      q->prev_items[1] = b.n_items[1];
+    }
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       bool dead = (b.timed_out >> qi) & 1u;
       if (dead) queries[qi]->solved = false;

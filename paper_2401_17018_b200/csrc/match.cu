@@ -730,15 +730,17 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
   __syncwarp();
 }
 
-#ifndef BDSM_WBM_MIN_BLOCKS
-#define BDSM_WBM_MIN_BLOCKS 2  // resident 256-thread CTAs per SM the register budget must allow (sweep: 2 beats 3, 4)
-#endif
+// Register budget per instantiation: kMinBlocks resident 256-thread CTAs per
+// SM.  2 (104 registers, no spills) wins when the launch is bound by its
+// longest subtree (C2: +6 % over 4); 4 (64 registers) wins when thousands of
+// items keep every warp busy (C5 cycle: +40 %).  The engine picks per launch
+// from the previous batch's work-item count (launch_wbm).
 // kEmit: bounded match materialisation (the reference's Match vectors,
 // src/matcher.cpp:169-217, for --dump-matches): the whole order is
 // enumerated (no counted tail) and every complete match is written in query
 // vertex order to a.match_out.
-template <bool kEmit>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BDSM_WBM_MIN_BLOCKS) k_wbm(PhaseArgs a) {
+template <bool kEmit, int kMinBlocks>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseArgs a) {
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
@@ -1193,15 +1195,21 @@ void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig,
   if (nsig) k_leaf_prefill<<<unsigned(num_sms * 8), 256, 0, s>>>(a, sigs, nsig, hubs, n_hubs);
 }
 
-void launch_wbm(const PhaseArgs& a, int num_sms, cudaStream_t s) {
+template <bool kEmit, int kMinBlocks>
+void launch_wbm_variant(const PhaseArgs& a, int num_sms, cudaStream_t s) {
   // persistent: as many resident CTAs as the SMs hold
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<false>, kWarpsPerBlock * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<kEmit, kMinBlocks>, kWarpsPerBlock * 32, 0);
     if (per_sm <= 0) per_sm = 1;
   }
-  if (a.match_out) k_wbm<true><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
-  else k_wbm<false><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
+  k_wbm<kEmit, kMinBlocks><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
+}
+
+void launch_wbm(const PhaseArgs& a, int num_sms, bool throughput, cudaStream_t s) {
+  if (a.match_out) launch_wbm_variant<true, 2>(a, num_sms, s);
+  else if (throughput) launch_wbm_variant<false, 4>(a, num_sms, s);
+  else launch_wbm_variant<false, 2>(a, num_sms, s);
 }
 
 }  // namespace bdsm_b200
