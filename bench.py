@@ -352,11 +352,13 @@ def ours(args, world, rank, local):
     }
     dom = max(kern, key=lambda k: kern[k][1])
     traffic = None  # DRAM bytes per launch of k_wbm from the committed ncu --set full capture
+    traffic_l2 = None
     try:
         with open(os.path.join(REPO, "profiles", "wbm_traffic.json")) as f:
             tr = json.load(f)
         if dom.startswith(tr["kernel"]):
             traffic = tr["dram_bytes_per_launch"]
+            traffic_l2 = {k: tr[k] for k in ("l2_read_bytes_per_launch", "l2_throughput_pct_of_peak", "note") if k in tr}
     except (OSError, KeyError, ValueError):
         pass
     ab, at = kern[dom]
@@ -364,6 +366,7 @@ def ours(args, world, rank, local):
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
             "traffic_source": "profiles/wbm_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
+            "physical": traffic_l2,
             "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
             "algorithmic_bytes": "4 B x backward-neighbour degrees per GenCandidates call made by k_wbm "
                                  "(SURVEY.md §8(d)), per step (negative + positive launch)",
