@@ -174,6 +174,74 @@ __host__ __device__ __forceinline__ uint32_t pair_hash(unsigned long long k) {
   return uint32_t(k);
 }
 
+// Persistent weight memo (matching kernel, invalidated by the merge): one
+// 64-bit word per (vertex x, query q, signature sig) = x << 32 | q << 27 |
+// sig << 19 | weight.  Weights >= kMemoInvalid are never stored; an entry
+// whose weight field is kMemoInvalid was invalidated (its list or a
+// neighbour's candidate row changed) and reads as a miss.  Linear probing,
+// at most kMemoProbes slots.
+constexpr int kMemoProbes = 8;
+constexpr unsigned long long kMemoEmpty = ~0ull;
+constexpr uint32_t kMemoWeightBits = 19;
+constexpr unsigned long long kMemoWeightMask = (1ull << kMemoWeightBits) - 1;
+constexpr unsigned long long kMemoInvalid = kMemoWeightMask;
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long memo_tag(uint32_t x, uint32_t q, uint32_t sig) {
+  return (uint64_t(x) << 32) | (uint64_t(q & 31) << 27) | (uint64_t(sig & 0xff) << kMemoWeightBits);
+}
+
+__device__ __forceinline__ bool memo_get(const unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
+                                         uint32_t sig, unsigned long long* w) {
+  const unsigned long long tag = memo_tag(x, q, sig);
+  uint32_t pos = pair_hash(tag) & mask;
+  for (int i = 0; i < kMemoProbes; ++i) {
+    const unsigned long long e = __ldcg(memo + pos);
+    if (e == kMemoEmpty) return false;
+    if ((e & ~kMemoWeightMask) == tag) {
+      if ((e & kMemoWeightMask) == kMemoInvalid) return false;
+      *w = e & kMemoWeightMask;
+      return true;
+    }
+    pos = (pos + 1) & mask;
+  }
+  return false;
+}
+
+// Returns true when a fresh slot was taken (fill accounting).
+__device__ __forceinline__ bool memo_put(unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
+                                         uint32_t sig, unsigned long long w) {
+  if (w >= kMemoInvalid) return false;
+  const unsigned long long tag = memo_tag(x, q, sig);
+  uint32_t pos = pair_hash(tag) & mask;
+  for (int i = 0; i < kMemoProbes; ++i) {
+    const unsigned long long prev = atomicCAS(memo + pos, kMemoEmpty, tag | w);
+    if (prev == kMemoEmpty) return true;
+    if ((prev & ~kMemoWeightMask) == tag) {
+      if ((prev & kMemoWeightMask) == kMemoInvalid) atomicCAS(memo + pos, prev, tag | w);
+      return false;
+    }
+    pos = (pos + 1) & mask;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
+                                                uint32_t sig) {
+  const unsigned long long tag = memo_tag(x, q, sig);
+  uint32_t pos = pair_hash(tag) & mask;
+  for (int i = 0; i < kMemoProbes; ++i) {
+    const unsigned long long e = __ldcg(memo + pos);
+    if (e == kMemoEmpty) return;
+    if ((e & ~kMemoWeightMask) == tag) {
+      atomicExch(memo + pos, tag | kMemoInvalid);
+      return;
+    }
+    pos = (pos + 1) & mask;
+  }
+}
+#endif
+
 // Device-side batch bookkeeping, copied back once per batch.
 struct BatchState {
   uint32_t err_count;            // validate_batch failures

@@ -97,6 +97,7 @@ struct QueryState {
   std::vector<uint32_t> tails;  // EdgeProg::tail per query edge
   bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
   uint32_t prev_items[2] = {0, 0};  // work items of the last batch per phase (kernel variant choice)
+  bool memo_cold = true;            // the memo holds none of this query's weights (full prefill next)
   DBuf<uint32_t> mbuf[2];        // materialised matches per phase (bdsm_engine_collect_matches)
   DBuf<unsigned long long> mcount;
   DBuf<LeafSig> leafsigs;        // distinct leaf signatures (prefill before each launch)
@@ -151,7 +152,15 @@ struct bdsm_engine {
   DBuf<DynItem> dyn;           // donated-subtree queue of the matching kernel
   DBuf<QueueState> qstate;
   DBuf<uint32_t> dyn_ready;
-  DBuf<unsigned long long> memo;  // leaf-weight memo of the matching kernel (2^21 words)
+  DBuf<unsigned long long> memo;  // weight memo of the matching kernel (2^21 words, persistent)
+  DBuf<unsigned long long> memo_fill;  // slots taken since the last reset
+  bool memo_persistent = true;     // false when a query has too many signatures to invalidate
+  void reset_memo() {
+    if (!memo.p) return;
+    CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+    CK(cudaMemsetAsync(memo_fill.p, 0, sizeof(unsigned long long), stream));
+    for (auto& q : queries) q->memo_cold = true;
+  }
   uint64_t collect_cap = 0;        // matches materialised per (query, phase); 0 = counts only
   // matching-kernel tuning knobs (BDSM_TUNE_BACKOFF / BDSM_TUNE_MERGE env overrides, for sweeps)
   uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
@@ -669,7 +678,11 @@ struct bdsm_engine {
     qs.orders.clear();
     qs.tails.clear();
     qs.has_leaf = false;
-    if (!memo.p) memo.ensure(size_t(1) << 21);
+    if (!memo.p) {
+      memo.ensure(size_t(1) << 21);
+      memo_fill.ensure(1);
+      reset_memo();
+    }
     std::vector<EdgeProg> progs;
     std::vector<AnchorEdge> anchors;
     std::vector<LeafSig> leafsigs;
@@ -703,6 +716,12 @@ struct bdsm_engine {
     }
     qs.has_leaf = !leafsigs.empty();
     qs.n_leafsig = uint32_t(leafsigs.size());
+    // the query's memo signatures, for the merge's invalidations; new orders
+    // mean new signatures, so the memo starts over
+    if (leafsigs.size() > sizeof(qs.denc.sig) / sizeof(qs.denc.sig[0])) memo_persistent = false;
+    qs.denc.nsig = uint32_t(std::min<size_t>(leafsigs.size(), sizeof(qs.denc.sig) / sizeof(qs.denc.sig[0])));
+    for (uint32_t k = 0; k < qs.denc.nsig; ++k) qs.denc.sig[k] = leafsigs[k].sig;
+    reset_memo();
     qs.leafsigs.ensure(std::max<size_t>(leafsigs.size(), 1));
     if (!leafsigs.empty())
       CK(cudaMemcpyAsync(qs.leafsigs.p, leafsigs.data(), sizeof(LeafSig) * leafsigs.size(), cudaMemcpyHostToDevice,
@@ -847,6 +866,8 @@ struct bdsm_engine {
     a.backoff_max = tune_backoff;
     a.memo = memo.p;
     a.memo_mask = uint32_t(memo.n - 1);
+    a.memo_fill = memo_fill.p;
+    a.heads = heads.p;
     a.match_out = nullptr;
     a.match_count = nullptr;
     a.match_cap = 0;
@@ -886,10 +907,22 @@ struct bdsm_engine {
       if (qs.q.n > 2) {
         CK(cudaEventRecord(next_kev(), stream));
         if (qs.has_leaf && !collect_cap) {
-          CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
-          refresh_hubs();
-          launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
-          ++launches;
+          // persistent memo: a full prefill over the hub list after a reset,
+          // then only the batch's touched vertices (the merge invalidated
+          // their weights) before the positive phase
+          if (!memo_persistent) {
+            CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+            qs.memo_cold = true;
+          }
+          if (qs.memo_cold) {
+            refresh_hubs();
+            launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
+            qs.memo_cold = false;
+            ++launches;
+          } else if (phase == 1) {
+            launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, stream);
+            ++launches;
+          }
         }
         // variant by the previous batch's work items of this (query, phase)
         launch_wbm(a, num_sms, qs.prev_items[phase] > kThroughputItems, stream);
@@ -995,7 +1028,8 @@ struct bdsm_engine {
       CK(cudaEventRecord(m0, stream));
       launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, stream);
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
-                           d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, num_sms, stream);
+                           d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
+                           uint32_t(memo.n ? memo.n - 1 : 0), num_sms, stream);
       CK(cudaEventRecord(m1, stream));
       launches += 5;  // prepare, post_sort, alloc, merge_refresh, merge_big
       cub_calls += 3; // sort, select, scan
@@ -1066,6 +1100,12 @@ struct bdsm_engine {
     for (auto& q : queries) {  // BatchState keeps the last query's item counts per phase
       q->prev_items[0] = b.n_items[0];
       q->prev_items[1] = b.n_items[1];
+    }
+    if (memo.p && batches_done % 32 == 0) {  // start the memo over before its probes run out
+      unsigned long long fill = 0;
+      CK(cudaMemcpyAsync(&fill, memo_fill.p, sizeof(fill), cudaMemcpyDeviceToHost, stream));
+      sync();
+      if (fill > memo.n * 2 / 5) reset_memo();
     }
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       bool dead = (b.timed_out >> qi) & 1u;
@@ -1427,6 +1467,7 @@ bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query) {
   return guarded([&]() -> bdsm_status {
     CK(cudaSetDevice(engine->device));
     engine->replan(query);
+    engine->upload_query_tables();
     return BDSM_OK;
   });
 }

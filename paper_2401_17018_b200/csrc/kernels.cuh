@@ -18,6 +18,8 @@ struct DevQueryEnc {
   uint32_t glabel[kMaxQ];
   uint32_t glo[kMaxQ], ghi[kMaxQ];  // internal-id range of each group's label (ids are label-ordered)
   uint32_t gcls[kMaxQ];          // label class index of each group's label (kNone: absent from the graph)
+  uint32_t nsig;                 // memo signatures of this query's weighted levels (invalidation)
+  uint32_t sig[kMaxQ * 2];
   uint8_t qcnt[kMaxQ][kMaxQ];    // [u][g]
 };
 
@@ -68,7 +70,8 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
                           DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
-                          uint64_t* const* colsize, BatchState* st, int num_sms, cudaStream_t s);
+                          uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+                          uint32_t memo_mask, int num_sms, cudaStream_t s);
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);
 void launch_label_index(DevGraphMut g, int num_sms, cudaStream_t s);
@@ -124,8 +127,10 @@ struct PhaseArgs {
   uint32_t epoch;
   uint32_t merge_ratio;          // merge-window intersection when |other| <= ratio x |driver|
   uint32_t backoff_max;          // idle warps' longest sleep between donation polls (ns)
-  unsigned long long* memo;      // leaf-weight memo (cleared before each launch)
+  unsigned long long* memo;      // weight memo (persistent; common.cuh)
   uint32_t memo_mask;
+  unsigned long long* memo_fill; // slots taken (the engine resets the memo when it fills up)
+  const uint32_t* heads;         // segment heads of the sorted batch keys (touched vertices)
   uint32_t* match_out;           // non-null: materialise matches ([match_cap][n], query vertex order)
   unsigned long long* match_count;
   unsigned long long match_cap;

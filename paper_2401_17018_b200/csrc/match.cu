@@ -529,37 +529,14 @@ __device__ __forceinline__ unsigned long long hidden_count(const PhaseArgs& a, c
   return n;
 }
 
-// Launch-wide memo of leaf weights: one 64-bit word per (x, sig) =
-// x << 32 | sig << 24 | weight (weights >= 2^24 are not memoised).  Linear
-// probing, bounded; entries are immutable once written, so a racing second
-// insert of the same key is harmless.
-constexpr int kMemoProbes = 8;
-constexpr unsigned long long kMemoEmpty = ~0ull;
-
+// Weight memo of this launch's query (common.cuh); persistent across launches
+// and batches, invalidated by the merge (store.cu finish_vertex).
 __device__ __forceinline__ bool memo_get(const PhaseArgs& a, uint32_t x, uint32_t sig, unsigned long long* w) {
-  const unsigned long long tag = (uint64_t(x) << 32) | (uint64_t(sig) << 24);
-  uint32_t pos = pair_hash(tag) & a.memo_mask;
-  for (int i = 0; i < kMemoProbes; ++i) {
-    const unsigned long long e = __ldcg(a.memo + pos);
-    if (e == kMemoEmpty) return false;
-    if ((e & ~0xffffffull) == tag) {
-      *w = e & 0xffffffull;
-      return true;
-    }
-    pos = (pos + 1) & a.memo_mask;
-  }
-  return false;
+  return ::bdsm_b200::memo_get(a.memo, a.memo_mask, x, a.query, sig, w);
 }
 
 __device__ __forceinline__ void memo_put(const PhaseArgs& a, uint32_t x, uint32_t sig, unsigned long long w) {
-  if (w >= (1ull << 24)) return;
-  const unsigned long long tag = (uint64_t(x) << 32) | (uint64_t(sig) << 24);
-  uint32_t pos = pair_hash(tag) & a.memo_mask;
-  for (int i = 0; i < kMemoProbes; ++i) {
-    const unsigned long long prev = atomicCAS(a.memo + pos, kMemoEmpty, tag | w);
-    if (prev == kMemoEmpty || (prev & ~0xffffffull) == tag) return;
-    pos = (pos + 1) & a.memo_mask;
-  }
+  if (::bdsm_b200::memo_put(a.memo, a.memo_mask, x, a.query, sig, w)) atomicAdd(a.memo_fill, 1ull);
 }
 
 // Per-lane leaf weight of level t for the lane's level-T candidate c (lanes
@@ -630,7 +607,9 @@ __global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
-  const uint32_t nh = *n_hubs;
+  // hubs == nullptr: the batch's touched vertices (their weights were
+  // invalidated by the merge) instead of the engine's hub list
+  const uint32_t nh = hubs ? *n_hubs : a.st->n_touched;
   const uint64_t nblk = (uint64_t(nh) + 31) / 32;
   for (uint64_t gi = warp; gi < nblk * nsig; gi += nwarps) {
     const LeafSig& ls = sigs[gi / nblk];
@@ -638,7 +617,7 @@ __global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig
     bool want = false;
     uint32_t x = 0;
     if (hi < nh) {
-      x = __ldg(hubs + hi);
+      x = hubs ? __ldg(hubs + hi) : uint32_t(__ldg(a.skeys + __ldg(a.heads + hi)) >> 32);
       want = x >= ls.plo && x < ls.phi && (__ldg(a.rows + x) & ls.pbit) && __ldg(a.g.deg + x) > kLeafLaneMax;
     }
     uint32_t todo = __ballot_sync(kFull, want);

@@ -317,7 +317,11 @@ __device__ __forceinline__ uint32_t row_of(const DevQueryEnc& qe, uint32_t vl, u
 __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const uint32_t* dst, uint32_t dnew,
                                               const uint64_t* seg, uint32_t segn, const uint32_t* segvals,
                                               const DevQueryEnc* __restrict__ qenc, uint32_t nq,
-                                              uint32_t* const* rows, uint64_t* const* colsize, uint32_t lane) {
+                                              uint32_t* const* rows, uint64_t* const* colsize,
+                                              unsigned long long* memo, uint32_t memo_mask, uint32_t lane) {
+  // the memoised weights of x (its list changed) are stale in every query
+  for (uint32_t q = 0; q < nq; ++q)
+    for (uint32_t k = lane; k < qenc[q].nsig; k += 32) memo_invalidate(memo, memo_mask, x, q, qenc[q].sig[k]);
     // membership bitmap of a hub: set inserted, clear deleted neighbours
     if (g.hub_slot) {
       const uint32_t hs = g.hub_slot[x];
@@ -353,22 +357,33 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
         cnt = group_counts(dst, dnew, qe, lane);
       }
       const uint32_t row = row_of(qe, vl, cnt, lane);
-      if (lane == 0) {
-        const uint32_t word = rows[q][x];
-        const uint32_t before = word & ~kRowFlags;  // keep the batch flags
-        if (before != row) {
+      uint32_t word = 0;
+      if (lane == 0) word = rows[q][x];
+      word = __shfl_sync(kFull, word, 0);
+      const uint32_t before = word & ~kRowFlags;  // keep the batch flags
+      if (before != row) {
+        const uint32_t diff = before ^ row;
+        if (lane == 0) {
           rows[q][x] = row | (word & kRowFlags);
-          uint32_t diff = before ^ row;
-          while (diff) {
-            uint32_t u = __ffs(diff) - 1;
-            diff &= diff - 1;
+          uint32_t d = diff;
+          while (d) {
+            uint32_t u = __ffs(d) - 1;
+            d &= d - 1;
             atomicAdd((unsigned long long*)(colsize[q] + u),
                       (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
           }
         }
+        // x's candidate bits changed: the memoised weights of its neighbours
+        // that count a query vertex among those bits are stale (a signature's
+        // low nibble is the counted child vertex)
+        for (uint32_t k = 0; k < qe.nsig; ++k) {
+          const uint32_t sg = qe.sig[k];
+          if (!((diff >> (sg & 15)) & 1u)) continue;
+          for (uint32_t i = lane; i < dnew; i += 32) memo_invalidate(memo, memo_mask, dst[i], q, sg);
+        }
       }
     }
-  }
+}
 
 constexpr uint32_t kMoveUnroll = 8;  // old elements per lane in flight per sweep step
 
@@ -387,7 +402,8 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
     const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
     const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
-    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st) {
+    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+    uint32_t memo_mask) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   if (st->pool_top > g.pool_size) {
     if (threadIdx.x == 0 && blockIdx.x == 0) st->overflow = 1;
@@ -483,7 +499,7 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
-    finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, lane);
+    finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, memo, memo_mask, lane);
   }
   if (lane == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
 }
@@ -497,7 +513,8 @@ __global__ void __launch_bounds__(256) k_merge_big(
     const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
     const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
-    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st) {
+    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+    uint32_t memo_mask) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   __shared__ uint32_t s_start;
@@ -583,7 +600,7 @@ __global__ void __launch_bounds__(256) k_merge_big(
         }
       }
       __syncwarp();
-      finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, lane);
+      finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, memo, memo_mask, lane);
       bytes += 4ull * (uint64_t(dold) + dnew);
     }
     __syncthreads();
@@ -792,17 +809,18 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
                           DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
-                          uint64_t* const* colsize, BatchState* st, int num_sms, cudaStream_t s) {
+                          uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+                          uint32_t memo_mask, int num_sms, cudaStream_t s) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
   uint64_t cap = uint64_t(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
-                                                  new_cap, ipos, qenc, nq, rows, colsize, st);
+                                                  new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask);
   uint64_t bb = std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 4);
   k_merge_big<<<unsigned(bb), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
-                                          nq, rows, colsize, st);
+                                          nq, rows, colsize, st, memo, memo_mask);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);

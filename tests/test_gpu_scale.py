@@ -11,7 +11,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("C1", 1, None, 3), ("C2", 20, 2000, 3), ("C5", 20, 2000, 3), ("C5cycle", 20, 2000, 3)]
+CASES = [("C1", 1, None, 4), ("C2", 20, 2000, 6), ("C5", 20, 2000, 3), ("C5cycle", 20, 2000, 3)]
 
 
 def _ops(b):
