@@ -230,7 +230,7 @@ __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, ui
   }
 }
 
-constexpr uint32_t kBigList = 4096;        // lists this long are merged by a whole CTA (k_merge_big)
+constexpr uint32_t kBigList = 1024;        // lists this long are merged by a whole CTA (k_merge_big)
 constexpr uint32_t kBigFlag = 0x80000000u;  // new_cap[t]: the list is merged by k_merge_big
 
 __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, uint32_t nt, uint32_t m) {
@@ -818,8 +818,9 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask);
-  uint64_t bb = std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 4);
-  k_merge_big<<<unsigned(bb), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+  // one CTA per touched vertex (<= m): CTAs of short lists exit at once, every
+  // long list gets its own CTA, so long lists merge concurrently
+  k_merge_big<<<unsigned(m ? m : 1), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
