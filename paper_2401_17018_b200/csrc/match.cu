@@ -742,6 +742,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
 #endif
   // per-warp counters (lane 0 updates them; kept out of the register budget)
   __shared__ unsigned long long s_stat[kWarpsPerBlock][5];  // count, visits, bytes, calls, kernel bytes
+  __shared__ unsigned long long s_lacc[kWarpsPerBlock][32][4];  // per-lane count/visits/bytes/calls (leaf levels)
   if (batch_aborted(a.st)) return;
   BatchState* st = a.st;
   const uint32_t lane = threadIdx.x & 31;
@@ -750,6 +751,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
   const DevGraph& g = a.g;
   unsigned long long* stat = s_stat[threadIdx.x >> 5];
   if ((threadIdx.x & 31) < 5) stat[threadIdx.x & 31] = 0;
+  for (int k = 0; k < 4; ++k) s_lacc[threadIdx.x >> 5][threadIdx.x & 31][k] = 0;
   __syncwarp();
   uint32_t dtick = 0;
   unsigned long long tt_pref = 0;  // prefetched donation-demand poll
@@ -1044,16 +1046,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
             prod *= cnt;
             vis += prod;
           }
-          prod = warp_sum_u64(prod);
-          vis = warp_sum_u64(vis);
-          bb = warp_sum_u64(bb);
-          cc = warp_sum_u64(cc);
-          if (lane == 0) {
-            stat[0] += prod;
-            stat[1] += vis;
-            stat[2] += bb;
-            stat[3] += cc;
-          }
+          // per-lane accumulators, summed across the warp once at the end
+          unsigned long long* la = s_lacc[w][lane];
+          la[0] += prod;
+          la[1] += vis;
+          la[2] += bb;
+          la[3] += cc;
 #ifdef BDSM_TRACE
           cy_leaf += clock64() - cy0;
 #endif
@@ -1153,6 +1151,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
     }
 #endif
     if (timed_out) break;
+  }
+  __syncwarp();
+  {  // fold the per-lane leaf-level accumulators into the warp's counters
+    unsigned long long v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = warp_sum_u64(s_lacc[w][lane][k]);
+    if (lane == 0)
+      for (int k = 0; k < 4; ++k) stat[k] += v[k];
   }
   __syncwarp();
   if (lane == 0) {
