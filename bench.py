@@ -370,6 +370,10 @@ def ours(args, world, rank, local):
             "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
             "algorithmic_bytes": "4 B x backward-neighbour degrees per GenCandidates call made by k_wbm "
                                  "(SURVEY.md §8(d)), per step (negative + positive launch)",
+            "note": "SURVEY.md §8(d) counts 4 B per element of every backward list of a GenCandidates call; the "
+                    "kernel reads only the label sub-range of the driver list and one bitmap word or a few search "
+                    "probes of the others, so achieved/peak can exceed 1 — the physically moved bytes are under "
+                    "'physical' (ncu: L2 and DRAM traffic of the profiled launch)",
             "reference_tree_bytes_per_step": bphase_ref,
             "reference_tree_equivalent_GBps": bphase_ref / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
             "other": {k: {"bytes": v[0], "ms": v[1], "GB/s": (v[0] / (v[1] / 1e3) / 1e9 if v[1] > 0 else 0)}

@@ -165,6 +165,8 @@ struct bdsm_engine {
   // matching-kernel tuning knobs (BDSM_TUNE_BACKOFF / BDSM_TUNE_MERGE env overrides, for sweeps)
   uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
+  uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 4: force a matching-kernel variant
+  uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
   static uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
     return v ? uint32_t(strtoul(v, nullptr, 10)) : dflt;
@@ -925,7 +927,8 @@ struct bdsm_engine {
           }
         }
         // variant by the previous batch's work items of this (query, phase)
-        launch_wbm(a, num_sms, qs.prev_items[phase] > kThroughputItems, stream);
+        launch_wbm(a, num_sms,
+                   tune_variant ? tune_variant == 4 : qs.prev_items[phase] > tune_throughput_items, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
       }

@@ -14,3 +14,4 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_w
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_merge_refresh -s 3 -c 1 -o gpurun_out/prof_merge \
     python bench.py --steps 1 --warmup 4 --no-cpu-baseline > gpurun_out/ncu_merge.log 2>&1
 ls -la gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
