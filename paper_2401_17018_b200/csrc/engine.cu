@@ -177,7 +177,7 @@ struct bdsm_engine {
   // arena at the pool's bump pointer and the engine stream gets a persisting
   // access-policy window over it.
   static constexpr uint64_t kHotPeriod = 8;
-  static constexpr uint32_t kThroughputItems = 20000;  // above: the 4-CTA matching-kernel variant
+  static constexpr uint32_t kThroughputItems = 2000;  // above: the 4-CTA matching-kernel variant (C2 ~300, C3 ~7K)
   // Hub list for the leaf-weight prefill, refreshed every kHubPeriod batches.
   static constexpr uint64_t kHubPeriod = 16;
   DBuf<uint32_t> hub_ids, n_hubs;
