@@ -83,6 +83,8 @@ struct EdgeProg {
   uint32_t leafmask;             // tail levels that are leaves of level `tail` (weight f(M[tail]))
   uint32_t singlemask;           // independent tail levels with one backward neighbour j (weight f(M[j]))
   uint32_t sig[kMaxQ];           // weighted level t: (order[parent] << 4) | order[t], the weight's memo tag
+  uint32_t natail;               // independent tail levels that depend on the anchor pair only
+  uint8_t atail_slot[kMaxQ];     // level t -> its slot in the per-task count cache (0xff: none)
   LevelProg lv[kMaxQ];
 };
 

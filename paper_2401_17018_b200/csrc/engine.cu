@@ -98,6 +98,7 @@ struct QueryState {
   bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
   uint32_t prev_items[2] = {0, 0};  // work items of the last batch per phase (kernel variant choice)
   bool memo_cold = true;            // the memo holds none of this query's weights (full prefill next)
+  uint32_t natail = 0;              // anchor-only tail levels per program (per-task count cache stride)
   DBuf<uint32_t> mbuf[2];        // materialised matches per phase (bdsm_engine_collect_matches)
   DBuf<unsigned long long> mcount;
   DBuf<LeafSig> leafsigs;        // distinct leaf signatures (prefill before each launch)
@@ -154,6 +155,8 @@ struct bdsm_engine {
   DBuf<uint32_t> dyn_ready;
   DBuf<unsigned long long> memo;  // weight memo of the matching kernel (2^21 words, persistent)
   DBuf<unsigned long long> memo_fill;  // slots taken since the last reset
+  DBuf<unsigned long long> task_tail;  // per-task counts of anchor-only tail levels (PhaseArgs::task_tail)
+  uint32_t qs_natail(int qi) const { return queries.at(size_t(qi))->natail; }
   bool memo_persistent = true;     // false when a query has too many signatures to invalidate
   void reset_memo() {
     if (!memo.p) return;
@@ -166,6 +169,7 @@ struct bdsm_engine {
   uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
   uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 4: force a matching-kernel variant
+  uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
   static uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
@@ -679,6 +683,7 @@ struct bdsm_engine {
     std::vector<uint64_t> cs = column_sizes(qi);
     qs.orders.clear();
     qs.tails.clear();
+    qs.natail = 0;
     qs.has_leaf = false;
     if (!memo.p) {
       memo.ensure(size_t(1) << 21);
@@ -698,6 +703,7 @@ struct bdsm_engine {
       qs.orders.push_back(matching_order(qs.q, e, cs));
       progs.push_back(build_program(qs.q, uint32_t(qi), qs.orders.back(), ranges, classes));
       qs.tails.push_back(progs.back().tail);
+      qs.natail = std::max(qs.natail, progs.back().natail);
       const EdgeProg& ep = progs.back();
       for (uint32_t t = 0; t < ep.n; ++t) {
         if (!(((ep.leafmask | ep.singlemask) >> t) & 1u)) continue;
@@ -870,6 +876,8 @@ struct bdsm_engine {
     a.memo_mask = uint32_t(memo.n - 1);
     a.memo_fill = memo_fill.p;
     a.heads = heads.p;
+    a.task_tail = nullptr;
+    a.natail_stride = qs_natail(qi);
     a.match_out = nullptr;
     a.match_count = nullptr;
     a.match_cap = 0;
@@ -925,6 +933,11 @@ struct bdsm_engine {
             launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, stream);
             ++launches;
           }
+        }
+        if (qs.natail && !tune_no_tasktail) {  // per-task counts of anchor-only tail levels, unset (~0) before the launch
+          task_tail.ensure_grow(tasks.n * qs.natail);
+          CK(cudaMemsetAsync(task_tail.p, 0xff, sizeof(unsigned long long) * tasks.n * qs.natail, stream));
+          a.task_tail = task_tail.p;
         }
         // variant by the previous batch's work items of this (query, phase)
         launch_wbm(a, num_sms,

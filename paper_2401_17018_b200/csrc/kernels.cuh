@@ -131,6 +131,8 @@ struct PhaseArgs {
   uint32_t memo_mask;
   unsigned long long* memo_fill; // slots taken (the engine resets the memo when it fills up)
   const uint32_t* heads;         // segment heads of the sorted batch keys (touched vertices)
+  unsigned long long* task_tail; // per-task counts of anchor-only tail levels ([task][natail_stride], ~0 = unset)
+  uint32_t natail_stride;
   uint32_t* match_out;           // non-null: materialise matches ([match_cap][n], query vertex order)
   unsigned long long* match_count;
   unsigned long long match_cap;

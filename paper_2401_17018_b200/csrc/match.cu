@@ -641,7 +641,7 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
                                             uint32_t (*s_ceil)[kMaxQ][kFloorB], uint32_t touched, uint32_t anchor,
                                             uint32_t flag, uint32_t lane, TailFactor* out,
                                             unsigned long long* stat, unsigned long long* tcnt, uint32_t* tdeg,
-                                            uint32_t& tvalid) {
+                                            uint32_t& tvalid, uint32_t task_id) {
   unsigned long long prod = 1, v = 1, b = 0, c = 0;
   for (uint32_t t = T + 1; t < P.n; ++t) {
     if ((P.leafmask >> t) & 1u) continue;  // leaves of T: weighted per level-T candidate
@@ -679,6 +679,20 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
         tdeg[t] = degsum;
       }
       tvalid |= 1u << t;
+    } else if (P.atail_slot[t] != 0xff && a.task_tail &&
+               __shfl_sync(kFull, lane == 0 ? uint32_t(__ldcg(a.task_tail + uint64_t(task_id) * a.natail_stride +
+                                                              P.atail_slot[t]) != kMemoEmpty)
+                                            : 0u, 0)) {
+      // anchor-only level already counted by another item of this task
+      const LevelProg& lp = P.lv[t];
+      cnt = __ldcg(a.task_tail + uint64_t(task_id) * a.natail_stride + P.atail_slot[t]);
+      degsum = 0;
+      for (uint32_t b = 0; b < lp.nback; ++b) degsum += __ldg(a.g.deg + M[lp.back[b]]);
+      if (lane == 0) {
+        tcnt[t] = cnt;
+        tdeg[t] = degsum;
+      }
+      tvalid |= 1u << t;
     } else {
       const LevelProg& lp = P.lv[t];
       const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t]);
@@ -705,6 +719,8 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
       if (lane == 0) {
         tcnt[t] = cnt;
         tdeg[t] = degsum;
+        if (P.atail_slot[t] != 0xff && a.task_tail)
+          a.task_tail[uint64_t(task_id) * a.natail_stride + P.atail_slot[t]] = cnt;
       }
       tvalid |= 1u << t;
     }
@@ -886,7 +902,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
         c_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
       }
       if (lstart == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
-                                 s_tcnt[w], s_tdeg[w], tvalid);
+                                 s_tcnt[w], s_tdeg[w], tvalid, task_id);
     }
     uint32_t l = lstart;
     while (true) {
@@ -1120,7 +1136,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
         c_drv = su.drv_b;
         c_tmask = 0;
         if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
-                                 s_tcnt[w], s_tdeg[w], tvalid);
+                                 s_tcnt[w], s_tdeg[w], tvalid, task_id);
 #ifdef BDSM_TRACE
         cy_setup += clock64() - cy0;
 #endif

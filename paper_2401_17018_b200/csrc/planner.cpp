@@ -149,6 +149,8 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
   p.tail = q.n >= 3 ? q.n - 1 : 0;
   while (p.tail > 2 && counted(p.tail - 1)) --p.tail;
   p.leafmask = 0;
+  p.natail = 0;
+  for (uint32_t t = 0; t < uint32_t(kMaxQ); ++t) p.atail_slot[t] = 0xff;
   for (uint32_t t = p.tail + 1; t < q.n; ++t) {
     const LevelProg& lp = p.lv[t];
     if ((lp.backmask >> p.tail) != 0) {  // leaf of T: weight memoised per M[T]
@@ -164,6 +166,10 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
     if (lp.nback == 1 && (lp.eqmask & ~lp.backmask) == 0) {
       p.singlemask |= 1u << t;
       p.sig[t] = (order[lp.back[0]] << 4) | order[t];
+    } else if ((dep & ~3u) == 0) {
+      // depends on the anchor pair only: one count per task, shared by all of
+      // the task's work items (EdgeProg::atail_slot)
+      p.atail_slot[t] = uint8_t(p.natail++);
     }
   }
   return p;

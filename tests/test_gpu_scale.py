@@ -65,3 +65,25 @@ def test_neighbours_follow_the_stream():
         assert len(eng.neighbors(int(v))) == o.degree(int(v))
     rows = eng.rows(0)
     assert all(int(rows[v]) == o.row(0, int(v)) for v in touched[:500])
+
+
+def test_task_tail_cache_does_not_change_counts(monkeypatch):
+    """C3 shape (8-vertex dense query) scaled down: tail levels that depend on
+    the anchor pair only are counted once per task and shared by the task's
+    work items; counts and reference-tree visits equal the per-item recount
+    (BDSM_TUNE_NO_TASKTAIL=1).  The restatement cannot enumerate C3's
+    matches in test time, so the per-item path (checked against it on the
+    golden suites) is the reference here."""
+    import paper_2401_17018_b200 as bd
+    import workload as W
+
+    wl = W.build("C3", 2, scale_down=8, device="cpu", batch=500)
+    out = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("BDSM_TUNE_NO_TASKTAIL", off)
+        eng = bd.Engine(wl.labels, wl.src, wl.dst)
+        eng.add_query(wl.qlabels, wl.qedges)
+        out.append([(r.positive[0], r.negative[0], r.stats["dfs_visits"]) for r in (eng.match_batch(b) for b in wl.batches)])
+        eng.close()
+    assert out[0] == out[1]
+    assert any(p or n for p, n, _ in out[0])
