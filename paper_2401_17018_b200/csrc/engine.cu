@@ -253,6 +253,7 @@ struct bdsm_engine {
   DBuf<BatchState> d_st;
   BatchState* h_st = nullptr;
   bdsm_update* h_ups = nullptr;
+  const bdsm_update* h_src = nullptr;  // this batch's host updates (caller's pinned buffer or h_ups)
   size_t h_ups_cap = 0;
   cudaEvent_t ev[6] = {};
   cudaEvent_t merge_ev[2] = {};
@@ -976,12 +977,8 @@ struct bdsm_engine {
       return BDSM_OK;
     }
     if (n >= (size_t(1) << 31)) throw std::invalid_argument("batch too large");
-    if (!device_input) {
-      bool labelled = false;
-      for (size_t i = 0; i < n && !labelled; ++i)
-        labelled = updates[i].op == 0 && updates[i].edge_label != BDSM_NO_LABEL;
-      if (labelled && !has_elab) enable_edge_labels();
-    }
+    // (a labelled insert into an unlabelled graph is detected by k_prepare:
+    // overflow 4 enables the label array and reruns the batch)
     ensure_batch(n);
     ensure_tasks(n);
     if (!h_st) CK(cudaMallocHost(&h_st, sizeof(BatchState)));
@@ -994,8 +991,18 @@ struct bdsm_engine {
     if (device_input) {
       src = reinterpret_cast<const bdsm_update_dev*>(updates);
     } else {
-      ensure_host_ups(n);
-      std::memcpy(h_ups, updates, n * sizeof(bdsm_update));
+      // pinned (page-locked) caller buffers are DMAed directly; pageable ones
+      // are staged through the engine's pinned buffer first
+      cudaPointerAttributes pa{};
+      const bool pinned = cudaPointerGetAttributes(&pa, updates) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();  // clear a pageable-pointer query error, if any
+      if (pinned) {
+        h_src = updates;
+      } else {
+        ensure_host_ups(n);
+        std::memcpy(h_ups, updates, n * sizeof(bdsm_update));
+        h_src = h_ups;
+      }
       src = ups_ext.p;
     }
     uint32_t compactions = 0;
@@ -1006,7 +1013,7 @@ struct bdsm_engine {
       cub_calls = 0;
       CK(cudaEventRecord(ev[0], stream));
       if (!device_input) {
-        CK(cudaMemcpyAsync(ups_ext.p, h_ups, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
         st.h2d_bytes = n * sizeof(bdsm_update);
       }
       *h_st = template_state();
@@ -1195,7 +1202,7 @@ struct bdsm_engine {
 
   void fetch_update(const bdsm_update_dev* src, bool device_input, uint32_t idx, bdsm_update* out) {
     if (!device_input) {
-      *out = h_ups[idx];
+      *out = h_src[idx];
       return;
     }
     CK(cudaMemcpyAsync(out, src + idx, sizeof(bdsm_update), cudaMemcpyDeviceToHost, stream));
