@@ -787,11 +787,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
 
   while (true) {
     // ---- acquire work ----------------------------------------------------
-    uint32_t kind = 0, ref = 0;  // 1 static item, 2 donated item, 3 exit
+    uint32_t kind = 0, ref = 0;  // 1 static item, 2 donated item, 3 exit, 4 deadline
     QueueState* Q = a.q;
     if (lane == 0) {
       // Static items first (counted as held before the index is taken, so a
       // waiter never sees holders == 0 while a static item is in flight).
+      // the deadline is checked before every work item, as the reference's
+      // workers check it before every task (Shared::stopping,
+      // src/scheduler.cpp:101-110): an expired budget stops the phase
+      if (a.deadline_ns && globaltimer() > a.deadline_ns) {
+        kind = 4;
+        static_done = true;
+      }
       if (!static_done) {
         atomicAdd(&Q->holders.v, 1u);
         uint32_t idx = atomicAdd(&Q->next_item.v, 1u);
@@ -803,7 +810,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
           atomicSub(&Q->holders.v, 1u);
         }
       }
-      if (!kind) {
+      if (!kind && !(a.deadline_ns && globaltimer() > a.deadline_ns)) {
         // Donated work: one ticket per idle period, then wait on that slot.
         if (ticket == kNone) ticket = atomicAdd(&Q->tt.tickets, 1u);
         uint32_t backoff = 128, spins = 0;
@@ -820,7 +827,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
               break;
             }
             if (a.deadline_ns && globaltimer() > a.deadline_ns) {
-              kind = 3;
+              kind = 4;
               break;
             }
           }
@@ -831,6 +838,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
     }
     kind = __shfl_sync(kFull, kind, 0);
     ref = __shfl_sync(kFull, ref, 0);
+    if (kind == 4) {  // deadline: counts of this query are dropped
+      timed_out = true;
+      break;
+    }
     if (kind == 3) break;
 #ifdef BDSM_TRACE
     const uint64_t t_item = globaltimer();

@@ -242,3 +242,39 @@ def test_long_list_merge_matches_restatement():
         assert (r.positive[0], r.negative[0]) == (exp[0][0], exp[1][0]), (bi, kind)
     assert e.neighbors(hub) == sorted(b for a, b in present if a == hub)
     e.close()
+
+
+@pytest.mark.parametrize("group_bits", [1, 3])
+def test_group_bits_only_filter(group_bits):
+    """--group-bits changes the NLF counter width (the candidate filter,
+    src/encoding.cpp:17-24), never the counts (PipelineConfig::group_bits)."""
+    import paper_2401_17018_b200 as bd
+    for inst in gu.load("streams")[:20] + gu.load("fig1"):
+        vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+        e = bd.Engine(vl, eu, ev, el, group_bits=group_bits)
+        e.add_query(ql, qe)
+        for b, exp in zip(batches, inst["expect"]):
+            r = e.match_batch(b)
+            assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (inst["name"], group_bits)
+        e.close()
+
+
+def test_deadline_marks_query_unsolved():
+    """MatchOptions::deadline / --timeout (src/scheduler.cpp:101-110,
+    src/bench.cpp:418-432): a query whose budget has run out is reported in
+    stats.timed_out, its counts are dropped, and it is skipped afterwards;
+    other queries are unaffected."""
+    import time
+    import paper_2401_17018_b200 as bd
+    inst = gu.load("skewed")[0]
+    vl, eu, ev, el, ql, qe, batches = gu.instance_arrays(inst)
+    e = bd.Engine(vl, eu, ev, el)
+    q0 = e.add_query(ql, qe)
+    q1 = e.add_query(ql, qe)
+    e.set_deadline(q0, 1e-9)
+    time.sleep(0.01)
+    r = e.match_batch(batches[0])
+    assert r.stats["timed_out"] & (1 << q0)
+    assert r.positive[q0] == 0 and r.negative[q0] == 0
+    assert (r.positive[q1], r.negative[q1]) == (inst["expect"][0]["pos"], inst["expect"][0]["neg"])
+    e.close()
