@@ -1284,19 +1284,19 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     o.group_bits = 2;
     o.slack = 0.25f;
     o.pool_reserve = 0.5f;
-    o.chunk = 32;
+    o.chunk = 8;
     o.shard_world = 1;
     if (opts) {
       o = *opts;
       if (o.group_bits == 0) o.group_bits = 2;
       if (o.slack <= 0) o.slack = 0.25f;
       if (o.pool_reserve <= 0) o.pool_reserve = 0.5f;
-      if (o.chunk == 0) o.chunk = 32;
+      if (o.chunk == 0) o.chunk = 8;
       if (o.shard_world == 0) o.shard_world = 1;
     }
     if (o.coalesce) throw std::invalid_argument("coalesced search is not supported: it is not exact in the reference (SURVEY.md F1)");
     if (o.shard_rank >= o.shard_world) throw std::invalid_argument("shard_rank must be < shard_world");
-    if (o.chunk % 32 != 0) throw std::invalid_argument("chunk must be a multiple of 32");
+    if (o.chunk % 8 != 0) throw std::invalid_argument("chunk must be a multiple of 8");
     e->opts = o;
     // zero-copy tier (north_star item 4): the adjacency pool in mapped pinned
     // host memory, for graphs whose lists exceed one GPU's HBM

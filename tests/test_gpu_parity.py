@@ -28,7 +28,7 @@ def test_counts_equal_reference(suite):
         e.close()
 
 
-@pytest.mark.parametrize("chunk", [32, 96, 256])
+@pytest.mark.parametrize("chunk", [8, 16, 32, 96, 256])
 def test_chunk_size_does_not_change_counts(chunk):
     for inst in gu.load("streams")[-4:] + gu.load("skewed"):
         e, batches = _engine(inst, chunk=chunk)
