@@ -610,13 +610,16 @@ __global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig
   // hubs == nullptr: the batch's touched vertices (their weights were
   // invalidated by the merge) instead of the engine's hub list
   const uint32_t nh = hubs ? *n_hubs : a.st->n_touched;
-  const uint64_t nblk = (uint64_t(nh) + 31) / 32;
+  // a warp takes kPrefillGroup candidates per signature, so the few long
+  // lists among them are spread over many warps instead of queueing in one
+  constexpr uint32_t kPrefillGroup = 4;
+  const uint64_t nblk = (uint64_t(nh) + kPrefillGroup - 1) / kPrefillGroup;
   for (uint64_t gi = warp; gi < nblk * nsig; gi += nwarps) {
     const LeafSig& ls = sigs[gi / nblk];
-    const uint64_t hi = (gi % nblk) * 32 + lane;
+    const uint64_t hi = (gi % nblk) * kPrefillGroup + lane;
     bool want = false;
     uint32_t x = 0;
-    if (hi < nh) {
+    if (lane < kPrefillGroup && hi < nh) {
       x = hubs ? __ldg(hubs + hi) : uint32_t(__ldg(a.skeys + __ldg(a.heads + hi)) >> 32);
       want = x >= ls.plo && x < ls.phi && (__ldg(a.rows + x) & ls.pbit) && __ldg(a.g.deg + x) > kLeafLaneMax;
     }
