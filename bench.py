@@ -158,7 +158,7 @@ def main():
     ap.add_argument("--cpu-batches", type=int, default=3)
     ap.add_argument("--cpu-time-cap", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--chunk", type=int, default=8)
+    ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--l2-hot-mb", type=int, default=0, help="K8 hot-list L2 persistence budget (0: off)")
     args = ap.parse_args()
 

@@ -72,7 +72,7 @@ typedef struct bdsm_options {
   uint32_t shard_world;  /* 0 or 1 = whole batch */
   float slack;           /* per-vertex adjacency slack fraction (default 0.25) */
   float pool_reserve;    /* extra adjacency pool for relocations, fraction of 2|E| (default 0.5) */
-  uint32_t chunk;        /* level-2 work-unit size, multiple of 8 (default 8) */
+  uint32_t chunk;        /* level-2 work-unit size, multiple of 8 (default 32) */
   uint32_t zero_copy;    /* 1: adjacency pool in mapped pinned host memory (graphs beyond HBM) */
   uint32_t l2_hot_mb;    /* > 0: hot-list L2 persistence budget in MB (K8 estimator + access-policy window) */
 } bdsm_options;

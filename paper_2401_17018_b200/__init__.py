@@ -213,7 +213,7 @@ class Engine:
 
     def __init__(self, vertex_labels, src, dst, edge_labels=None, *, group_bits: int = 2, device: int = 0,
                  shard_rank: int = 0, shard_world: int = 1, slack: float = 0.25, pool_reserve: float = 0.5,
-                 chunk: int = 8, zero_copy: bool = False, l2_hot_mb: int = 0):
+                 chunk: int = 32, zero_copy: bool = False, l2_hot_mb: int = 0):
         L = lib()
         self._vl = _u32(vertex_labels)
         s, d = _u32(src), _u32(dst)

@@ -255,7 +255,7 @@ struct BatchState {
   uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
   uint32_t n_items[2];
   uint32_t donations;            // statistics: donated subtrees
-  uint32_t pad;
+  uint32_t n_big;                // long lists this batch (k_alloc -> k_merge_big)
   uint64_t pool_top;             // adjacency pool bump pointer (elements)
   uint64_t relocations;
   uint64_t bytes_update;

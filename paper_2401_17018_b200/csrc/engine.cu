@@ -141,7 +141,7 @@ struct bdsm_engine {
   DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
   DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
   DBuf<uint64_t> keys, skeys;
-  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap;
+  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
   DBuf<unsigned long long> hkeys;  // visibility table of the batch
@@ -158,6 +158,7 @@ struct bdsm_engine {
   DBuf<unsigned long long> task_tail;  // per-task counts of anchor-only tail levels (PhaseArgs::task_tail)
   uint32_t qs_natail(int qi) const { return queries.at(size_t(qi))->natail; }
   bool memo_persistent = true;     // false when a query has too many signatures to invalidate
+  unsigned long long* h_memo_fill = nullptr;  // pinned copy of memo_fill, refreshed every batch
   void reset_memo() {
     if (!memo.p) return;
     CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
@@ -279,6 +280,7 @@ struct bdsm_engine {
       if (e) cudaEventDestroy(e);
     for (auto& e : kev) cudaEventDestroy(e);
     if (h_st) cudaFreeHost(h_st);
+    if (h_memo_fill) cudaFreeHost(h_memo_fill);
     if (h_ups) cudaFreeHost(h_ups);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -687,7 +689,10 @@ struct bdsm_engine {
     qs.natail = 0;
     qs.has_leaf = false;
     if (!memo.p) {
-      memo.ensure(size_t(1) << 21);
+      // one slot per vertex (power of two), 2^21..2^25 words: 32 MB at C2, 256 MB at C4
+      size_t words = size_t(1) << 21;
+      while (words < g.V && words < (size_t(1) << 25)) words <<= 1;
+      memo.ensure(words);
       memo_fill.ensure(1);
       reset_memo();
     }
@@ -803,6 +808,7 @@ struct bdsm_engine {
     ipos.ensure(m);
     new_off.ensure(m);
     new_cap.ensure(m);
+    big_list.ensure(m);
     upd_cnt.ensure(cap_n + 1);
     upd_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
@@ -1049,10 +1055,11 @@ struct bdsm_engine {
       CK(cudaEventRecord(ev[2], stream));
       cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
       CK(cudaEventRecord(m0, stream));
-      launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, stream);
+      launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
+                   stream);
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
-                           uint32_t(memo.n ? memo.n - 1 : 0), num_sms, stream);
+                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, num_sms, stream);
       CK(cudaEventRecord(m1, stream));
       launches += 5;  // prepare, post_sort, alloc, merge_refresh, merge_big
       cub_calls += 3; // sort, select, scan
@@ -1071,6 +1078,10 @@ struct bdsm_engine {
       ++launches;
       CK(cudaEventRecord(ev[4], stream));
       CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+      if (memo.p) {
+        if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
+        CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+      }
       CK(cudaEventRecord(ev[5], stream));
       sync();
       const BatchState& b = *h_st;
@@ -1113,7 +1124,7 @@ struct bdsm_engine {
       if (b.overflow == 3) {  // positive phase only (graph already merged)
         max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
         items.ensure(max_items);
-        rerun_positive(uint32_t(n), src);
+        rerun_positive(uint32_t(n));
       }
       break;
     }
@@ -1124,12 +1135,8 @@ struct bdsm_engine {
       q->prev_items[0] = b.n_items[0];
       q->prev_items[1] = b.n_items[1];
     }
-    if (memo.p && batches_done % 32 == 0) {  // start the memo over before its probes run out
-      unsigned long long fill = 0;
-      CK(cudaMemcpyAsync(&fill, memo_fill.p, sizeof(fill), cudaMemcpyDeviceToHost, stream));
-      sync();
-      if (fill > memo.n * 2 / 5) reset_memo();
-    }
+    // start the memo over before its probes run out (fill read with the batch's final copy)
+    if (memo.p && h_memo_fill && *h_memo_fill > memo.n * 2 / 5) reset_memo();
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       bool dead = (b.timed_out >> qi) & 1u;
       if (dead) queries[qi]->solved = false;
@@ -1172,19 +1179,9 @@ struct bdsm_engine {
     return BDSM_OK;
   }
 
-  // RAII helper: kernels launched through phase_args read `ups.p`; for
-  // device-resident input we temporarily point it at the caller's buffer.
-  struct PhaseArgsFix {
-    bdsm_engine* e;
-    bdsm_update_dev* saved;
-    PhaseArgsFix(bdsm_engine* en, const bdsm_update_dev* src) : e(en), saved(en->ups.p) {
-      e->ups.p = const_cast<bdsm_update_dev*>(src);
-    }
-    ~PhaseArgsFix() { e->ups.p = saved; }
-  };
-
-  void rerun_positive(uint32_t n, const bdsm_update_dev* src) {
-    (void)src;
+  // Positive-phase work items overflowed after the merge: grow and rerun that
+  // phase alone (the graph is already G').
+  void rerun_positive(uint32_t n) {
     h_st->overflow = 0;
     for (auto& c : h_st->counts[1]) c = 0;
     CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
@@ -1284,14 +1281,14 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     o.group_bits = 2;
     o.slack = 0.25f;
     o.pool_reserve = 0.5f;
-    o.chunk = 8;
+    o.chunk = 32;
     o.shard_world = 1;
     if (opts) {
       o = *opts;
       if (o.group_bits == 0) o.group_bits = 2;
       if (o.slack <= 0) o.slack = 0.25f;
       if (o.pool_reserve <= 0) o.pool_reserve = 0.5f;
-      if (o.chunk == 0) o.chunk = 8;
+      if (o.chunk == 0) o.chunk = 32;
       if (o.shard_world == 0) o.shard_world = 1;
     }
     if (o.coalesce) throw std::invalid_argument("coalesced search is not supported: it is not exact in the reference (SURVEY.md F1)");

@@ -241,7 +241,7 @@ __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, u
 // list no longer fits its slack.
 __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
                         const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
-                        BatchState* st, uint64_t* new_off, uint32_t* new_cap) {
+                        BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   uint32_t nt = st->n_touched;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
@@ -253,6 +253,7 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
     uint32_t dnew = dold + nins - ndel;
     // top bit: the pre-batch list is long (merged by k_merge_big, not k_merge_refresh)
     const uint32_t big = dold >= kBigList ? kBigFlag : 0u;
+    if (big) big_list[atomicAdd(&st->n_big, 1u)] = t;
     if (dnew > g.cap[x] || (nins && ndel)) {  // overflow, or a mixed segment (see merge)
       uint32_t c = slack_cap(dnew, slack);
       new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
@@ -514,19 +515,20 @@ __global__ void __launch_bounds__(256) k_merge_big(
     const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
     uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
-    uint32_t memo_mask) {
+    uint32_t memo_mask, const uint32_t* __restrict__ big_list) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   __shared__ uint32_t s_start;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const uint32_t nt = st->n_touched;
   uint64_t bytes = 0;
-  for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+  const uint32_t nbig = st->n_big;
+  for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    const uint32_t t = big_list[bi];  // long lists, listed by k_alloc
     const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
     const uint64_t* seg = skeys + s;
     const uint32_t segn = e - s;
     const uint32_t x = uint32_t(seg[0] >> 32);
-    if (!(new_cap[t] & kBigFlag)) continue;  // uniform across the CTA
     const uint32_t ncap = new_cap[t] & ~kBigFlag;
     const uint32_t dold = g.deg[x];
     const uint64_t ooff = g.off[x];
@@ -802,15 +804,16 @@ void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
-                  uint32_t* new_cap, cudaStream_t s) {
-  k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap);
+                  uint32_t* new_cap, uint32_t* big_list, cudaStream_t s) {
+  k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap,
+                                             big_list);
 }
 void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
                           DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
-                          uint32_t memo_mask, int num_sms, cudaStream_t s) {
+                          uint32_t memo_mask, const uint32_t* big_list, int num_sms, cudaStream_t s) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
@@ -818,10 +821,9 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask);
-  // one CTA per touched vertex (<= m): CTAs of short lists exit at once, every
-  // long list gets its own CTA, so long lists merge concurrently
-  k_merge_big<<<unsigned(m ? m : 1), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
-                                          nq, rows, colsize, st, memo, memo_mask);
+  // a CTA per long list (k_alloc's list), so long lists merge concurrently
+  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+                                          nq, rows, colsize, st, memo, memo_mask, big_list);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);
