@@ -386,7 +386,11 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
     }
 }
 
-constexpr uint32_t kMoveUnroll = 8;  // old elements per lane in flight per sweep step
+constexpr uint32_t kMoveUnroll = 8;      // old elements per thread in flight per sweep step (k_merge_big)
+constexpr uint32_t kWarpMoveUnroll = 4;  // the same for k_merge_refresh (lists < kBigList)
+// k_merge_refresh is latency-bound over many short lists: a tighter register
+// budget (6 CTAs = 48 warps per SM) keeps more lists in flight
+constexpr int kMergeWarpBlocks = 6;
 
 // K3 (part 2) + K4: one warp per touched vertex.  Insert slots are computed
 // first against the intact old list.  In place (merged list fits the slack)
@@ -398,7 +402,7 @@ constexpr uint32_t kMoveUnroll = 8;  // old elements per lane in flight per swee
 // with kMoveUnroll loads in flight per lane.  Relocated lists are merged out
 // of place.  The same warp then recomputes the candidate row of every query
 // from label-range counts of the new list (K4).
-__global__ void __launch_bounds__(256) k_merge_refresh(
+__global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
     const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
     const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
@@ -448,14 +452,14 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
     // 2. move old elements
     start = __shfl_sync(kFull, start, 31);
     const bool ascending = reloc || nins == 0;  // left-movers ascend, right-movers descend
-    const uint32_t step = 32 * kMoveUnroll;
+    const uint32_t step = 32 * kWarpMoveUnroll;
     const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
     for (uint32_t si = 0; si < nsteps; ++si) {
       const uint32_t base = start + (ascending ? si : nsteps - 1 - si) * step;
-      uint32_t a[kMoveUnroll], p[kMoveUnroll], el[kMoveUnroll];
-      bool mv[kMoveUnroll];
+      uint32_t a[kWarpMoveUnroll], p[kWarpMoveUnroll], el[kWarpMoveUnroll];
+      bool mv[kWarpMoveUnroll];
 #pragma unroll
-      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+      for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
         const uint32_t i = base + k * 32 + lane;
         mv[k] = false;
         el[k] = kNone;
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
         }
       }
 #pragma unroll
-      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+      for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
         const uint32_t i = base + k * 32 + lane;
         if (i < dold) {
           bool dl;
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(256) k_merge_refresh(
       }
       __syncwarp();
 #pragma unroll
-      for (uint32_t k = 0; k < kMoveUnroll; ++k) {
+      for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
         if (mv[k]) {
           dst[p[k]] = a[k];
           if (edst) edst[p[k]] = el[k];

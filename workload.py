@@ -216,6 +216,8 @@ class _KeysGraph:
     def __init__(self, keys: torch.Tensor, V: int):
         self.keys = keys
         self.V = V
+        # the reverse direction (max << 32 | min), sorted, so a neighbour query is two range lookups
+        self.rkeys = torch.sort(((keys & 0xFFFFFFFF) << 32) | (keys >> 32)).values
         deg = torch.zeros(V, dtype=torch.int64, device=keys.device)
         step = 1 << 28
         for s in range(0, keys.numel(), step):
@@ -228,11 +230,11 @@ class _KeysGraph:
         return int(self.deg[u])
 
     def neighbors(self, u: int) -> np.ndarray:
-        lo = int(torch.searchsorted(self.keys, torch.tensor([u << 32], device=self.keys.device)))
-        hi = int(torch.searchsorted(self.keys, torch.tensor([(u + 1) << 32], device=self.keys.device)))
-        up = self.keys[lo:hi] & 0xFFFFFFFF
-        down = self.keys[(self.keys & 0xFFFFFFFF) == u] >> 32
-        return torch.sort(torch.cat([up, down])).values.cpu().numpy()
+        bounds = torch.tensor([u << 32, (u + 1) << 32], device=self.keys.device)
+        lo, hi = torch.searchsorted(self.keys, bounds).tolist()
+        rlo, rhi = torch.searchsorted(self.rkeys, bounds).tolist()
+        both = torch.cat([self.keys[lo:hi], self.rkeys[rlo:rhi]]) & 0xFFFFFFFF
+        return torch.sort(both).values.cpu().numpy()
 
 
 @dataclass
@@ -443,7 +445,10 @@ def build(name: str, nbatches: int, seed_graph: int = 1, seed_query: int = 7, se
         ql = [0] * n
         qe = [(i, (i + 1) % n) for i in range(n)]
     else:
-        ql, qe = extract_query(csr, labels, cfg["qsize"], cfg["qcat"], seed_query)
+        # sparse queries need an induced cycle, rare in a walk over a 1.8B-edge
+        # graph with mean degree 55: more attempts for the billion-edge shape
+        ql, qe = extract_query(csr, labels, cfg["qsize"], cfg["qcat"], seed_query,
+                               attempts=40000 if keys is not None else 4000)
     bsz = batch or cfg["batch"]
     batches = make_stream(a, b, labels_t, V, nbatches, bsz, cfg["mode"], seed_stream, keys=keys)
     deg = csr.deg
@@ -451,6 +456,7 @@ def build(name: str, nbatches: int, seed_graph: int = 1, seed_query: int = 7, se
             "isolated": int((deg == 0).sum()), "batch": bsz, "mode": cfg["mode"], "generator": cfg["kind"],
             "seeds": {"graph": seed_graph, "query": seed_query, "stream": seed_stream}, "desc": cfg["desc"]}
     if keys is not None:  # u32 endpoint arrays, converted in slices
+        del csr.rkeys
         src = np.empty(keys.numel(), np.uint32)
         dst = np.empty(keys.numel(), np.uint32)
         step = 1 << 28
