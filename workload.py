@@ -149,18 +149,19 @@ def chung_lu_keys(V: int, E: int, seed: int, device, dmax: int, gamma: float, ch
     8 B per edge instead of the per-step copies of the small-shape path)."""
     g = _gen(seed, device)
     alpha = 1.0 / (gamma - 1.0)
-    i = torch.arange(V, dtype=torch.float64, device=device)
-    w = (i + 1.0) ** (-alpha)
-    del i
+    # weights and CDF on the host: numpy's sequential float64 sums are
+    # reproducible, a device scan's association order is not (and the CDF
+    # decides every endpoint draw)
+    w = (np.arange(V, dtype=np.float64) + 1.0) ** (-alpha)
     target = 2.0 * E / V
     for _ in range(50):
         w = w * (target * V / float(w.sum()))
-        w = torch.clamp(w, max=float(dmax))
+        w = np.minimum(w, float(dmax))
         if abs(float(w.sum()) / V - target) < 1e-3 * target:
             break
-    cdf = torch.cumsum(w, 0)
-    cdf = cdf / cdf[-1]
-    del w
+    cdf_h = np.cumsum(w)
+    cdf = torch.from_numpy(cdf_h / cdf_h[-1]).to(device)
+    del w, cdf_h
     perm = torch.randperm(V, generator=g, device=device)
 
     def keys_of(u, v):
