@@ -141,7 +141,7 @@ struct bdsm_engine {
   DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
   DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
   DBuf<uint64_t> keys, skeys;
-  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list;
+  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
   DBuf<unsigned long long> hkeys;  // visibility table of the batch
@@ -172,6 +172,9 @@ struct bdsm_engine {
   uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 4: force a matching-kernel variant
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
+  // batches of at least this many directed keys merge short lists one per
+  // thread (k_merge_small); below it the warp kernel's latency is lower
+  uint32_t tune_small_min = env_u32("BDSM_TUNE_SMALLMIN", kSmallMergeMinKeys);
   static uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
     return v ? uint32_t(strtoul(v, nullptr, 10)) : dflt;
@@ -182,6 +185,7 @@ struct bdsm_engine {
   // arena at the pool's bump pointer and the engine stream gets a persisting
   // access-policy window over it.
   static constexpr uint64_t kHotPeriod = 8;
+  static constexpr uint32_t kSmallMergeMinKeys = 65536;  // C2 batches: 20K keys, C4: 2M
   static constexpr uint32_t kThroughputItems = 2000;  // above: the 4-CTA matching-kernel variant (C2 ~300, C3 ~7K)
   // Hub list for the leaf-weight prefill, refreshed every kHubPeriod batches.
   static constexpr uint64_t kHubPeriod = 16;
@@ -809,6 +813,7 @@ struct bdsm_engine {
     new_off.ensure(m);
     new_cap.ensure(m);
     big_list.ensure(m);
+    small_list.ensure(m);
     upd_cnt.ensure(cap_n + 1);
     upd_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
@@ -1055,13 +1060,14 @@ struct bdsm_engine {
       CK(cudaEventRecord(ev[2], stream));
       cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
       CK(cudaEventRecord(m0, stream));
+      const bool small_ok = m >= tune_small_min;
       launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
-                   stream);
+                   small_list.p, small_ok, stream);
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
-                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, num_sms, stream);
+                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, small_ok, num_sms, stream);
       CK(cudaEventRecord(m1, stream));
-      launches += 5;  // prepare, post_sort, alloc, merge_refresh, merge_big
+      launches += small_ok ? 6 : 5;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big
       cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);

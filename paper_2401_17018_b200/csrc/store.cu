@@ -40,7 +40,7 @@ __device__ __forceinline__ uint32_t slack_cap(uint32_t d, float slack) {
   if (extra < 4) extra = 4;
   uint64_t c = uint64_t(d) + extra;
   c = (c + 3) & ~uint64_t(3);  // 16-byte aligned lists (128-bit loads)
-  if (c > 0xfffffff0ull) c = 0xfffffff0ull;
+  if (c > 0x3ffffff0ull) c = 0x3ffffff0ull;  // new_cap[] keeps two flag bits above the capacity
   return uint32_t(c);
 }
 
@@ -232,6 +232,9 @@ __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, ui
 
 constexpr uint32_t kBigList = 1024;        // lists this long are merged by a whole CTA (k_merge_big)
 constexpr uint32_t kBigFlag = 0x80000000u;  // new_cap[t]: the list is merged by k_merge_big
+constexpr uint32_t kSmallList = 64;         // lists up to this long (before and after) are merged by one thread
+constexpr uint32_t kSmallFlag = 0x40000000u;  // new_cap[t]: the list is merged by k_merge_small
+constexpr uint32_t kCapMask = 0x3fffffffu;
 
 __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, uint32_t nt, uint32_t m) {
   return t + 1 < nt ? heads[t + 1] : m;
@@ -241,7 +244,8 @@ __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, u
 // list no longer fits its slack.
 __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
                         const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
-                        BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list) {
+                        BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
+                        uint32_t* small_list, bool small_ok) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   uint32_t nt = st->n_touched;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
@@ -254,14 +258,16 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
     // top bit: the pre-batch list is long (merged by k_merge_big, not k_merge_refresh)
     const uint32_t big = dold >= kBigList ? kBigFlag : 0u;
     if (big) big_list[atomicAdd(&st->n_big, 1u)] = t;
+    const uint32_t small = small_ok && dold <= kSmallList && dnew <= kSmallList ? kSmallFlag : 0u;
+    if (small) small_list[atomicAdd(&st->n_small, 1u)] = t;
     if (dnew > g.cap[x] || (nins && ndel)) {  // overflow, or a mixed segment (see merge)
       uint32_t c = slack_cap(dnew, slack);
       new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
-      new_cap[t] = c | big;
+      new_cap[t] = c | big | small;
       atomicAdd((unsigned long long*)&st->relocations, 1ull);
     } else {
       new_off[t] = g.off[x];
-      new_cap[t] = big;  // in place
+      new_cap[t] = big | small;  // in place
     }
   }
 }
@@ -428,8 +434,8 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const uint64_t ooff = g.off[x];
     const uint32_t nins = ins_prefix[e] - ins_prefix[s];
     const uint32_t dnew = dold + nins - (segn - nins);
-    if (new_cap[t] & kBigFlag) continue;  // k_merge_big: a whole CTA per long list
-    const uint32_t ncap = new_cap[t];
+    if (new_cap[t] & (kBigFlag | kSmallFlag)) continue;  // k_merge_big / k_merge_small
+    const uint32_t ncap = new_cap[t] & kCapMask;
     const bool reloc = ncap != 0;
     const uint64_t noff = new_off[t];
     uint32_t* src = g.adj + ooff;
@@ -509,6 +515,196 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
   if (lane == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
 }
 
+// Short lists (<= kSmallList entries before and after the batch; most touched
+// lists at the C2-C4 shapes) are merged by ONE thread each, so a warp merges
+// 32 of them at once instead of one.  The batch keys' positions in the old
+// list are found first (independent searches); the old entries then move as
+// runs between them, 8 loads in flight (ascending in place for delete-only
+// lists, descending in place for insert-only ones, out of place for relocated
+// ones), so no load waits on the previous comparison.  The finish is
+// finish_vertex's done serially: the label index comes from the old one
+// shifted by the batch keys below each class (no pass over the new list),
+// then candidate rows, memo invalidations and hub bitmap bits.
+__global__ void __launch_bounds__(256) k_merge_small(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+    const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
+    const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
+    const uint32_t* __restrict__ new_cap, const DevQueryEnc* __restrict__ qenc, uint32_t nq,
+    uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+    uint32_t memo_mask, const uint32_t* __restrict__ small_list) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
+  const uint32_t nt = st->n_touched, nsmall = st->n_small;
+  uint64_t bytes = 0;
+  for (uint32_t si = blockIdx.x * blockDim.x + threadIdx.x; si < nsmall; si += gridDim.x * blockDim.x) {
+    const uint32_t t = small_list[si];
+    const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    const uint64_t* seg = skeys + s;
+    const uint32_t segn = e - s;
+    const uint32_t x = uint32_t(seg[0] >> 32);
+    const uint32_t dold = g.deg[x];
+    const uint64_t ooff = g.off[x];
+    const uint32_t nins = ins_prefix[e] - ins_prefix[s];
+    const uint32_t dnew = dold + nins - (segn - nins);
+    const uint32_t ncap = new_cap[t] & kCapMask;
+    const bool reloc = ncap != 0;
+    const uint64_t noff = new_off[t];
+    const uint32_t* src = g.adj + ooff;
+    uint32_t* dst = g.adj + noff;
+    const uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
+    uint32_t* edst = g.elab ? g.elab + noff : nullptr;
+    auto ins_label = [&](uint32_t k) { return ups[svals[s + k] & 0x7fffffffu].elab; };
+    // where each batch key falls in the old list (independent searches)
+    uint32_t ypos[2 * kSmallList];
+    for (uint32_t k = 0; k < segn; ++k) ypos[k] = lower_bound_u32(src, dold, uint32_t(seg[k]));
+    // copy a run of old entries, 8 loads in flight; in place the runs move
+    // left in ascending order or right in descending order, and a block is
+    // read completely before it is written, so overlapping runs are safe
+    auto copy_up = [&](uint32_t from, uint32_t to, uint32_t len) {
+      for (uint32_t b = 0; b < len; b += 8) {
+        uint32_t v[8], l[8];
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          v[k] = b + k < len ? src[from + b + k] : 0u;
+          l[k] = esrc && b + k < len ? esrc[from + b + k] : 0u;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+          if (b + k < len) {
+            dst[to + b + k] = v[k];
+            if (edst) edst[to + b + k] = l[k];
+          }
+      }
+    };
+    auto copy_down = [&](uint32_t from, uint32_t to, uint32_t len) {
+      for (uint32_t b = len; b > 0;) {
+        const uint32_t nb = b < 8 ? b : 8;
+        b -= nb;
+        uint32_t v[8], l[8];
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+          v[k] = k < nb ? src[from + b + k] : 0u;
+          l[k] = esrc && k < nb ? esrc[from + b + k] : 0u;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+          if (k < nb) {
+            dst[to + b + k] = v[k];
+            if (edst) edst[to + b + k] = l[k];
+          }
+      }
+    };
+    if (reloc || nins == 0) {  // ascending: out of place, or delete-only in place (moves left)
+      // in place the entries below the first batch key do not move
+      uint32_t r = reloc || segn == 0 ? 0 : ypos[0], w = r;
+      for (uint32_t k = 0; k < segn; ++k) {
+        const uint32_t pk = ypos[k];
+        copy_up(r, w, pk - r);
+        w += pk - r;
+        r = pk;
+        if (svals[s + k] >> 31) {
+          ++r;  // the deleted entry
+        } else {
+          dst[w] = uint32_t(seg[k]);
+          if (edst) edst[w] = ins_label(k);
+          ++w;
+        }
+      }
+      if (r < dold) copy_up(r, w, dold - r);
+    } else {  // insert-only in place: descending (moves right)
+      uint32_t r = dold, w = dnew;
+      for (int k = int(segn) - 1; k >= 0; --k) {
+        const uint32_t pk = ypos[k];
+        copy_down(pk, w - (r - pk), r - pk);
+        w -= r - pk;
+        r = pk;
+        --w;
+        dst[w] = uint32_t(seg[k]);
+        if (edst) edst[w] = ins_label(uint32_t(k));
+      }
+    }
+    g.deg[x] = dnew;
+    if (reloc) {
+      g.off[x] = noff;
+      g.cap[x] = ncap;
+    }
+    bytes += 4ull * (uint64_t(dold) + dnew);
+    // --- finish (finish_vertex, serially) ---
+    if (g.hub_slot) {
+      const uint32_t hs = g.hub_slot[x];
+      if (hs != kNone) {
+        uint32_t* bm = g.bitmaps + uint64_t(hs) * g.bm_words;
+        for (uint32_t k = 0; k < segn; ++k) {
+          const uint32_t y = uint32_t(seg[k]);
+          if (svals[s + k] >> 31) atomicAnd(bm + (y >> 5), ~(1u << (y & 31)));
+          else atomicOr(bm + (y >> 5), 1u << (y & 31));
+        }
+      }
+    }
+    for (uint32_t q = 0; q < nq; ++q)
+      for (uint32_t k = 0; k < qenc[q].nsig; ++k) memo_invalidate(memo, memo_mask, x, q, qenc[q].sig[k]);
+    // label index of the new list from the old one: class k's first
+    // position moves by the inserts minus the deletes below class_lo[k]
+    uint32_t lpos[kMaxLabelIndex + 1];
+    const bool indexed = g.loff != nullptr;
+    if (indexed) {
+      uint32_t* row = g.loff + uint64_t(x) * (g.nlab + 1);
+      for (uint32_t k = 0; k < g.nlab; ++k) lpos[k] = row[k];
+      int acc = 0;
+      uint32_t ci = 0;
+      for (uint32_t k = 0; k < segn; ++k) {
+        const uint32_t y = uint32_t(seg[k]);
+        while (ci < g.nlab && g.class_lo[ci] <= y) lpos[ci++] += acc;
+        acc += (svals[s + k] >> 31) ? -1 : 1;
+      }
+      while (ci < g.nlab) lpos[ci++] += acc;
+      lpos[g.nlab] = dnew;
+      for (uint32_t k = 0; k <= g.nlab; ++k) row[k] = lpos[k];
+    }
+    const uint32_t vl = g.vlabel[x];
+    for (uint32_t q = 0; q < nq; ++q) {
+      const DevQueryEnc& qe = qenc[q];
+      uint32_t cnt[kMaxQ];
+      for (uint32_t gi = 0; gi < qe.G; ++gi) {
+        uint32_t c = 0;
+        if (indexed) {
+          const uint32_t cls = qe.gcls[gi];
+          c = cls == kNone ? 0u : lpos[cls + 1] - lpos[cls];
+        } else {
+          for (uint32_t i = 0; i < dnew; ++i) c += dst[i] >= qe.glo[gi] && dst[i] < qe.ghi[gi];
+        }
+        cnt[gi] = c > qe.cap ? qe.cap : c;
+      }
+      uint32_t row = 0;
+      for (uint32_t u = 0; u < qe.n; ++u) {
+        if (vl != qe.qlabel[u]) continue;
+        bool ok = true;
+        for (uint32_t gi = 0; gi < qe.G && ok; ++gi) ok = cnt[gi] >= qe.qcnt[u][gi];
+        if (ok) row |= 1u << u;
+      }
+      const uint32_t word = rows[q][x];
+      const uint32_t before = word & ~kRowFlags;
+      if (before != row) {
+        rows[q][x] = row | (word & kRowFlags);
+        const uint32_t diff = before ^ row;
+        uint32_t d = diff;
+        while (d) {
+          const uint32_t u = __ffs(d) - 1;
+          d &= d - 1;
+          atomicAdd((unsigned long long*)(colsize[q] + u), (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
+        }
+        for (uint32_t k = 0; k < qe.nsig; ++k) {  // neighbours' weights that count a flipped bit
+          const uint32_t sg = qe.sig[k];
+          if ((diff >> (sg & 15)) & 1u)
+            for (uint32_t i = 0; i < dnew; ++i) memo_invalidate(memo, memo_mask, dst[i], q, sg);
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+}
+
 // The same merge for lists of >= kBigList entries, one CTA per list: each
 // sweep step moves 256 threads x kMoveUnroll elements (read completely, then
 // written, with a CTA barrier between), so an 18K-neighbour hub moves in a
@@ -533,7 +729,7 @@ __global__ void __launch_bounds__(256) k_merge_big(
     const uint64_t* seg = skeys + s;
     const uint32_t segn = e - s;
     const uint32_t x = uint32_t(seg[0] >> 32);
-    const uint32_t ncap = new_cap[t] & ~kBigFlag;
+    const uint32_t ncap = new_cap[t] & kCapMask;
     const uint32_t dold = g.deg[x];
     const uint64_t ooff = g.off[x];
     const uint32_t nins = ins_prefix[e] - ins_prefix[s];
@@ -808,16 +1004,18 @@ void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
-                  uint32_t* new_cap, uint32_t* big_list, cudaStream_t s) {
+                  uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, bool small_ok,
+                  cudaStream_t s) {
   k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap,
-                                             big_list);
+                                             big_list, small_list, small_ok);
 }
 void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
                           DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
-                          uint32_t memo_mask, const uint32_t* big_list, int num_sms, cudaStream_t s) {
+                          uint32_t memo_mask, const uint32_t* big_list, const uint32_t* small_list,
+                          bool small_ok, int num_sms, cudaStream_t s) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
@@ -825,6 +1023,10 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask);
+  if (small_ok)
+    k_merge_small<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) + 255) / 256, uint64_t(num_sms) * 8)), 256,
+                    0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
+                            st, memo, memo_mask, small_list);
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
   k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, big_list);

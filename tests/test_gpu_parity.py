@@ -190,6 +190,53 @@ def test_hub_bitmaps_do_not_change_counts(monkeypatch):
             e.close()
 
 
+@pytest.mark.parametrize("bitmap_mindeg", [None, "4"])
+def test_thread_merge_matches_reference(monkeypatch, bitmap_mindeg):
+    """Short lists (<= 64 entries) of large batches are merged one per thread
+    (k_merge_small); the threshold is lowered so every golden batch takes
+    that path: counts equal the reference's, and on a mixed random stream
+    every neighbour list equals the expected one after each batch.  With
+    bitmaps forced onto small vertices the thread path's bitmap maintenance
+    is exercised too."""
+    import os
+    import sys
+    import paper_2401_17018_b200 as bd
+    monkeypatch.setenv("BDSM_TUNE_SMALLMIN", "1")
+    if bitmap_mindeg:
+        monkeypatch.setenv("BDSM_BITMAP_MINDEG", bitmap_mindeg)
+    for suite in gu.SUITES:
+        for inst in gu.load(suite):
+            e, batches = _engine(inst)
+            for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
+                r = e.match_batch(b)
+                assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (suite, inst["name"], bi)
+            e.close()
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    from oracle_py import Oracle
+    vl, edges, batches = _random_stream(23)
+    eu = [a for a, _ in edges]
+    ev = [b for _, b in edges]
+    q = ([0, 1, 2, 0], [(0, 1), (1, 2), (2, 0), (2, 3)])
+    e = bd.Engine(vl, eu, ev)
+    e.add_query(*q)
+    o = Oracle(vl, eu, ev)
+    o.add_query(*q)
+    adj = {v: set() for v in range(len(vl))}
+    for a, b in edges:
+        adj[a].add(b)
+        adj[b].add(a)
+    for bi, b in enumerate(batches):
+        r = e.match_batch(b)
+        exp = o.apply_batch(b)
+        assert (r.positive[0], r.negative[0]) == (exp[0][0], exp[1][0]), bi
+        for op, x, y in b:
+            (adj[x].discard if op else adj[x].add)(y)
+            (adj[y].discard if op else adj[y].add)(x)
+        for v in range(0, len(vl), 7):
+            assert e.neighbors(v) == sorted(adj[v]), (bi, v)
+    e.close()
+
+
 def test_long_list_merge_matches_restatement():
     """Lists of >= 4096 entries are merged by a whole CTA (k_merge_big), in
     place (delete-only / insert-only) or relocated (mixed): a 5000-neighbour
