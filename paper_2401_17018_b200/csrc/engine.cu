@@ -1067,7 +1067,7 @@ struct bdsm_engine {
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
                            uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, small_ok, num_sms, stream);
       CK(cudaEventRecord(m1, stream));
-      launches += small_ok ? 6 : 5;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big
+      launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
       cub_calls += 3; // sort, select, scan
       CK(cudaEventRecord(ev[3], stream));
       run_phase(uint32_t(n), 1);

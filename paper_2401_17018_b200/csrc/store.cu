@@ -341,12 +341,22 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
         }
       }
     }
-    // label index of the new list (lane k: class k's first position)
+    // label index of the new list (lane k: class k's first position): the
+    // old position moved by the batch's inserts minus deletes below
+    // class_lo[k] (the segment is sorted), no search of the new list
     uint32_t lpos = 0;
     if (g.loff)
       for (uint32_t k = lane; k <= g.nlab; k += 32) {
-        lpos = k < g.nlab ? lower_bound_u32(dst, dnew, g.class_lo[k]) : dnew;
-        g.loff[uint64_t(x) * (g.nlab + 1) + k] = lpos;
+        uint32_t* cell = g.loff + uint64_t(x) * (g.nlab + 1) + k;
+        if (k < g.nlab) {
+          const uint32_t lo = g.class_lo[k];
+          int acc = 0;
+          for (uint32_t j = 0; j < segn && uint32_t(seg[j]) < lo; ++j) acc += (segvals[j] >> 31) ? -1 : 1;
+          lpos = uint32_t(int(*cell) + acc);
+        } else {
+          lpos = dnew;
+        }
+        *cell = lpos;
       }
     const bool from_index = g.loff && g.nlab < 32;  // the whole index sits in lanes 0..nlab
     // 4. refresh: saturated per-group neighbour counts -> candidate rows (K4)
@@ -740,12 +750,18 @@ __global__ void __launch_bounds__(256) k_merge_big(
     uint32_t* dst = g.adj + noff;
     uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
     uint32_t* edst = g.elab ? g.elab + noff : nullptr;
-    if (tid == 0) s_start = reloc ? 0u : lower_bound_u32(src, dold, uint32_t(seg[0]));
+    // insert slots against the intact old list; key 0's search also gives
+    // the first position that can move (entries below it never move)
+    if (tid == 0 && reloc) s_start = 0u;
     for (uint32_t k = tid; k < segn; k += blockDim.x) {
-      if (svals[s + k] >> 31) continue;
-      const uint32_t y = uint32_t(seg[k]);
-      const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
-      ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - (k - ib));
+      const bool del = svals[s + k] >> 31;
+      if (del && (k || reloc)) continue;
+      const uint32_t lb = lower_bound_u32(src, dold, uint32_t(seg[k]));
+      if (k == 0 && !reloc) s_start = lb;
+      if (!del) {
+        const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+        ipos[s + k] = ib + (lb - (k - ib));
+      }
     }
     __syncthreads();
     const uint32_t start = s_start;
@@ -775,7 +791,10 @@ __global__ void __launch_bounds__(256) k_merge_big(
           mv[k] = !dl && (reloc || p[k] != i);
         }
       }
-      __syncthreads();
+      // in place, a step's writes may land on entries the step read; they
+      // never reach the next step's reads (left moves ascend, right moves
+      // descend), so one barrier per step suffices, none when relocating
+      if (!reloc) __syncthreads();
 #pragma unroll
       for (uint32_t k = 0; k < kMoveUnroll; ++k) {
         if (mv[k]) {
@@ -783,7 +802,6 @@ __global__ void __launch_bounds__(256) k_merge_big(
           if (edst) edst[p[k]] = el[k];
         }
       }
-      __syncthreads();
     }
     for (uint32_t k = tid; k < segn; k += blockDim.x) {
       const uint32_t val = svals[s + k];
@@ -792,22 +810,40 @@ __global__ void __launch_bounds__(256) k_merge_big(
       dst[pp] = uint32_t(seg[k]);
       if (edst) edst[pp] = ups[val & 0x7fffffffu].elab;
     }
-    __syncthreads();
-    if (tid < 32) {
-      if (tid == 0) {
-        g.deg[x] = dnew;
-        if (reloc) {
-          g.off[x] = noff;
-          g.cap[x] = ncap;
-        }
+    if (tid == 0) {
+      g.deg[x] = dnew;
+      if (reloc) {
+        g.off[x] = noff;
+        g.cap[x] = ncap;
       }
-      __syncwarp();
-      finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, memo, memo_mask, lane);
       bytes += 4ull * (uint64_t(dold) + dnew);
     }
-    __syncthreads();
+    __syncthreads();  // s_start and this list's reads are done before the next list
   }
   if (tid == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+}
+
+// finish_vertex of the long lists k_merge_big moved, a warp per list, so a
+// CTA's other warps do not wait on one warp's serial finish between lists.
+__global__ void __launch_bounds__(256) k_finish_big(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+    const uint32_t* __restrict__ svals, uint32_t m, DevGraphMut g, const DevQueryEnc* __restrict__ qenc,
+    uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+    uint32_t memo_mask, const uint32_t* __restrict__ big_list) {
+  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (st->pool_top > g.pool_size) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nt = st->n_touched, nbig = st->n_big;
+  for (uint32_t bi = warp; bi < nbig; bi += nwarps) {
+    const uint32_t t = big_list[bi];
+    const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    const uint64_t* seg = skeys + s;
+    const uint32_t x = uint32_t(seg[0] >> 32);
+    finish_vertex(g, x, g.adj + g.off[x], g.deg[x], seg, e - s, svals + s, qenc, nq, rows, colsize, memo,
+                  memo_mask, lane);
+  }
 }
 
 // Full encode (QueryEncodingState::initialize, src/matcher.cpp:10-18):
@@ -1030,6 +1066,8 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
   k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, big_list);
+  k_finish_big<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * 32 + 255) / 256, uint64_t(num_sms) * 8)), 256, 0,
+                 s>>>(heads, skeys, svals, m, g, qenc, nq, rows, colsize, st, memo, memo_mask, big_list);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);
