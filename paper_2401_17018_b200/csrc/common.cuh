@@ -257,7 +257,7 @@ struct BatchState {
   uint32_t donations;            // statistics: donated subtrees
   uint32_t n_big;                // long lists this batch (k_alloc -> k_merge_big)
   uint32_t n_small;              // short lists this batch (k_alloc -> k_merge_small)
-  uint32_t pad2;
+  uint32_t n_mid;                // the other lists (k_alloc -> k_merge_refresh)
   uint64_t pool_top;             // adjacency pool bump pointer (elements)
   uint64_t relocations;
   uint64_t bytes_update;

@@ -141,7 +141,7 @@ struct bdsm_engine {
   DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
   DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
   DBuf<uint64_t> keys, skeys;
-  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list;
+  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list, mid_list;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
   DBuf<unsigned long long> hkeys;  // visibility table of the batch
@@ -814,6 +814,7 @@ struct bdsm_engine {
     new_cap.ensure(m);
     big_list.ensure(m);
     small_list.ensure(m);
+    mid_list.ensure(m);
     upd_cnt.ensure(cap_n + 1);
     upd_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
@@ -1062,10 +1063,11 @@ struct bdsm_engine {
       CK(cudaEventRecord(m0, stream));
       const bool small_ok = m >= tune_small_min;
       launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
-                   small_list.p, small_ok, stream);
+                   small_list.p, mid_list.p, small_ok, stream);
       launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
                            d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
-                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, small_ok, num_sms, stream);
+                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, mid_list.p, small_ok,
+                           num_sms, stream);
       CK(cudaEventRecord(m1, stream));
       launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
       cub_calls += 3; // sort, select, scan

@@ -245,29 +245,63 @@ __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, u
 __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
                         const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
                         BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
-                        uint32_t* small_list, bool small_ok) {
+                        uint32_t* small_list, uint32_t* mid_list, bool small_ok) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
-  uint32_t nt = st->n_touched;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-    uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
-    uint32_t x = uint32_t(skeys[s] >> 32);
-    uint32_t nins = ins_prefix[e] - ins_prefix[s];
-    uint32_t ndel = (e - s) - nins;
-    const uint32_t dold = g.deg[x];
-    uint32_t dnew = dold + nins - ndel;
-    // top bit: the pre-batch list is long (merged by k_merge_big, not k_merge_refresh)
-    const uint32_t big = dold >= kBigList ? kBigFlag : 0u;
-    if (big) big_list[atomicAdd(&st->n_big, 1u)] = t;
-    const uint32_t small = small_ok && dold <= kSmallList && dnew <= kSmallList ? kSmallFlag : 0u;
-    if (small) small_list[atomicAdd(&st->n_small, 1u)] = t;
-    if (dnew > g.cap[x] || (nins && ndel)) {  // overflow, or a mixed segment (see merge)
-      uint32_t c = slack_cap(dnew, slack);
-      new_off[t] = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)c);
-      new_cap[t] = c | big | small;
-      atomicAdd((unsigned long long*)&st->relocations, 1ull);
-    } else {
-      new_off[t] = g.off[x];
-      new_cap[t] = big | small;  // in place
+  const uint32_t nt = st->n_touched;
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  // warp-uniform loop: list appends and pool allocations are aggregated per
+  // warp (one atomic each instead of one per list)
+  for (uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x - lane; t0 < nt; t0 += gridDim.x * blockDim.x) {
+    const uint32_t t = t0 + lane;
+    uint32_t big = 0, small = 0, c = 0, x = 0;
+    if (t < nt) {
+      const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+      x = uint32_t(skeys[s] >> 32);
+      const uint32_t nins = ins_prefix[e] - ins_prefix[s];
+      const uint32_t ndel = (e - s) - nins;
+      const uint32_t dold = g.deg[x];
+      const uint32_t dnew = dold + nins - ndel;
+      // the pre-batch list is long (k_merge_big) / both lists are short (k_merge_small)
+      big = dold >= kBigList ? kBigFlag : 0u;
+      small = small_ok && dold <= kSmallList && dnew <= kSmallList ? kSmallFlag : 0u;
+      if (dnew > g.cap[x] || (nins && ndel)) c = slack_cap(dnew, slack);  // overflow, or a mixed segment
+    }
+    const uint32_t bb = __ballot_sync(kFull, big != 0), bs = __ballot_sync(kFull, small != 0);
+    const uint32_t bm = __ballot_sync(kFull, t < nt && !big && !small);
+    uint32_t base = 0;
+    if (bm) {
+      if (lane == 0) base = atomicAdd(&st->n_mid, __popc(bm));
+      base = __shfl_sync(kFull, base, 0);
+      if ((bm >> lane) & 1u) mid_list[base + __popc(bm & lt)] = t;
+    }
+    if (bb) {
+      if (lane == 0) base = atomicAdd(&st->n_big, __popc(bb));
+      base = __shfl_sync(kFull, base, 0);
+      if (big) big_list[base + __popc(bb & lt)] = t;
+    }
+    if (bs) {
+      if (lane == 0) base = atomicAdd(&st->n_small, __popc(bs));
+      base = __shfl_sync(kFull, base, 0);
+      if (small) small_list[base + __popc(bs & lt)] = t;
+    }
+    const uint32_t br = __ballot_sync(kFull, c != 0);
+    uint64_t at = 0;
+    if (br) {  // relocations: one pool allocation for the warp, carved by an inclusive scan
+      uint64_t inc = c;
+#pragma unroll
+      for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint64_t v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) {
+        at = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)inc);
+        atomicAdd((unsigned long long*)&st->relocations, (unsigned long long)__popc(br));
+      }
+      at = __shfl_sync(kFull, at, 31) + inc - c;
+    }
+    if (t < nt) {
+      new_off[t] = c ? at : g.off[x];
+      new_cap[t] = c | big | small;  // capacity 0: in place
     }
   }
 }
@@ -424,7 +458,7 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
     uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
-    uint32_t memo_mask) {
+    uint32_t memo_mask, const uint32_t* __restrict__ mid_list) {
   if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
   if (st->pool_top > g.pool_size) {
     if (threadIdx.x == 0 && blockIdx.x == 0) st->overflow = 1;
@@ -433,9 +467,10 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t nt = st->n_touched;
+  const uint32_t nt = st->n_touched, nmid = st->n_mid;
   uint64_t bytes = 0;
-  for (uint32_t t = warp; t < nt; t += nwarps) {
+  for (uint32_t mi = warp; mi < nmid; mi += nwarps) {
+    const uint32_t t = mid_list[mi];  // neither long nor short (k_alloc's list)
     const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
     const uint64_t* seg = skeys + s;
     const uint32_t segn = e - s;
@@ -444,7 +479,6 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const uint64_t ooff = g.off[x];
     const uint32_t nins = ins_prefix[e] - ins_prefix[s];
     const uint32_t dnew = dold + nins - (segn - nins);
-    if (new_cap[t] & (kBigFlag | kSmallFlag)) continue;  // k_merge_big / k_merge_small
     const uint32_t ncap = new_cap[t] & kCapMask;
     const bool reloc = ncap != 0;
     const uint64_t noff = new_off[t];
@@ -1040,10 +1074,10 @@ void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
-                  uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, bool small_ok,
-                  cudaStream_t s) {
+                  uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, uint32_t* mid_list,
+                  bool small_ok, cudaStream_t s) {
   k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap,
-                                             big_list, small_list, small_ok);
+                                             big_list, small_list, mid_list, small_ok);
 }
 void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
@@ -1051,14 +1085,15 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
                           uint32_t memo_mask, const uint32_t* big_list, const uint32_t* small_list,
-                          bool small_ok, int num_sms, cudaStream_t s) {
+                          const uint32_t* mid_list, bool small_ok, int num_sms, cudaStream_t s) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
   uint64_t cap = uint64_t(num_sms) * 8;
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
-                                                  new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask);
+                                                  new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask,
+                                                  mid_list);
   if (small_ok)
     k_merge_small<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) + 255) / 256, uint64_t(num_sms) * 8)), 256,
                     0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
