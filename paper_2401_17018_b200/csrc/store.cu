@@ -35,6 +35,25 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__
   return lo;
 }
 
+// lower_bound by a whole warp: 32 probes per round narrow the range 32-fold,
+// so a list of up to 1024 entries takes two dependent loads instead of ten.
+// Every lane returns the same position.
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t x,
+                                                     uint32_t lane) {
+  uint32_t lo = 0, len = n;
+  while (len > 32) {
+    const uint32_t b = (len + 31) >> 5;  // bucket size; lane i probes bucket i's last entry
+    const uint32_t idx = lo + (lane + 1) * b - 1;
+    const bool less = idx < lo + len && __ldg(a + idx) < x;
+    const uint32_t c = __popc(__ballot_sync(kFull, less));  // buckets entirely below x
+    const uint32_t end = lo + len;
+    lo += c * b;
+    len = lo >= end ? 0u : (end - lo < b ? end - lo : b);
+  }
+  const bool less = lane < len && __ldg(a + lo + lane) < x;
+  return lo + __popc(__ballot_sync(kFull, less));
+}
+
 __device__ __forceinline__ uint32_t slack_cap(uint32_t d, float slack) {
   uint64_t extra = uint64_t(float(d) * slack);
   if (extra < 4) extra = 4;
@@ -438,6 +457,7 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
 
 constexpr uint32_t kMoveUnroll = 8;      // old elements per thread in flight per sweep step (k_merge_big)
 constexpr uint32_t kWarpMoveUnroll = 4;  // the same for k_merge_refresh (lists < kBigList)
+constexpr uint32_t kWarpSearchKeys = 4;  // k_merge_refresh: segments up to this many keys use warp searches
 // k_merge_refresh is latency-bound over many short lists: a tighter register
 // budget (6 CTAs = 48 warps per SM) keeps more lists in flight
 constexpr int kMergeWarpBlocks = 6;
@@ -487,20 +507,35 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
     uint32_t* edst = g.elab ? g.elab + noff : nullptr;
 
-    // 1. insert slots against the intact old list; lane 31 meanwhile finds the
-    // first position that can move (elements below the first batch key never move)
+    // 1. insert slots against the intact old list, and the first position
+    // that can move (entries below the first batch key never move).  A few
+    // keys are searched one after another by the whole warp (two dependent
+    // loads each below 1024 entries); many keys by one lane each.
     uint32_t start = 0;
-    if (lane == 31 && !reloc && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
-    for (uint32_t k = lane; k < segn; k += 32) {
-      if (svals[s + k] >> 31) continue;  // delete
-      uint32_t y = uint32_t(seg[k]);
-      uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
-      uint32_t db = k - ib;
-      ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
+    if (segn <= kWarpSearchKeys) {
+      for (uint32_t k = 0; k < segn; ++k) {
+        const bool del = svals[s + k] >> 31;
+        if (del && (k || reloc)) continue;
+        const uint32_t lb = warp_lower_bound(src, dold, uint32_t(seg[k]), lane);
+        if (k == 0 && !reloc) start = lb;
+        if (!del && lane == 0) {
+          const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+          ipos[s + k] = ib + (lb - (k - ib));
+        }
+      }
+    } else {
+      if (lane == 31 && !reloc && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
+      for (uint32_t k = lane; k < segn; k += 32) {
+        if (svals[s + k] >> 31) continue;  // delete
+        uint32_t y = uint32_t(seg[k]);
+        uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+        uint32_t db = k - ib;
+        ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
+      }
+      start = __shfl_sync(kFull, start, 31);
     }
     __syncwarp();
     // 2. move old elements
-    start = __shfl_sync(kFull, start, 31);
     const bool ascending = reloc || nins == 0;  // left-movers ascend, right-movers descend
     const uint32_t step = 32 * kWarpMoveUnroll;
     const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
