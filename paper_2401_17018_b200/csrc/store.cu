@@ -821,11 +821,17 @@ __global__ void __launch_bounds__(256) k_merge_big(
     uint32_t* edst = g.elab ? g.elab + noff : nullptr;
     // insert slots against the intact old list; key 0's search also gives
     // the first position that can move (entries below it never move)
+    // (a few keys: one warp-cooperative search per key, spread over the
+    // warps, three dependent loads each below 32K entries instead of 15)
     if (tid == 0 && reloc) s_start = 0u;
-    for (uint32_t k = tid; k < segn; k += blockDim.x) {
+    const uint32_t nw = blockDim.x >> 5;
+    const bool warp_search = segn <= 2 * nw;
+    for (uint32_t k = warp_search ? tid >> 5 : tid; k < segn; k += warp_search ? nw : blockDim.x) {
       const bool del = svals[s + k] >> 31;
       if (del && (k || reloc)) continue;
-      const uint32_t lb = lower_bound_u32(src, dold, uint32_t(seg[k]));
+      const uint32_t lb = warp_search ? warp_lower_bound(src, dold, uint32_t(seg[k]), lane)
+                                      : lower_bound_u32(src, dold, uint32_t(seg[k]));
+      if (warp_search && lane) continue;
       if (k == 0 && !reloc) s_start = lb;
       if (!del) {
         const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
