@@ -175,6 +175,7 @@ struct bdsm_engine {
   // batches of at least this many directed keys merge short lists one per
   // thread (k_merge_small); below it the warp kernel's latency is lower
   uint32_t tune_small_min = env_u32("BDSM_TUNE_SMALLMIN", kSmallMergeMinKeys);
+  uint32_t tune_self_scan = env_u32("BDSM_TUNE_SELFSCAN", kSelfScanUpdates);
   static uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
     return v ? uint32_t(strtoul(v, nullptr, 10)) : dflt;
@@ -185,6 +186,7 @@ struct bdsm_engine {
   // arena at the pool's bump pointer and the engine stream gets a persisting
   // access-policy window over it.
   static constexpr uint64_t kHotPeriod = 8;
+  static constexpr uint32_t kSelfScanUpdates = 16384;  // batches up to this size: anchor offsets scanned in k_anchor_emit
   static constexpr uint32_t kSmallMergeMinKeys = 65536;  // C2 batches: 20K keys, C4: 2M
   static constexpr uint32_t kThroughputItems = 2000;  // above: the 4-CTA matching-kernel variant (C2 ~300, C3 ~7K)
   // Hub list for the leaf-weight prefill, refreshed every kHubPeriod batches.
@@ -909,15 +911,18 @@ struct bdsm_engine {
         a.deadline_ns = device_deadline(qs.deadline_s);
       }
       launch_anchor_count(a, stream);
-      size_t tmp = cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(), AnchorCount{0, 0, 0},
-                                        int(n + 1), stream));
+      a.self_scan = n <= tune_self_scan;
+      if (!a.self_scan) {
+        size_t tmp = cub_tmp.n;
+        CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(),
+                                          AnchorCount{0, 0, 0}, int(n + 1), stream));
+        cub_calls += 1;
+      }
       if (!(collect_cap && qs.q.n <= 2)) launch_anchor_emit(a, stream);
       // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
       CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
       a.epoch = ++epoch;
       launches += 2;
-      cub_calls += 1;
       if (collect_cap) {  // --dump-matches: materialise this (query, phase)'s matches
         qs.mbuf[phase].ensure(collect_cap * qs.q.n);
         qs.mcount.ensure(2);

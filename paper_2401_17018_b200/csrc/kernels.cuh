@@ -117,6 +117,7 @@ struct PhaseArgs {
   uint32_t shard_rank, shard_world;
   AnchorCount* upd_cnt;          // [n_ups + 1] per-update anchors / items / driver mass (scan input)
   AnchorCount* upd_off;          // its exclusive scan
+  uint32_t self_scan;            // small batch: k_anchor_emit scans upd_cnt itself (upd_off unused)
   Task* tasks;
   Item* items;
   uint32_t max_items;

@@ -121,9 +121,68 @@ __global__ void k_anchor_count(PhaseArgs a) {
   }
 }
 
+__device__ __forceinline__ AnchorCount ac_add(const AnchorCount& x, const AnchorCount& y) {
+  return AnchorCount{x.tasks + y.tasks, x.items + y.items, x.cost + y.cost};
+}
+__device__ __forceinline__ AnchorCount ac_shfl_up(const AnchorCount& v, uint32_t o) {
+  return AnchorCount{__shfl_up_sync(kFull, v.tasks, o), __shfl_up_sync(kFull, v.items, o),
+                     __shfl_up_sync(kFull, v.cost, o)};
+}
+__device__ __forceinline__ AnchorCount ac_shfl_xor(const AnchorCount& v, uint32_t o) {
+  return AnchorCount{__shfl_xor_sync(kFull, v.tasks, o), __shfl_xor_sync(kFull, v.items, o),
+                     __shfl_xor_sync(kFull, v.cost, o)};
+}
+
+// Small batches (a.self_scan): the exclusive scan of the per-update counts is
+// done here instead of by a separate device scan — every block sums the counts
+// before its first update and the grand total (a few thousand 16-byte loads
+// per block), then scans its own 256 updates.  Launched with one thread per
+// update.
+__device__ void anchor_self_scan(const PhaseArgs& a, AnchorCount& off, AnchorCount& tot) {
+  __shared__ AnchorCount s_pre[8], s_tot[8], s_w[8];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t first = blockIdx.x * blockDim.x;
+  AnchorCount pre{0, 0, 0}, all{0, 0, 0};
+  for (uint32_t j = threadIdx.x; j < a.n_ups; j += blockDim.x) {
+    const AnchorCount v = a.upd_cnt[j];
+    all = ac_add(all, v);
+    if (j < first) pre = ac_add(pre, v);
+  }
+#pragma unroll
+  for (uint32_t o = 16; o; o >>= 1) {
+    pre = ac_add(pre, ac_shfl_xor(pre, o));
+    all = ac_add(all, ac_shfl_xor(all, o));
+  }
+  const uint32_t i = first + threadIdx.x;
+  const AnchorCount mine = i < a.n_ups ? a.upd_cnt[i] : AnchorCount{0, 0, 0};
+  AnchorCount inc = mine;
+#pragma unroll
+  for (uint32_t o = 1; o < 32; o <<= 1) {
+    const AnchorCount t = ac_shfl_up(inc, o);
+    if (lane >= o) inc = ac_add(inc, t);
+  }
+  if (lane == 0) {
+    s_pre[w] = pre;
+    s_tot[w] = all;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  AnchorCount base{0, 0, 0};
+  tot = AnchorCount{0, 0, 0};
+  for (uint32_t k = 0; k < (blockDim.x >> 5); ++k) {
+    base = ac_add(base, s_pre[k]);
+    tot = ac_add(tot, s_tot[k]);
+    if (k < w) base = ac_add(base, s_w[k]);
+  }
+  off = AnchorCount{base.tasks + inc.tasks - mine.tasks, base.items + inc.items - mine.items,
+                    base.cost + inc.cost - mine.cost};
+}
+
 __global__ void k_anchor_emit(PhaseArgs a) {
   if (batch_aborted(a.st)) return;
-  const AnchorCount tot = a.upd_off[a.n_ups];
+  AnchorCount tot, self_off{0, 0, 0};
+  if (a.self_scan) anchor_self_scan(a, self_off, tot);
+  else tot = a.upd_off[a.n_ups];
   const uint64_t total_cost = tot.cost;
   const uint32_t total_items = tot.items;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -136,7 +195,7 @@ __global__ void k_anchor_emit(PhaseArgs a) {
   uint64_t direct = 0;    // 2-vertex queries: every anchor is a match
   uint64_t bytes = 0, calls = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ups; i += gridDim.x * blockDim.x) {
-    const AnchorCount off = a.upd_off[i];
+    const AnchorCount off = a.self_scan ? self_off : a.upd_off[i];
     uint32_t t = off.tasks, it = off.items;
     uint64_t c = off.cost;
     for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up) {

@@ -190,6 +190,21 @@ def test_hub_bitmaps_do_not_change_counts(monkeypatch):
             e.close()
 
 
+@pytest.mark.parametrize("self_scan", ["0", "1000000"])
+def test_anchor_offset_scan_paths(monkeypatch, self_scan):
+    """Anchor offsets come from a separate device scan (large batches) or from
+    k_anchor_emit's own block scan (batches up to 16K updates); both paths,
+    forced on every golden suite, give the reference's counts."""
+    monkeypatch.setenv("BDSM_TUNE_SELFSCAN", self_scan)
+    for suite in gu.SUITES:
+        for inst in gu.load(suite):
+            e, batches = _engine(inst)
+            for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
+                r = e.match_batch(b)
+                assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (suite, inst["name"], bi)
+            e.close()
+
+
 @pytest.mark.parametrize("bitmap_mindeg", [None, "4"])
 def test_thread_merge_matches_reference(monkeypatch, bitmap_mindeg):
     """Short lists (<= 64 entries) of large batches are merged one per thread
