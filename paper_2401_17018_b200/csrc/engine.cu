@@ -169,7 +169,7 @@ struct bdsm_engine {
   // matching-kernel tuning knobs (BDSM_TUNE_BACKOFF / BDSM_TUNE_MERGE env overrides, for sweeps)
   uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
-  uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 4: force a matching-kernel variant
+  uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 3 / 4: force a matching-kernel variant
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
   // batches of at least this many directed keys merge short lists one per
@@ -959,7 +959,7 @@ struct bdsm_engine {
         }
         // variant by the previous batch's work items of this (query, phase)
         launch_wbm(a, num_sms,
-                   tune_variant ? tune_variant == 4 : qs.prev_items[phase] > tune_throughput_items, stream);
+                   tune_variant ? int(tune_variant) : qs.prev_items[phase] > tune_throughput_items ? 4 : 2, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
       }

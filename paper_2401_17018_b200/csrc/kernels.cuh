@@ -143,8 +143,8 @@ struct PhaseArgs {
 
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);
 void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s);
-// throughput: the 64-register / 4-CTA variant for launches with many work items
-void launch_wbm(const PhaseArgs& a, int num_sms, bool throughput, cudaStream_t s);
+// ctas_per_sm: 2 (104 registers, launches bound by their longest subtree), 3 (80), 4 (64, many work items)
+void launch_wbm(const PhaseArgs& a, int num_sms, int ctas_per_sm, cudaStream_t s);
 void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, const uint32_t* hubs,
                          const uint32_t* n_hubs, int num_sms, cudaStream_t s);
 void launch_select_hubs(const uint32_t* deg, uint32_t V, uint32_t min_deg, uint32_t* hubs, uint32_t* n_hubs,

@@ -1289,9 +1289,10 @@ void launch_wbm_variant(const PhaseArgs& a, int num_sms, cudaStream_t s) {
   k_wbm<kEmit, kMinBlocks><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
 }
 
-void launch_wbm(const PhaseArgs& a, int num_sms, bool throughput, cudaStream_t s) {
+void launch_wbm(const PhaseArgs& a, int num_sms, int ctas_per_sm, cudaStream_t s) {
   if (a.match_out) launch_wbm_variant<true, 2>(a, num_sms, s);
-  else if (throughput) launch_wbm_variant<false, 4>(a, num_sms, s);
+  else if (ctas_per_sm >= 4) launch_wbm_variant<false, 4>(a, num_sms, s);
+  else if (ctas_per_sm == 3) launch_wbm_variant<false, 3>(a, num_sms, s);
   else launch_wbm_variant<false, 2>(a, num_sms, s);
 }
 
