@@ -343,6 +343,12 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   const uint32_t nb = lp.nback;
   uint32_t myd = 0xffffffffu;
   uint64_t myo = 0;
+  const uint32_t lb_list = (lane >> 1) & 31;
+  // with a label index the sub-range bounds depend only on the list's vertex:
+  // lanes 2b / 2b+1 load them in the same round trip as the degrees
+  uint32_t ibnd = 0;
+  if (g.loff && lp.lcls != kNone && lane < 2 * nb)
+    ibnd = __ldg(g.loff + uint64_t(M[lp.back[lb_list]]) * (g.nlab + 1) + lp.lcls + (lane & 1));
   if (lane < nb) {
     const uint32_t x = M[lp.back[lane]];
     myd = __ldg(g.deg + x);
@@ -352,12 +358,12 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   LevelSetup s;
   s.drv_b = __ffs(__ballot_sync(kFull, myd == mn)) - 1;
   s.deg_sum = __reduce_add_sync(kFull, lane < nb ? myd : 0u);
-  const uint32_t lb_list = (lane >> 1) & 31;
   const uint32_t bd = __shfl_sync(kFull, myd, lb_list);
   const uint64_t bo = __shfl_sync(kFull, myo, lb_list);
   uint32_t bnd = 0;
   if (lane < 2 * nb) {
     if (bd <= 32) bnd = (lane & 1) ? bd : 0u;
+    else if (g.loff) bnd = lp.lcls == kNone ? 0u : ibnd;
     else bnd = label_bound(g, M[lp.back[lb_list]], g.adj + bo, bd, lp.lcls, lp.vlo, lp.vhi, lane & 1);
   }
   const uint32_t f = __shfl_sync(kFull, bnd, (2 * lane) & 31);
@@ -485,12 +491,16 @@ __device__ __forceinline__ unsigned long long leaf_count(const PhaseArgs& a, con
                                                          bool x_touched, uint32_t anchor, uint32_t flag,
                                                          uint32_t lane) {
   const DevGraph& g = a.g;
+  // the label-index bounds are loaded in the same round trip as the list
+  uint32_t ib = 0;
+  if (g.loff && lp.lcls != kNone && lane < 2) ib = __ldg(g.loff + uint64_t(x) * (g.nlab + 1) + lp.lcls + lane);
   const uint64_t xo = __ldg(g.off + x);
   const uint32_t xd = __ldg(g.deg + x);
   uint32_t lo = 0, hi = xd;
   if (xd > 32) {
     uint32_t bnd = 0;
-    if (lane < 2) bnd = label_bound(g, x, g.adj + xo, xd, lp.lcls, lp.vlo, lp.vhi, lane);
+    if (lane < 2)
+      bnd = g.loff ? (lp.lcls == kNone ? 0u : ib) : label_bound(g, x, g.adj + xo, xd, lp.lcls, lp.vlo, lp.vhi, lane);
     lo = __shfl_sync(kFull, bnd, 0);
     hi = __shfl_sync(kFull, bnd, 1);
   }
