@@ -144,6 +144,18 @@ BDSM_API bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const b
                                            size_t n, uint64_t* pos, uint64_t* neg,
                                            bdsm_batch_stats* stats);
 
+/* Pipelined form of bdsm_engine_apply_batch (run_pipeline's stage overlap,
+ * src/bench.cpp:370-564): submit copies the host batch into the engine's
+ * page-locked staging buffer, enqueues its H2D and every phase, and returns
+ * without waiting — the caller may reuse `updates` at once and prepare the
+ * next batch while this one matches.  wait blocks until the batch is done,
+ * runs any rerun it needs and reports exactly as bdsm_engine_apply_batch
+ * (same counts, errors and all-or-nothing contract).  One batch in flight per
+ * engine: submit while one is in flight, or wait with none, is
+ * BDSM_INVALID_ARGUMENT. */
+BDSM_API bdsm_status bdsm_engine_submit_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n);
+BDSM_API bdsm_status bdsm_engine_wait(bdsm_engine* engine, uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats);
+
 /* Per-query time budget in seconds for subsequent batches (MatchOptions::
  * deadline, PipelineConfig::timeout_seconds); <= 0 disables. */
 BDSM_API bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seconds_from_now);

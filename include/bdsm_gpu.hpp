@@ -129,16 +129,22 @@ class Engine {
 
   // match_batch (src/matcher.cpp:370-389) for every registered query.
   std::vector<Counts> match_batch(const std::vector<EdgeUpdate>& batch, bdsm_batch_stats* stats = nullptr) {
-    std::vector<bdsm_update> ups;
-    ups.reserve(batch.size());
-    for (const auto& u : batch)
-      ups.push_back({u.u, u.v, u.is_insert() ? 0u : 1u,
-                     u.is_insert() && u.edge_label ? *u.edge_label : BDSM_NO_LABEL});
+    const std::vector<bdsm_update> ups = pack(batch);
     std::vector<std::uint64_t> pos(nq_), neg(nq_);
     check(bdsm_engine_apply_batch(e_, ups.data(), ups.size(), pos.data(), neg.data(), stats));
-    std::vector<Counts> out(nq_);
-    for (std::size_t i = 0; i < nq_; ++i) out[i] = {pos[i], neg[i]};
-    return out;
+    return counts(pos, neg);
+  }
+
+  // Pipelined match_batch (run_pipeline's stage overlap, src/bench.cpp:370-564):
+  // submit returns once the batch is enqueued; wait returns its counts.
+  void submit(const std::vector<EdgeUpdate>& batch) {
+    const std::vector<bdsm_update> ups = pack(batch);
+    check(bdsm_engine_submit_batch(e_, ups.data(), ups.size()));
+  }
+  std::vector<Counts> wait(bdsm_batch_stats* stats = nullptr) {
+    std::vector<std::uint64_t> pos(nq_), neg(nq_);
+    check(bdsm_engine_wait(e_, pos.data(), neg.data(), stats));
+    return counts(pos, neg);
   }
 
   void set_deadline(int query, double seconds_from_now) {
@@ -169,6 +175,19 @@ class Engine {
   bdsm_engine* handle() { return e_; }
 
  private:
+  static std::vector<bdsm_update> pack(const std::vector<EdgeUpdate>& batch) {
+    std::vector<bdsm_update> ups;
+    ups.reserve(batch.size());
+    for (const auto& u : batch)
+      ups.push_back({u.u, u.v, u.is_insert() ? 0u : 1u,
+                     u.is_insert() && u.edge_label ? *u.edge_label : BDSM_NO_LABEL});
+    return ups;
+  }
+  std::vector<Counts> counts(const std::vector<std::uint64_t>& pos, const std::vector<std::uint64_t>& neg) const {
+    std::vector<Counts> out(nq_);
+    for (std::size_t i = 0; i < nq_; ++i) out[i] = {pos[i], neg[i]};
+    return out;
+  }
   void check(bdsm_status s) {
     if (s == BDSM_OK) return;
     std::string msg = bdsm_last_error();

@@ -95,6 +95,10 @@ def _load():
         f = getattr(L, name)
         f.restype = C.c_int
         f.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
+    L.bdsm_engine_submit_batch.restype = C.c_int
+    L.bdsm_engine_submit_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.bdsm_engine_wait.restype = C.c_int
+    L.bdsm_engine_wait.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
     L.bdsm_engine_set_deadline.restype = C.c_int
     L.bdsm_engine_set_deadline.argtypes = [C.c_void_p, C.c_int, C.c_double]
     L.bdsm_last_batch_errors.restype = C.c_size_t
@@ -262,6 +266,24 @@ class Engine:
         return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
 
     apply_batch = match_batch
+
+    def submit_batch(self, updates) -> None:
+        """Pipelined match_batch, first half: stages the host batch and
+        enqueues it; returns at once (the caller may reuse `updates`)."""
+        ups = make_updates(updates)
+        r = lib().bdsm_engine_submit_batch(self._h, _ptr(ups) if len(ups) else None, len(ups))
+        if r != 0:
+            _raise(r, self._h)
+
+    def wait(self) -> BatchResult:
+        """Second half: the submitted batch's result (as match_batch)."""
+        pos = np.zeros(max(self.nq, 1), np.uint64)
+        neg = np.zeros(max(self.nq, 1), np.uint64)
+        st = _Stats()
+        r = lib().bdsm_engine_wait(self._h, _ptr(pos), _ptr(neg), C.byref(st))
+        if r != 0:
+            _raise(r, self._h)
+        return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
 
     def match_batch_device(self, dev_ptr: int, n: int) -> BatchResult:
         """Same, with the packed updates already in device memory (e.g. a

@@ -980,20 +980,118 @@ struct bdsm_engine {
     return s;
   }
 
-  bdsm_status apply(const bdsm_update* updates, size_t n, bool device_input, uint64_t* pos,
-                    uint64_t* neg, bdsm_batch_stats* stats) {
-    auto t0 = std::chrono::steady_clock::now();
-    last_errors.clear();
+  // One batch in flight per engine: submit enqueues it (H2D, every phase) and
+  // returns; wait synchronises once, handles reruns and reports.  apply() is
+  // the two back to back; the pipelined API (bdsm_engine_submit_batch /
+  // bdsm_engine_wait) lets the caller prepare the next batch meanwhile.
+  struct Pending {
+    bool active = false;
+    size_t n = 0;
+    bool device_input = false;
+    const bdsm_update_dev* src = nullptr;
+    std::chrono::steady_clock::time_point t0;
     bdsm_batch_stats st{};
-    for (size_t qi = 0; qi < queries.size(); ++qi) {
-      if (pos) pos[qi] = 0;
-      if (neg) neg[qi] = 0;
+    uint32_t compactions = 0;
+    int attempt = 0;
+  };
+  Pending pend;
+
+  void launch_attempt() {
+    const size_t n = pend.n;
+    const bool device_input = pend.device_input;
+    const bdsm_update_dev* src = pend.src;
+    kev_used = 0;
+    launches = 0;
+    cub_calls = 0;
+    CK(cudaEventRecord(ev[0], stream));
+    if (!device_input) {
+      CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+      pend.st.h2d_bytes = n * sizeof(bdsm_update);
     }
-    if (n == 0) {
-      if (stats) *stats = st;
-      return BDSM_OK;
+    *h_st = template_state();
+    CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+    const uint32_t m = uint32_t(2 * n);
+    const uint32_t nq = uint32_t(queries.size());
+    if (pend.attempt == 0) hot_pack_maybe();
+    launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
+                   stream);
+    {
+      size_t tmp = cub_tmp.n;
+      cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
+      cub::DoubleBuffer<uint32_t> vb(vals.p, svals.p);
+      CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, 64, stream));
+      if (kb.Current() != skeys.p)
+        CK(cudaMemcpyAsync(skeys.p, kb.Current(), 8ull * m, cudaMemcpyDeviceToDevice, stream));
+      if (vb.Current() != svals.p)
+        CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
     }
+    // device-input batches: the ups buffer the kernels read is `src`
+    CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
+    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
+                     uint32_t(hkeys.n - 1), stream);
+    {
+      size_t tmp = cub_tmp.n;
+      CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
+                                    &d_st.p->n_touched, int(m), stream));
+      tmp = cub_tmp.n;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, insflag.p, ins_prefix.p, int(m + 1), stream));
+    }
+    CK(cudaEventRecord(ev[1], stream));
+    run_phase(uint32_t(n), 0);
+    CK(cudaEventRecord(ev[2], stream));
+    cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
+    CK(cudaEventRecord(m0, stream));
+    const bool small_ok = m >= tune_small_min;
+    launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
+                 small_list.p, mid_list.p, small_ok, stream);
+    launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
+                         d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
+                         uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, mid_list.p, small_ok,
+                         num_sms, stream);
+    CK(cudaEventRecord(m1, stream));
+    launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
+    cub_calls += 3; // sort, select, scan
+    CK(cudaEventRecord(ev[3], stream));
+    run_phase(uint32_t(n), 1);
+    if (opts.l2_hot_mb) {  // K8 estimator: walks from this batch's touched vertices
+      heat.ensure(g.V);
+      if (!heat_init) {
+        CK(cudaMemsetAsync(heat.p, 0, 4ull * g.V, stream));
+        heat_init = true;
+      }
+      launch_hot_walks(heads.p, skeys.p, d_st.p, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
+      ++launches;
+    }
+    launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
+    ++launches;
+    CK(cudaEventRecord(ev[4], stream));
+    CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+    if (memo.p) {
+      if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
+      CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+    }
+    CK(cudaEventRecord(ev[5], stream));
+  }
+
+  void relaunch() {
+    if (++pend.attempt > 8) throw std::runtime_error("batch could not be scheduled");
+    launch_attempt();
+  }
+
+  // copy_host: always stage host updates through the engine's pinned buffer
+  // (the caller may reuse its buffer as soon as submit returns)
+  void submit(const bdsm_update* updates, size_t n, bool device_input, bool copy_host) {
+    if (pend.active) throw std::invalid_argument("a batch is already in flight on this engine (wait for it first)");
+    pend = Pending{};
+    pend.t0 = std::chrono::steady_clock::now();
+    last_errors.clear();
+    pend.n = n;
+    pend.device_input = device_input;
     if (n >= (size_t(1) << 31)) throw std::invalid_argument("batch too large");
+    if (n == 0) {
+      pend.active = true;
+      return;
+    }
     // (a labelled insert into an unlabelled graph is detected by k_prepare:
     // overflow 4 enables the label array and reruns the batch)
     ensure_batch(n);
@@ -1013,7 +1111,7 @@ struct bdsm_engine {
       cudaPointerAttributes pa{};
       const bool pinned = cudaPointerGetAttributes(&pa, updates) == cudaSuccess && pa.type == cudaMemoryTypeHost;
       cudaGetLastError();  // clear a pageable-pointer query error, if any
-      if (pinned) {
+      if (pinned && !copy_host) {
         h_src = updates;
       } else {
         ensure_host_ups(n);
@@ -1022,123 +1120,75 @@ struct bdsm_engine {
       }
       src = ups_ext.p;
     }
-    uint32_t compactions = 0;
-    for (int attempt = 0;; ++attempt) {
-      if (attempt > 8) throw std::runtime_error("batch could not be scheduled");
-      kev_used = 0;
-      launches = 0;
-      cub_calls = 0;
-      CK(cudaEventRecord(ev[0], stream));
-      if (!device_input) {
-        CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
-        st.h2d_bytes = n * sizeof(bdsm_update);
-      }
-      *h_st = template_state();
-      CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
-      const uint32_t m = uint32_t(2 * n);
-      const uint32_t nq = uint32_t(queries.size());
-      if (attempt == 0) hot_pack_maybe();
-      launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
-                     stream);
-      {
-        size_t tmp = cub_tmp.n;
-        cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
-        cub::DoubleBuffer<uint32_t> vb(vals.p, svals.p);
-        CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, 64, stream));
-        if (kb.Current() != skeys.p)
-          CK(cudaMemcpyAsync(skeys.p, kb.Current(), 8ull * m, cudaMemcpyDeviceToDevice, stream));
-        if (vb.Current() != svals.p)
-          CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
-      }
-      // device-input batches: the ups buffer the kernels read is `src`
-      CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-      launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
-                       uint32_t(hkeys.n - 1), stream);
-      {
-        size_t tmp = cub_tmp.n;
-        CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
-                                      &d_st.p->n_touched, int(m), stream));
-        tmp = cub_tmp.n;
-        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, insflag.p, ins_prefix.p, int(m + 1), stream));
-      }
-      CK(cudaEventRecord(ev[1], stream));
-      run_phase(uint32_t(n), 0);
-      CK(cudaEventRecord(ev[2], stream));
-      cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
-      CK(cudaEventRecord(m0, stream));
-      const bool small_ok = m >= tune_small_min;
-      launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
-                   small_list.p, mid_list.p, small_ok, stream);
-      launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
-                           d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
-                           uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, mid_list.p, small_ok,
-                           num_sms, stream);
-      CK(cudaEventRecord(m1, stream));
-      launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
-      cub_calls += 3; // sort, select, scan
-      CK(cudaEventRecord(ev[3], stream));
-      run_phase(uint32_t(n), 1);
-      if (opts.l2_hot_mb) {  // K8 estimator: walks from this batch's touched vertices
-        heat.ensure(g.V);
-        if (!heat_init) {
-          CK(cudaMemsetAsync(heat.p, 0, 4ull * g.V, stream));
-          heat_init = true;
-        }
-        launch_hot_walks(heads.p, skeys.p, d_st.p, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
-        ++launches;
-      }
-      launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
-      ++launches;
-      CK(cudaEventRecord(ev[4], stream));
-      CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
-      if (memo.p) {
-        if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
-        CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
-      }
-      CK(cudaEventRecord(ev[5], stream));
+    pend.src = src;
+    launch_attempt();
+    pend.active = true;
+  }
+
+  bdsm_status wait(uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats) {
+    if (!pend.active) throw std::invalid_argument("no batch in flight on this engine");
+    struct Done {
+      Pending& p;
+      ~Done() { p.active = false; }
+    } done{pend};
+    for (size_t qi = 0; qi < queries.size(); ++qi) {
+      if (pos) pos[qi] = 0;
+      if (neg) neg[qi] = 0;
+    }
+    if (pend.n == 0) {
+      if (stats) *stats = pend.st;
+      return BDSM_OK;
+    }
+    const size_t n = pend.n;
+    const bool device_input = pend.device_input;
+    const bdsm_update_dev* src = pend.src;
+    for (;;) {
       sync();
-      const BatchState& b = *h_st;
-      // the hot-list arena (K8) is reserved even when the batch is then rejected
-      // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
-      if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
-      if (b.selfloop_min != kNone || b.conflict_min != kNone) {
-        bdsm_update bad{};
-        uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
-        fetch_update(src, device_input, idx, &bad);
-        if (b.selfloop_min <= b.conflict_min)
-          throw std::invalid_argument("self-loop update (" + std::to_string(bad.u) + "," +
-                                      std::to_string(bad.v) + ")");
-        throw std::invalid_argument("conflicting updates on edge (" + std::to_string(bad.u) + "," +
-                                    std::to_string(bad.v) + ") within one batch");
-      }
-      if (b.err_count) {
-        std::vector<uint8_t> codes(n);
-        CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
-        sync();
-        for (size_t i = 0; i < n; ++i)
-          if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
-        throw BatchRejected("batch rejected: " + std::to_string(last_errors.size()) +
-                            " invalid update(s), none applied");
-      }
-      if (b.overflow == 4) {  // labelled insert into an unlabelled graph: nothing merged
-        enable_edge_labels();
-        continue;
-      }
-      if (b.overflow == 1) {  // adjacency pool exhausted: nothing merged yet
-        compact(b.pool_top > g.pool_size ? b.pool_top - pool_top : 0);
-        ++compactions;
-        continue;
-      }
-      if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
-        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
-        items.ensure(max_items);
-        continue;
-      }
-      if (b.overflow == 3) {  // positive phase only (graph already merged)
-        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
-        items.ensure(max_items);
-        rerun_positive(uint32_t(n));
-      }
+    const BatchState& b = *h_st;
+    // the hot-list arena (K8) is reserved even when the batch is then rejected
+    // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
+    if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
+    if (b.selfloop_min != kNone || b.conflict_min != kNone) {
+      bdsm_update bad{};
+      uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
+      fetch_update(src, device_input, idx, &bad);
+      if (b.selfloop_min <= b.conflict_min)
+        throw std::invalid_argument("self-loop update (" + std::to_string(bad.u) + "," +
+                                    std::to_string(bad.v) + ")");
+      throw std::invalid_argument("conflicting updates on edge (" + std::to_string(bad.u) + "," +
+                                  std::to_string(bad.v) + ") within one batch");
+    }
+    if (b.err_count) {
+      std::vector<uint8_t> codes(n);
+      CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
+      sync();
+      for (size_t i = 0; i < n; ++i)
+        if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
+      throw BatchRejected("batch rejected: " + std::to_string(last_errors.size()) +
+                          " invalid update(s), none applied");
+    }
+    if (b.overflow == 4) {  // labelled insert into an unlabelled graph: nothing merged
+      enable_edge_labels();
+      relaunch();
+      continue;
+    }
+    if (b.overflow == 1) {  // adjacency pool exhausted: nothing merged yet
+      compact(b.pool_top > g.pool_size ? b.pool_top - pool_top : 0);
+      ++pend.compactions;
+      relaunch();
+      continue;
+    }
+    if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
+      max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
+      items.ensure(max_items);
+      relaunch();
+      continue;
+    }
+    if (b.overflow == 3) {  // positive phase only (graph already merged)
+      max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
+      items.ensure(max_items);
+      rerun_positive(uint32_t(n));
+    }
       break;
     }
     const BatchState& b = *h_st;
@@ -1158,38 +1208,44 @@ struct bdsm_engine {
     }
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[0], ev[5]);
-    st.ms_device = ms;
+    pend.st.ms_device = ms;
     cudaEventElapsedTime(&ms, ev[1], ev[2]);
-    st.ms_negative = ms;
+    pend.st.ms_negative = ms;
     cudaEventElapsedTime(&ms, ev[2], ev[3]);
-    st.ms_update = ms;
+    pend.st.ms_update = ms;
     cudaEventElapsedTime(&ms, ev[3], ev[4]);
-    st.ms_positive = ms;
+    pend.st.ms_positive = ms;
     double mk = 0;
     for (size_t i = 0; i + 1 < kev_used; i += 2) {
       cudaEventElapsedTime(&ms, kev[i], kev[i + 1]);
       mk += ms;
     }
-    st.ms_match_kernel = mk;
+    pend.st.ms_match_kernel = mk;
     cudaEventElapsedTime(&ms, merge_ev[0], merge_ev[1]);
-    st.ms_merge_kernel = ms;
-    st.kernel_launches = launches;
-    st.cub_launches = cub_calls;
-    st.dfs_visits = b.visits;
-    st.tasks = b.tasks_total;
-    st.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
-    st.gen_calls = b.gen_calls;
-    st.bytes_phase = b.bytes_phase;
-    st.bytes_kernel = b.bytes_kernel;
-    st.bytes_update = b.bytes_update + 16ull * n;
-    st.touched = b.n_touched;
-    st.relocations = b.relocations;
-    st.compactions = compactions;
-    st.timed_out = b.timed_out;
-    st.d2h_bytes = sizeof(BatchState);
-    st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    if (stats) *stats = st;
+    pend.st.ms_merge_kernel = ms;
+    pend.st.kernel_launches = launches;
+    pend.st.cub_launches = cub_calls;
+    pend.st.dfs_visits = b.visits;
+    pend.st.tasks = b.tasks_total;
+    pend.st.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
+    pend.st.gen_calls = b.gen_calls;
+    pend.st.bytes_phase = b.bytes_phase;
+    pend.st.bytes_kernel = b.bytes_kernel;
+    pend.st.bytes_update = b.bytes_update + 16ull * n;
+    pend.st.touched = b.n_touched;
+    pend.st.relocations = b.relocations;
+    pend.st.compactions = pend.compactions;
+    pend.st.timed_out = b.timed_out;
+    pend.st.d2h_bytes = sizeof(BatchState);
+    pend.st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pend.t0).count();
+    if (stats) *stats = pend.st;
     return BDSM_OK;
+  }
+
+  bdsm_status apply(const bdsm_update* updates, size_t n, bool device_input, uint64_t* pos, uint64_t* neg,
+                    bdsm_batch_stats* stats) {
+    submit(updates, n, device_input, false);
+    return wait(pos, neg, stats);
   }
 
   // Positive-phase work items overflowed after the merge: grow and rerun that
@@ -1354,6 +1410,24 @@ bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const bdsm_updat
   return guarded([&]() -> bdsm_status {
     CK(cudaSetDevice(engine->device));
     return engine->apply(d_updates, n, true, pos, neg, stats);
+  });
+}
+
+bdsm_status bdsm_engine_submit_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  if (n && !updates) return fail(BDSM_INVALID_ARGUMENT, "null updates");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    engine->submit(updates, n, false, true);
+    return BDSM_OK;
+  });
+}
+
+bdsm_status bdsm_engine_wait(bdsm_engine* engine, uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    return engine->wait(pos, neg, stats);
   });
 }
 

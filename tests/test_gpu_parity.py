@@ -63,6 +63,52 @@ def test_batch_errors_all_or_nothing():
     assert (r.positive, r.negative) == ([4], [0])
 
 
+def test_pipelined_submit_wait():
+    """bdsm_engine_submit_batch / bdsm_engine_wait (run_pipeline's stage
+    overlap): the caller's buffer is free once submit returns, the counts equal
+    match_batch's on every batch of a random stream, errors surface at wait
+    with nothing applied, and one batch at most is in flight."""
+    import numpy as np
+    import paper_2401_17018_b200 as bd
+    fig = {i["name"]: i for i in gu.load("fig1")}
+    e, _ = _engine(fig["fig1_batch"])
+    with pytest.raises(ValueError, match="no batch in flight"):
+        e.wait()
+    e.submit_batch([(0, 0, 2), (1, 0, 1), (0, 0, 3)])
+    with pytest.raises(ValueError, match="already in flight"):
+        e.submit_batch([(0, 1, 4)])
+    with pytest.raises(bd.BatchError):
+        e.wait()
+    e.submit_batch([(0, 0, 2), (0, 3, 3)])
+    with pytest.raises(ValueError, match="self-loop update"):
+        e.wait()
+    ups = bd.make_updates([(0, 0, 2), (0, 1, 4), (1, 4, 5)])
+    e.submit_batch(ups)
+    ups[:] = bd.make_updates([(1, 0, 3), (1, 0, 4), (1, 0, 6)])  # reused at once
+    r = e.wait()
+    assert (r.positive, r.negative) == ([4], [0])
+    e.close()
+    vl, edges, batches = _random_stream(31)
+    eu = [a for a, _ in edges]
+    ev = [b for _, b in edges]
+    q = ([0, 1, 2, 0], [(0, 1), (1, 2), (2, 0), (2, 3)])
+    e1, e2 = bd.Engine(vl, eu, ev), bd.Engine(vl, eu, ev)
+    e1.add_query(*q)
+    e2.add_query(*q)
+    buf = bd.make_updates(batches[0])
+    e2.submit_batch(buf)
+    for bi, b in enumerate(batches):
+        r1 = e1.match_batch(b)
+        r2 = e2.wait()
+        if bi + 1 < len(batches):
+            e2.submit_batch(bd.make_updates(batches[bi + 1]))
+        assert (r1.positive, r1.negative) == (r2.positive, r2.negative), bi
+    for v in range(0, len(vl), 97):
+        assert e1.neighbors(v) == e2.neighbors(v)
+    e1.close()
+    e2.close()
+
+
 def test_multi_query_sums_and_independence():
     import paper_2401_17018_b200 as bd
     insts = gu.load("streams")[:6]
