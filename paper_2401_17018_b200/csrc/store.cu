@@ -249,9 +249,18 @@ __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, ui
   }
 }
 
-constexpr uint32_t kBigList = 1024;        // lists this long are merged by a whole CTA (k_merge_big)
+#ifndef BDSM_BIG_LIST
+#define BDSM_BIG_LIST 1024
+#endif
+#ifndef BDSM_SMALL_LIST
+#define BDSM_SMALL_LIST 256
+#endif
+#ifndef BDSM_BIG_THREADS
+#define BDSM_BIG_THREADS 256
+#endif
+constexpr uint32_t kBigList = BDSM_BIG_LIST;  // lists this long are merged by a whole CTA (k_merge_big)
 constexpr uint32_t kBigFlag = 0x80000000u;  // new_cap[t]: the list is merged by k_merge_big
-constexpr uint32_t kSmallList = 64;         // lists up to this long (before and after) are merged by one thread
+constexpr uint32_t kSmallList = BDSM_SMALL_LIST;  // lists up to this long (before and after): one thread each
 constexpr uint32_t kSmallFlag = 0x40000000u;  // new_cap[t]: the list is merged by k_merge_small
 constexpr uint32_t kCapMask = 0x3fffffffu;
 
@@ -1140,7 +1149,7 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                     0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
                             st, memo, memo_mask, small_list);
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
-  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), BDSM_BIG_THREADS, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, big_list);
   k_finish_big<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * 32 + 255) / 256, uint64_t(num_sms) * 8)), 256, 0,
                  s>>>(heads, skeys, svals, m, g, qenc, nq, rows, colsize, st, memo, memo_mask, big_list);

@@ -253,7 +253,7 @@ def test_anchor_offset_scan_paths(monkeypatch, self_scan):
 
 @pytest.mark.parametrize("bitmap_mindeg", [None, "4"])
 def test_thread_merge_matches_reference(monkeypatch, bitmap_mindeg):
-    """Short lists (<= 64 entries) of large batches are merged one per thread
+    """Short lists (<= 256 entries) of large batches are merged one per thread
     (k_merge_small); the threshold is lowered so every golden batch takes
     that path: counts equal the reference's, and on a mixed random stream
     every neighbour list equals the expected one after each batch.  With
