@@ -119,6 +119,10 @@ uint64_t now_ns() {
 struct bdsm_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // the positive phase's touched-hub memo prefill runs here, beside the
+  // anchor kernels (both only read G'); joined before the matching kernel
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int num_sms = 148;
   bdsm_options opts{};
   DevGraphMut g{};
@@ -288,6 +292,9 @@ struct bdsm_engine {
     if (h_st) cudaFreeHost(h_st);
     if (h_memo_fill) cudaFreeHost(h_memo_fill);
     if (h_ups) cudaFreeHost(h_ups);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -904,6 +911,17 @@ struct bdsm_engine {
       QueryState& qs = *queries[qi];
       if (!qs.solved || qs.q.edges.empty()) continue;
       PhaseArgs a = phase_args(n, phase, int(qi));
+      // positive phase, warm memo: the touched hubs' weights are refilled on
+      // the side stream while the anchors are counted and emitted
+      const bool side_prefill = phase == 1 && qs.q.n > 2 && qs.has_leaf && !collect_cap && memo_persistent &&
+                                !qs.memo_cold && qs.n_leafsig;
+      if (side_prefill) {
+        CK(cudaEventRecord(fork_ev, stream));
+        CK(cudaStreamWaitEvent(side, fork_ev, 0));
+        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, side);
+        CK(cudaEventRecord(join_ev, side));
+        ++launches;
+      }
       if (qs.deadline_s > 0) {
         // device %globaltimer is in ns since an arbitrary epoch: express the
         // deadline relative to "now" on both clocks via a calibration kernel
@@ -947,6 +965,8 @@ struct bdsm_engine {
             launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
             qs.memo_cold = false;
             ++launches;
+          } else if (side_prefill) {
+            CK(cudaStreamWaitEvent(stream, join_ev, 0));
           } else if (phase == 1) {
             launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, stream);
             ++launches;
@@ -1373,6 +1393,9 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     e->device = o.device;
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
     e->build(graph);
     *out = e.release();
