@@ -123,6 +123,7 @@ struct bdsm_engine {
   // anchor kernels (both only read G'); joined before the matching kernel
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  bool early_anchors = false;  // this attempt's negative-phase anchors were issued on `side`
   int num_sms = 148;
   bdsm_options opts{};
   DevGraphMut g{};
@@ -928,17 +929,21 @@ struct bdsm_engine {
         // would be exact; the host steady clock offset is applied instead.
         a.deadline_ns = device_deadline(qs.deadline_s);
       }
-      launch_anchor_count(a, stream);
-      a.self_scan = n <= tune_self_scan;
-      if (!a.self_scan) {
-        size_t tmp = cub_tmp.n;
-        CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(),
-                                          AnchorCount{0, 0, 0}, int(n + 1), stream));
-        cub_calls += 1;
+      if (phase == 0 && early_anchors) {  // issued on the side stream by launch_attempt
+        CK(cudaStreamWaitEvent(stream, join_ev, 0));
+      } else {
+        launch_anchor_count(a, stream);
+        a.self_scan = n <= tune_self_scan;
+        if (!a.self_scan) {
+          size_t tmp = cub_tmp.n;
+          CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(),
+                                            AnchorCount{0, 0, 0}, int(n + 1), stream));
+          cub_calls += 1;
+        }
+        if (!(collect_cap && qs.q.n <= 2)) launch_anchor_emit(a, stream);
+        // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
+        CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
       }
-      if (!(collect_cap && qs.q.n <= 2)) launch_anchor_emit(a, stream);
-      // fresh work queues for this launch (next_item, dyn_head, dyn_tail, busy, idle)
-      CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
       a.epoch = ++epoch;
       launches += 2;
       if (collect_cap) {  // --dump-matches: materialise this (query, phase)'s matches
@@ -1035,6 +1040,22 @@ struct bdsm_engine {
     if (pend.attempt == 0) hot_pack_maybe();
     launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
                    stream);
+    // one query, small batch: the negative phase's anchors need only the
+    // translated updates and G, so they are counted and emitted on the side
+    // stream while the keys are sorted (joined before the matching kernel)
+    early_anchors = false;
+    if (queries.size() == 1 && n <= tune_self_scan && !collect_cap && queries[0]->solved &&
+        !queries[0]->q.edges.empty()) {
+      PhaseArgs a = phase_args(uint32_t(n), 0, 0);
+      a.self_scan = 1;
+      CK(cudaEventRecord(fork_ev, stream));
+      CK(cudaStreamWaitEvent(side, fork_ev, 0));
+      launch_anchor_count(a, side);
+      launch_anchor_emit(a, side);
+      CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), side));
+      CK(cudaEventRecord(join_ev, side));
+      early_anchors = true;
+    }
     {
       size_t tmp = cub_tmp.n;
       cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
