@@ -124,6 +124,8 @@ struct bdsm_engine {
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   bool early_anchors = false;  // this attempt's negative-phase anchors were issued on `side`
+  cudaEvent_t fork2_ev = nullptr, join2_ev = nullptr;  // the insert-prefix scan on `side`
+  DBuf<uint8_t> cub_tmp_side;
   int num_sms = 148;
   bdsm_options opts{};
   DevGraphMut g{};
@@ -295,6 +297,8 @@ struct bdsm_engine {
     if (h_ups) cudaFreeHost(h_ups);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
+    if (fork2_ev) cudaEventDestroy(fork2_ev);
+    if (join2_ev) cudaEventDestroy(join2_ev);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1071,15 +1075,24 @@ struct bdsm_engine {
     launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
                      uint32_t(hkeys.n - 1), stream);
     {
-      size_t tmp = cub_tmp.n;
+      // the merge's insert prefix is only needed after the negative phase: it
+      // is scanned on the side stream (own temporary storage) meanwhile
+      CK(cudaEventRecord(fork2_ev, stream));
+      CK(cudaStreamWaitEvent(side, fork2_ev, 0));
+      size_t tmp = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, insflag.p, ins_prefix.p, int(m + 1), side));
+      cub_tmp_side.ensure(tmp);
+      tmp = cub_tmp_side.n;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp_side.p, tmp, insflag.p, ins_prefix.p, int(m + 1), side));
+      CK(cudaEventRecord(join2_ev, side));
+      tmp = cub_tmp.n;
       CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
                                     &d_st.p->n_touched, int(m), stream));
-      tmp = cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, insflag.p, ins_prefix.p, int(m + 1), stream));
     }
     CK(cudaEventRecord(ev[1], stream));
     run_phase(uint32_t(n), 0);
     CK(cudaEventRecord(ev[2], stream));
+    CK(cudaStreamWaitEvent(stream, join2_ev, 0));
     cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
     CK(cudaEventRecord(m0, stream));
     const bool small_ok = m >= tune_small_min;
@@ -1417,6 +1430,8 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->fork2_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->join2_ev, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
     e->build(graph);
     *out = e.release();
