@@ -1022,6 +1022,7 @@ struct bdsm_engine {
     bdsm_batch_stats st{};
     uint32_t compactions = 0;
     int attempt = 0;
+    bool full_sort = false;  // rerun with the 64-bit key sort (an id beyond the sorted bits)
   };
   Pending pend;
 
@@ -1042,8 +1043,13 @@ struct bdsm_engine {
     const uint32_t m = uint32_t(2 * n);
     const uint32_t nq = uint32_t(queries.size());
     if (pend.attempt == 0) hot_pack_maybe();
+    // the sort orders the source id's significant bits only (+ the full
+    // destination word); larger (invalid) ids rerun with all 64 bits
+    const uint32_t id_bits = g.V > 1 ? 32u - uint32_t(__builtin_clz(g.V - 1)) : 1u;
+    const bool full_sort = pend.full_sort || id_bits >= 32;
+    const int sort_end_bit = full_sort ? 64 : int(32 + id_bits);
     launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
-                   stream);
+                   full_sort ? 0xffffffffu : (1u << id_bits), stream);
     // one query, small batch: the negative phase's anchors need only the
     // translated updates and G, so they are counted and emitted on the side
     // stream while the keys are sorted (joined before the matching kernel)
@@ -1064,7 +1070,7 @@ struct bdsm_engine {
       size_t tmp = cub_tmp.n;
       cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
       cub::DoubleBuffer<uint32_t> vb(vals.p, svals.p);
-      CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, 64, stream));
+      CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
       if (kb.Current() != skeys.p)
         CK(cudaMemcpyAsync(skeys.p, kb.Current(), 8ull * m, cudaMemcpyDeviceToDevice, stream));
       if (vb.Current() != svals.p)
@@ -1198,51 +1204,56 @@ struct bdsm_engine {
     const bdsm_update_dev* src = pend.src;
     for (;;) {
       sync();
-    const BatchState& b = *h_st;
-    // the hot-list arena (K8) is reserved even when the batch is then rejected
-    // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
-    if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
-    if (b.selfloop_min != kNone || b.conflict_min != kNone) {
-      bdsm_update bad{};
-      uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
-      fetch_update(src, device_input, idx, &bad);
-      if (b.selfloop_min <= b.conflict_min)
-        throw std::invalid_argument("self-loop update (" + std::to_string(bad.u) + "," +
-                                    std::to_string(bad.v) + ")");
-      throw std::invalid_argument("conflicting updates on edge (" + std::to_string(bad.u) + "," +
-                                  std::to_string(bad.v) + ") within one batch");
-    }
-    if (b.err_count) {
-      std::vector<uint8_t> codes(n);
-      CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
-      sync();
-      for (size_t i = 0; i < n; ++i)
-        if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
-      throw BatchRejected("batch rejected: " + std::to_string(last_errors.size()) +
-                          " invalid update(s), none applied");
-    }
-    if (b.overflow == 4) {  // labelled insert into an unlabelled graph: nothing merged
-      enable_edge_labels();
-      relaunch();
-      continue;
-    }
-    if (b.overflow == 1) {  // adjacency pool exhausted: nothing merged yet
-      compact(b.pool_top > g.pool_size ? b.pool_top - pool_top : 0);
-      ++pend.compactions;
-      relaunch();
-      continue;
-    }
-    if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
-      max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
-      items.ensure(max_items);
-      relaunch();
-      continue;
-    }
-    if (b.overflow == 3) {  // positive phase only (graph already merged)
-      max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
-      items.ensure(max_items);
-      rerun_positive(uint32_t(n));
-    }
+      const BatchState& b = *h_st;
+      // the hot-list arena (K8) is reserved even when the batch is then rejected
+      // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
+      if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
+      if (b.overflow == 5) {  // an id beyond the sorted bits (an invalid batch): exact errors need the full sort
+        pend.full_sort = true;
+        relaunch();
+        continue;
+      }
+      if (b.selfloop_min != kNone || b.conflict_min != kNone) {
+        bdsm_update bad{};
+        uint32_t idx = std::min(b.selfloop_min, b.conflict_min);
+        fetch_update(src, device_input, idx, &bad);
+        if (b.selfloop_min <= b.conflict_min)
+          throw std::invalid_argument("self-loop update (" + std::to_string(bad.u) + "," +
+                                      std::to_string(bad.v) + ")");
+        throw std::invalid_argument("conflicting updates on edge (" + std::to_string(bad.u) + "," +
+                                    std::to_string(bad.v) + ") within one batch");
+      }
+      if (b.err_count) {
+        std::vector<uint8_t> codes(n);
+        CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
+        sync();
+        for (size_t i = 0; i < n; ++i)
+          if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
+        throw BatchRejected("batch rejected: " + std::to_string(last_errors.size()) +
+                            " invalid update(s), none applied");
+      }
+      if (b.overflow == 4) {  // labelled insert into an unlabelled graph: nothing merged
+        enable_edge_labels();
+        relaunch();
+        continue;
+      }
+      if (b.overflow == 1) {  // adjacency pool exhausted: nothing merged yet
+        compact(b.pool_top > g.pool_size ? b.pool_top - pool_top : 0);
+        ++pend.compactions;
+        relaunch();
+        continue;
+      }
+      if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
+        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
+        items.ensure(max_items);
+        relaunch();
+        continue;
+      }
+      if (b.overflow == 3) {  // positive phase only (graph already merged)
+        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
+        items.ensure(max_items);
+        rerun_positive(uint32_t(n));
+      }
       break;
     }
     const BatchState& b = *h_st;

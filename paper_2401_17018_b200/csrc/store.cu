@@ -156,14 +156,18 @@ __global__ void k_compact(DevGraphMut g, const uint64_t* __restrict__ new_off,
 // binary search in the lower-degree endpoint's sorted list.
 // External vertex ids are translated to the internal label-ordered ids here;
 // every later kernel reads the translated copy `iups`.
+// id_limit: the radix sort only orders the low bits of the source id; an
+// (invalid) id at or above it sets overflow 5 and the host reruns the batch
+// with the full 64-bit sort, so its error is reported exactly.
 __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, DevGraph g,
                           const uint32_t* __restrict__ new_of, bdsm_update_dev* iups, BatchState* st,
-                          uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode) {
+                          uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, uint32_t id_limit) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
     if (up.u < g.V) up.u = new_of[up.u];
     if (up.v < g.V) up.v = new_of[up.v];
     iups[i] = up;
+    if (up.u >= id_limit || up.v >= id_limit) st->overflow = 5;
     uint32_t del = up.op != 0 ? 1u : 0u;
     keys[2 * i] = (uint64_t(up.u) << 32) | up.v;
     keys[2 * i + 1] = (uint64_t(up.v) << 32) | up.u;
@@ -1109,8 +1113,8 @@ void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* 
 }
 void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const uint32_t* new_of,
                     bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
-                    uint8_t* ecode, cudaStream_t s) {
-  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode);
+                    uint8_t* ecode, uint32_t id_limit, cudaStream_t s) {
+  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode, id_limit);
 }
 void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
                       uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
