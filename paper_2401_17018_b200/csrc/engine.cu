@@ -147,8 +147,8 @@ struct bdsm_engine {
   // batch buffers
   DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
   DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
-  DBuf<uint64_t> keys, skeys;
-  DBuf<uint32_t> vals, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list, mid_list;
+  DBuf<uint64_t> keys, keys2, skeys;
+  DBuf<uint32_t> vals, vals2, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list, mid_list;
   DBuf<uint8_t> ecode, head;
   DBuf<uint64_t> new_off;
   DBuf<unsigned long long> hkeys;  // visibility table of the batch
@@ -814,8 +814,10 @@ struct bdsm_engine {
     ups.ensure(cap_n);
     ups_ext.ensure(cap_n);
     keys.ensure(m);
+    keys2.ensure(m);
     skeys.ensure(m);
     vals.ensure(m);
+    vals2.ensure(m);
     svals.ensure(m);
     dlab.ensure(cap_n);
     ecode.ensure(cap_n);
@@ -1047,9 +1049,10 @@ struct bdsm_engine {
     // destination word); larger (invalid) ids rerun with all 64 bits
     const uint32_t id_bits = g.V > 1 ? 32u - uint32_t(__builtin_clz(g.V - 1)) : 1u;
     const bool full_sort = pend.full_sort || id_bits >= 32;
-    const int sort_end_bit = full_sort ? 64 : int(32 + id_bits);
+    const uint32_t key_bits = full_sort ? 32u : id_bits;  // both ids packed into 2 x id_bits
+    const int sort_end_bit = full_sort ? 64 : int(2 * id_bits);
     launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
-                   full_sort ? 0xffffffffu : (1u << id_bits), stream);
+                   full_sort ? 0xffffffffu : (1u << id_bits), key_bits, stream);
     // one query, small batch: the negative phase's anchors need only the
     // translated updates and G, so they are counted and emitted on the side
     // stream while the keys are sorted (joined before the matching kernel)
@@ -1066,20 +1069,17 @@ struct bdsm_engine {
       CK(cudaEventRecord(join_ev, side));
       early_anchors = true;
     }
+    // the sort ping-pongs between keys/keys2 (vals/vals2); k_post_sort
+    // widens its output into skeys/svals, which every later kernel reads
+    cub::DoubleBuffer<uint64_t> kb(keys.p, keys2.p);
+    cub::DoubleBuffer<uint32_t> vb(vals.p, vals2.p);
     {
       size_t tmp = cub_tmp.n;
-      cub::DoubleBuffer<uint64_t> kb(keys.p, skeys.p);
-      cub::DoubleBuffer<uint32_t> vb(vals.p, svals.p);
       CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
-      if (kb.Current() != skeys.p)
-        CK(cudaMemcpyAsync(skeys.p, kb.Current(), 8ull * m, cudaMemcpyDeviceToDevice, stream));
-      if (vb.Current() != svals.p)
-        CK(cudaMemcpyAsync(svals.p, vb.Current(), 4ull * m, cudaMemcpyDeviceToDevice, stream));
     }
-    // device-input batches: the ups buffer the kernels read is `src`
     CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
-                     uint32_t(hkeys.n - 1), stream);
+    launch_post_sort(kb.Current(), vb.Current(), key_bits, skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p,
+                     nq, g.V, hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
     {
       // the merge's insert prefix is only needed after the negative phase: it
       // is scanned on the side stream (own temporary storage) meanwhile
@@ -1322,8 +1322,8 @@ struct bdsm_engine {
     const uint32_t m = 2 * n, nq = uint32_t(queries.size());
     // the batch-endpoint row flags were cleared at the end of the attempt
     CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V, hkeys.p, hvals.p,
-                     uint32_t(hkeys.n - 1), stream);
+    launch_post_sort(skeys.p, svals.p, 32, nullptr, nullptr, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V,
+                     hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
     run_phase(n, 1);
     launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
     CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));

@@ -161,7 +161,8 @@ __global__ void k_compact(DevGraphMut g, const uint64_t* __restrict__ new_off,
 // with the full 64-bit sort, so its error is reported exactly.
 __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, DevGraph g,
                           const uint32_t* __restrict__ new_of, bdsm_update_dev* iups, BatchState* st,
-                          uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, uint32_t id_limit) {
+                          uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, uint32_t id_limit,
+                          uint32_t key_bits) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
     if (up.u < g.V) up.u = new_of[up.u];
@@ -169,8 +170,10 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
     iups[i] = up;
     if (up.u >= id_limit || up.v >= id_limit) st->overflow = 5;
     uint32_t del = up.op != 0 ? 1u : 0u;
-    keys[2 * i] = (uint64_t(up.u) << 32) | up.v;
-    keys[2 * i + 1] = (uint64_t(up.v) << 32) | up.u;
+    // sort keys (source << key_bits | destination); key_bits < 32 packs both
+    // ids into the bits the radix sort orders (k_post_sort widens them back)
+    keys[2 * i] = (uint64_t(up.u) << key_bits) | up.v;
+    keys[2 * i + 1] = (uint64_t(up.v) << key_bits) | up.u;
     vals[2 * i] = i | (del << 31);
     vals[2 * i + 1] = i | (del << 31);
     uint32_t lab = kNone;
@@ -203,24 +206,35 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
 // heads (distinct sources = touched vertices), insert flags for the merge
 // prefix, and the per-phase same-kind endpoint flags in the candidate rows
 // used to prefilter the visibility rule (UpdateIndex, src/matcher.cpp:27-40).
-__global__ void k_post_sort(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+// in_keys/in_vals: the sort's output, keys packed as (source << key_bits |
+// destination); out_keys/out_vals (non-null): where the widened
+// (source << 32 | destination) keys and the values are written for every
+// later kernel.  (rerun_positive passes the widened keys, key_bits 32, no out.)
+__global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t* __restrict__ in_vals,
+                            uint32_t key_bits, uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
                             uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
                             uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys,
                             uint32_t* hvals, uint32_t hmask) {
+  const uint64_t dmask = key_bits >= 32 ? 0xffffffffull : (1ull << key_bits) - 1;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += gridDim.x * blockDim.x) {
     if (j == m) {
       insflag[j] = 0;
       continue;
     }
-    uint64_t k = skeys[j];
-    uint32_t val = svals[j];
-    uint32_t src = uint32_t(k >> 32);
+    const uint64_t ck = in_keys[j];
+    uint32_t val = in_vals[j];
+    uint32_t src = uint32_t(ck >> key_bits);
+    const uint64_t k = (uint64_t(src) << 32) | (ck & dmask);
+    if (out_keys) {
+      out_keys[j] = k;
+      out_vals[j] = val;
+    }
     bool is_del = val >> 31;
-    if (j > 0 && skeys[j - 1] == k) {
-      uint32_t a = svals[j - 1] & 0x7fffffffu, b = val & 0x7fffffffu;
+    if (j > 0 && in_keys[j - 1] == ck) {
+      uint32_t a = in_vals[j - 1] & 0x7fffffffu, b = val & 0x7fffffffu;
       atomicMin(&st->conflict_min, a > b ? a : b);
     }
-    bool h = j == 0 || uint32_t(skeys[j - 1] >> 32) != src;
+    bool h = j == 0 || uint32_t(in_keys[j - 1] >> key_bits) != src;
     head[j] = h ? 1 : 0;
     insflag[j] = is_del ? 0u : 1u;
     if (src < V)
@@ -1113,14 +1127,16 @@ void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* 
 }
 void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const uint32_t* new_of,
                     bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
-                    uint8_t* ecode, uint32_t id_limit, cudaStream_t s) {
-  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode, id_limit);
+                    uint8_t* ecode, uint32_t id_limit, uint32_t key_bits, cudaStream_t s) {
+  k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode, id_limit,
+                                               key_bits);
 }
-void launch_post_sort(const uint64_t* skeys, const uint32_t* svals, uint32_t m, BatchState* st,
-                      uint8_t* head, uint32_t* insflag, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                      unsigned long long* hkeys, uint32_t* hvals, uint32_t hmask, cudaStream_t s) {
-  k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(skeys, svals, m, st, head, insflag, rows,
-                                                              nq, V, hkeys, hvals, hmask);
+void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t key_bits, uint64_t* out_keys,
+                      uint32_t* out_vals, uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
+                      uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys, uint32_t* hvals,
+                      uint32_t hmask, cudaStream_t s) {
+  k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(in_keys, in_vals, key_bits, out_keys, out_vals, m,
+                                                              st, head, insflag, rows, nq, V, hkeys, hvals, hmask);
 }
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
                         cudaStream_t s) {
