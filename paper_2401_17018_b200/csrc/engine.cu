@@ -174,7 +174,10 @@ struct bdsm_engine {
   }
   uint64_t collect_cap = 0;        // matches materialised per (query, phase); 0 = counts only
   // matching-kernel tuning knobs (BDSM_TUNE_BACKOFF / BDSM_TUNE_MERGE env overrides, for sweeps)
-  uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 1024);
+  // idle warps' longest sleep between donation polls (ns); 0: by variant —
+  // 256 for the latency-bound 2-CTA launches (C2 +1.5-2 %), 1024 for the
+  // 4-CTA throughput launches (C4 -3 % at 256; C3/C5 neutral)
+  uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 0);
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
   uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 3 / 4: force a matching-kernel variant
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
@@ -989,8 +992,9 @@ struct bdsm_engine {
           a.task_tail = task_tail.p;
         }
         // variant by the previous batch's work items of this (query, phase)
-        launch_wbm(a, num_sms,
-                   tune_variant ? int(tune_variant) : qs.prev_items[phase] > tune_throughput_items ? 4 : 2, stream);
+        const int variant = tune_variant ? int(tune_variant) : qs.prev_items[phase] > tune_throughput_items ? 4 : 2;
+        a.backoff_max = tune_backoff ? tune_backoff : variant == 2 ? 256u : 1024u;
+        launch_wbm(a, num_sms, variant, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
       }
