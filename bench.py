@@ -146,6 +146,39 @@ def run_reference_binary(path: str, prefix: int, batches: int, time_cap: float, 
     return {"kind": kind, "cores": cores, "summary": summ[0], "batches": per, "wall_s": wall}
 
 
+def run_restatement_full(path: str, batches: int, timeout: float):
+    """Full-batch parity checker: the CPU restatement (oracle/oracle_bench,
+    pinned to the reference on tests/golden/ by counts and MatchStats) over the
+    first `batches` complete batches of a workload file, all host threads."""
+    exe = os.path.join(REPO, "oracle", "oracle_bench")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(REPO, "oracle")], check=False)
+    cores = os.cpu_count() or 1
+    cmd = [exe, path, "--threads", str(cores), "--batches", str(batches)]
+    log("full-batch parity:", " ".join(cmd))
+    t0 = time.time()
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        text = out.stdout
+    except subprocess.TimeoutExpired as e:
+        text = e.stdout.decode() if isinstance(e.stdout, bytes) else (e.stdout or "")
+    lines = [json.loads(l) for l in text.splitlines() if l.startswith("{")]
+    per = [l for l in lines if "batch" in l]
+    summ = [l for l in lines if l.get("summary")]
+    return {"batches": per, "summary": summ[0] if summ else None, "cores": cores, "wall_s": time.time() - t0}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -158,6 +191,9 @@ def main():
     ap.add_argument("--cpu-batches", type=int, default=3)
     ap.add_argument("--cpu-time-cap", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity-full", type=int, default=-1,
+                    help="batches checked against the CPU restatement at full size (-1: all; 0: off)")
+    ap.add_argument("--parity-timeout", type=float, default=600.0)
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--l2-hot-mb", type=int, default=0, help="K8 hot-list L2 persistence budget (0: off)")
     args = ap.parse_args()
@@ -413,15 +449,36 @@ def ours(args, world, rank, local):
         line["cpu_baseline"] = {"value": None, "unit": "updates/s", "cores": os.cpu_count(), "kind": "reference",
                                 "sample": "not run: the reference's graph build needs > 100 GB of host RAM at "
                                           f"{wl.meta['E']} edges (SURVEY.md §8(d))"}
-    elif world == 1 and not args.no_cpu_baseline:
+    tmp = None
+    if world == 1 and (args.parity_full != 0 or not args.no_cpu_baseline) and wl.meta["E"] <= 500_000_000:
         tmp = tempfile.mkdtemp(prefix="bdsm_cpu_")
         path = os.path.join(tmp, "workload.bin")
         W.write_file(wl, path)
+    if tmp and args.parity_full != 0:
+        # Full-scale parity: every batch of the run — warm-up
+        # and timed — at full size against the reference-pinned restatement;
+        # counts and the reference's dfs_visits must both match.
+        nchk = nb if args.parity_full < 0 else min(nb, args.parity_full)
+        res = run_restatement_full(path, nchk, args.parity_timeout)
+        ours_c = [(flatA[2 * i], flatA[2 * i + 1]) for i in range(nb)]
+        ours_v = [None] * args.warmup + [s["dfs_visits"] for s in statsA]
+        got = [(b["positive"], b["negative"]) for b in res["batches"]]
+        vis = [b["dfs_visits"] for b in res["batches"]]
+        eq_counts = got == ours_c[:len(got)]
+        eq_vis = all(v is None or v == r for v, r in zip(ours_v, vis))
+        line["parity_full"] = {
+            "checker": "oracle/oracle_bench: count-only CPU restatement of match_batch (coalesce off), pinned to "
+                       "the reference on tests/golden/ (counts, dfs_visits, intersection_ops, tasks_run)",
+            "batches": len(got), "batch_updates": wl.meta["batch"], "of": nb, "equal": bool(eq_counts and len(got) == nchk),
+            "counts_equal": eq_counts, "dfs_visits_equal": eq_vis,
+            "reference": got, "ours": ours_c[:len(got)], "dfs_visits_reference": vis,
+            "dfs_visits_ours": ours_v[:len(vis)], "cpu_s": res["summary"]["timed_s"] if res["summary"] else None,
+            "cores": res["cores"], "max_count": max([max(p) for p in got] or [0])}
+    if world == 1 and not args.no_cpu_baseline and tmp:
         res = run_reference_binary(path, args.cpu_prefix, args.cpu_batches, args.cpu_time_cap, timeout=600)
-        shutil.rmtree(tmp, ignore_errors=True)
         if res.get("batches"):
-            # Full-scale parity against the reference itself: replay the same
-            # sub-batch protocol (prefix counted, rest applied) on a fresh engine.
+            # The reference itself on its feasible sub-batches: replay the same
+            # protocol (prefix counted, rest applied) on a fresh engine.
             engC = bd.Engine(wl.labels, wl.src, wl.dst, device=local, chunk=args.chunk)
             engC.add_query(wl.qlabels, wl.qedges)
             ours_sub = []
@@ -440,6 +497,7 @@ def ours(args, world, rank, local):
             s = res["summary"]
             line["cpu_baseline"] = {
                 "value": s["updates_per_s"], "unit": "updates/s", "cores": res["cores"], "kind": res["kind"],
+                "cpu_model": cpu_model(),
                 "median_ms_per_subbatch": s["median_ms"],
                 "sample": f"first {args.cpu_prefix} updates of each of the first {s['batches']} batches of the "
                           f"same stream (rest applied untimed), {res['cores']} worker threads, "
@@ -448,6 +506,8 @@ def ours(args, world, rank, local):
         else:
             line["cpu_baseline"] = {"value": None, "unit": "updates/s", "cores": res.get("cores"),
                                     "kind": res.get("kind"), "sample": "failed", "error": res.get("error")}
+    if tmp:
+        shutil.rmtree(tmp, ignore_errors=True)
     print(json.dumps(line), flush=True)
     engA.close()
     engB.close()

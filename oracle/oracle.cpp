@@ -4,7 +4,12 @@
 #include "oracle.hpp"
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+#include <omp.h>
 #include <bit>
 #include <cstring>
 #include <stdexcept>
@@ -69,6 +74,25 @@ struct Query {
   }
 };
 
+// Per-phase memo of column(u) ∩ N(x) for long lists: the graph and the
+// candidate rows are fixed within a phase, so the filtered list is a function
+// of (x, u).  Lists live until the memo is reset at the next phase.
+struct ColListMemo {
+  std::vector<std::atomic<const std::vector<std::uint32_t>*>> cell;  // [V * n]
+  std::vector<std::unique_ptr<std::vector<std::uint32_t>>> owned;
+  std::mutex m;
+  std::uint32_t n = 0;
+  void reset(std::size_t V, std::uint32_t qn) {
+    if (n != qn || cell.size() != V * qn) {
+      n = qn;
+      cell = std::vector<std::atomic<const std::vector<std::uint32_t>*>>(V * qn);
+    } else if (!owned.empty()) {
+      for (auto& c : cell) c.store(nullptr, std::memory_order_relaxed);
+    }
+    owned.clear();
+  }
+};
+
 // Per-query filter state: encoding.cpp's scheme + per-vertex saturated
 // neighbour-label counters + CandidateTable rows and sorted columns.
 struct QState {
@@ -78,8 +102,9 @@ struct QState {
   std::vector<std::uint8_t> qcnt;           // [n][G]
   std::vector<std::uint8_t> vcnt;           // [V][G]
   std::vector<std::uint32_t> rows;          // [V]
-  std::vector<std::vector<std::uint32_t>> columns;
+  std::vector<std::uint64_t> colsize;       // |column(u)| (columns = rows' bits, encoding.hpp:95-97)
   std::vector<std::vector<std::uint32_t>> orders;  // per query edge
+  std::shared_ptr<ColListMemo> memo = std::make_shared<ColListMemo>();
 
   int group_index(std::uint32_t l) const {
     auto it = std::lower_bound(group_labels.begin(), group_labels.end(), l);
@@ -153,7 +178,7 @@ std::vector<std::uint32_t> matching_order(const QState& qs, std::uint32_t e) {
   std::uint32_t assigned = (1u << q.edges[e].a) | (1u << q.edges[e].b);
   std::uint32_t all = q.n == 32 ? ~0u : (1u << q.n) - 1;
   auto sel = [&](std::uint32_t u) {
-    return double(qs.columns[u].size()) / double(std::max<std::uint32_t>(q.degree[u], 1));
+    return double(qs.colsize[u]) / double(std::max<std::uint32_t>(q.degree[u], 1));
   };
   while ((assigned & all) != all) {
     int best = -1;
@@ -178,18 +203,16 @@ std::vector<std::uint32_t> matching_order(const QState& qs, std::uint32_t e) {
   return order;
 }
 
-// Reference intersect_sorted (matcher.cpp:59-73): binary-search each element
-// of the smaller list in the larger; counts the same intersection_ops.
-void intersect(const std::vector<std::uint32_t>& a, const std::vector<std::uint32_t>& b,
-               std::vector<std::uint32_t>& out, Stats& st) {
-  const auto& small = a.size() <= b.size() ? a : b;
-  const auto& large = a.size() <= b.size() ? b : a;
-  out.clear();
-  std::uint64_t probe = 1 + std::uint64_t(std::bit_width(large.size()));
-  st.iops += probe * small.size();
-  for (std::uint32_t x : small) {
-    if (std::binary_search(large.begin(), large.end(), x)) out.push_back(x);
-  }
+// Reference intersect_sorted (matcher.cpp:59-73) charges
+// size(small) * (1 + bit_width(size(large))) intersection_ops per call; the
+// set it returns is small ∩ large in ascending order.  The restatement
+// computes the same sets (the first, column-sided intersection by row-bit
+// filtering, since column(u) = {v : row[v] bit u}, encoding.hpp:95-97; the
+// rest by binary search) and charges the same ops from the operand sizes, so
+// intersection_ops stays equal to the reference's.
+inline std::uint64_t iops_of(std::uint64_t a, std::uint64_t b) {
+  std::uint64_t small = std::min(a, b), large = std::max(a, b);
+  return small * (1 + std::uint64_t(std::bit_width(large)));
 }
 
 // labeled_neighbors with oracle semantics (F4): unlabelled query edges accept
@@ -205,103 +228,370 @@ const std::vector<std::uint32_t>& labeled_neighbors(const Graph& g, std::uint32_
   return scratch;
 }
 
+// Same-kind updates of the phase incident to a vertex, for the visibility
+// rule on counted last levels: sorted (vertex << 32 | other, order).
+struct UpdAdj {
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> e;
+  template <typename F>
+  void for_each(std::uint32_t x, F&& f) const {
+    auto it = std::lower_bound(e.begin(), e.end(), std::make_pair(std::uint64_t(x) << 32, 0u));
+    for (; it != e.end() && (it->first >> 32) == x; ++it) f(std::uint32_t(it->first), it->second);
+  }
+};
+
 struct Ctx {
   const Graph& g;
   const QState& qs;
   const std::vector<Update>& ups;
   const std::unordered_map<std::uint64_t, std::uint32_t>& order_by_pair;  // UpdateIndex
+  const std::vector<std::uint8_t>& endpoint;  // v is an endpoint of a same-kind update
+  const UpdAdj& upd_adj;
+  ColListMemo& memo;
+  bool fast;  // no edge labels anywhere: neighbour lists are the adjacency itself
 };
 
-// gen_candidates (matcher.cpp:87-108).
-void gen_candidates(const Ctx& c, const std::vector<std::uint32_t>& order,
-                    const std::uint32_t* assign, std::size_t level,
-                    std::vector<std::uint32_t>& res, Stats& st) {
+// Lists at or above this length use the memoised column counts (first
+// intersection) and the counted last level; 0 forces them everywhere (tests).
+std::size_t memo_min() {
+  static const std::size_t v = [] {
+    const char* e = std::getenv("ORC_MEMO_MIN");
+    return e ? std::size_t(std::strtoull(e, nullptr, 10)) : std::size_t(512);
+  }();
+  return v;
+}
+
+const std::vector<std::uint32_t>& col_list(const Ctx& c, std::uint32_t x, std::uint32_t u) {
+  auto& cell = c.memo.cell[std::size_t(x) * c.memo.n + u];
+  if (const auto* p = cell.load(std::memory_order_acquire)) return *p;
+  const std::uint32_t ubit = 1u << u;
+  auto fresh = std::make_unique<std::vector<std::uint32_t>>();
+  for (std::uint32_t y : c.g.adj[x]) {
+    if (c.qs.rows[y] & ubit) fresh->push_back(y);
+  }
+  const std::vector<std::uint32_t>* expect = nullptr;
+  const std::vector<std::uint32_t>* mine = fresh.get();
+  if (cell.compare_exchange_strong(expect, mine, std::memory_order_acq_rel)) {
+    std::lock_guard<std::mutex> lk(c.memo.m);
+    c.memo.owned.push_back(std::move(fresh));
+    return *mine;
+  }
+  return *expect;
+}
+
+// Backward-neighbour lists of position `level` in ascending i.
+struct BackLists {
+  const std::vector<std::uint32_t>* l[32];
+  std::uint32_t who[32];
+  std::size_t m = 0;
+};
+
+void back_lists(const Ctx& c, const std::vector<std::uint32_t>& order, const std::uint32_t* assign,
+                std::size_t level, BackLists& bl, Stats& st) {
   const Query& q = c.qs.q;
-  std::uint32_t u = order[level];
-  ++st.calls;
+  const std::uint32_t u = order[level];
+  bl.m = 0;
+  for (std::size_t i = 0; i < level; ++i) {
+    if (!q.adjacent(order[i], u)) continue;
+    st.balg += 4ull * c.g.adj[assign[i]].size();
+    bl.l[bl.m] = &c.g.adj[assign[i]];
+    bl.who[bl.m++] = assign[i];
+  }
+}
+
+void erase_assigned(std::vector<std::uint32_t>& res, const std::uint32_t* assign, std::size_t level) {
+  if (res.empty()) return;
+  std::erase_if(res, [&](std::uint32_t v) {
+    for (std::size_t i = 0; i < level; ++i) {
+      if (assign[i] == v) return true;
+    }
+    return false;
+  });
+}
+
+// Sorted-set intersection small ∩ large (both ascending) by galloping from
+// the previous match position: the result equals the reference's binary
+// search of each element of the smaller list (matcher.cpp:59-73).
+template <typename Keep>
+void gallop_intersect(const std::vector<std::uint32_t>& small, const std::vector<std::uint32_t>& large,
+                      std::vector<std::uint32_t>& out, Keep&& keep) {
+  const std::uint32_t* lo = large.data();
+  const std::uint32_t* const end = lo + large.size();
+  for (std::uint32_t x : small) {
+    if (lo == end) break;
+    if (!keep(x)) continue;
+    std::size_t step = 1;
+    const std::uint32_t* hi = lo;
+    while (hi < end && *hi < x) {
+      lo = hi + 1;
+      hi = lo + step - 1 < end ? lo + step - 1 : end;
+      step <<= 1;
+    }
+    lo = std::lower_bound(lo, hi < end ? hi + 1 : end, x);
+    if (lo != end && *lo == x) out.push_back(x);
+  }
+}
+
+// gen_candidates (matcher.cpp:87-108), general form (edge labels): column(u)
+// ∩ N(M(π[i])) over the backward neighbours i < level in ascending i,
+// stopping once empty, then the already-assigned vertices removed.
+void gen_candidates_labelled(const Ctx& c, const std::vector<std::uint32_t>& order,
+                             const std::uint32_t* assign, std::size_t level,
+                             std::vector<std::uint32_t>& res, Stats& st) {
+  const Query& q = c.qs.q;
+  const std::uint32_t u = order[level];
+  const std::uint32_t ubit = 1u << u;
   for (std::size_t i = 0; i < level; ++i) {
     if (q.adjacent(order[i], u)) st.balg += 4ull * c.g.adj[assign[i]].size();
   }
-  const std::vector<std::uint32_t>* cur = &c.qs.columns[u];
+  static thread_local std::vector<std::uint32_t> scratch, tmp;
+  std::uint64_t cur = c.qs.colsize[u];
   bool own = false;
-  std::vector<std::uint32_t> scratch, tmp;
-  for (std::size_t i = 0; i < level && !cur->empty(); ++i) {
+  res.clear();
+  for (std::size_t i = 0; i < level && cur != 0; ++i) {
     std::uint32_t prev = order[i];
     if (!q.adjacent(prev, u)) continue;
     const auto& nbrs = labeled_neighbors(c.g, assign[i], q.edge_label(prev, u), scratch);
-    intersect(*cur, nbrs, tmp, st);
-    res.swap(tmp);
-    cur = &res;
-    own = true;
-  }
-  if (!own) res = *cur;
-  if (!res.empty()) {
-    std::erase_if(res, [&](std::uint32_t v) {
-      for (std::size_t i = 0; i < level; ++i) {
-        if (assign[i] == v) return true;
+    st.iops += iops_of(cur, nbrs.size());
+    if (!own) {
+      for (std::uint32_t x : nbrs) {
+        if (c.qs.rows[x] & ubit) res.push_back(x);
       }
-      return false;
-    });
+      own = true;
+    } else {
+      tmp.clear();
+      const bool res_small = res.size() <= nbrs.size();
+      const auto& small = res_small ? res : nbrs;
+      const auto& large = res_small ? nbrs : res;
+      for (std::uint32_t x : small) {
+        if (std::binary_search(large.begin(), large.end(), x)) tmp.push_back(x);
+      }
+      res.swap(tmp);
+    }
+    cur = res.size();
   }
+  if (!own && cur != 0) {  // no backward neighbour (unreachable for a prefix-connected order)
+    for (std::uint32_t v = 0; v < c.qs.rows.size(); ++v) {
+      if (c.qs.rows[v] & ubit) res.push_back(v);
+    }
+  }
+  erase_assigned(res, assign, level);
 }
 
-// dedupe_by_order (matcher.cpp:110-117) over the image by query vertex.
-bool dedupe(const Ctx& c, const std::uint32_t* image, std::uint32_t anchor_order) {
-  for (const QEdge& e : c.qs.q.edges) {
-    auto it = c.order_by_pair.find(pair_key(image[e.a], image[e.b]));
-    if (it != c.order_by_pair.end() && it->second < anchor_order) return false;
+// gen_candidates (matcher.cpp:87-108) without edge labels.  The reference
+// intersects column(u) with N_0, then the result with N_1, ... (ascending i);
+// the candidate set is the same whatever the order, so it is computed from
+// the shorter lists, while intersection_ops is charged on the reference's
+// sequence of operand sizes: |column(u)|, then |column ∩ N_0| (memoised for
+// long N_0), |column ∩ N_0 ∩ N_1|, ...
+void gen_candidates(const Ctx& c, const std::vector<std::uint32_t>& order,
+                    const std::uint32_t* assign, std::size_t level,
+                    std::vector<std::uint32_t>& res, Stats& st) {
+  ++st.calls;
+  if (!c.fast) {
+    gen_candidates_labelled(c, order, assign, level, res, st);
+    return;
   }
-  return true;
+  const std::uint32_t u = order[level];
+  const std::uint32_t ubit = 1u << u;
+  const auto& rows = c.qs.rows;
+  BackLists bl;
+  back_lists(c, order, assign, level, bl, st);
+  static thread_local std::vector<std::uint32_t> tmp;
+  res.clear();
+  std::uint64_t cur = c.qs.colsize[u];
+  if (bl.m == 0) {  // unreachable for a prefix-connected order
+    for (std::uint32_t v = 0; cur != 0 && v < rows.size(); ++v) {
+      if (rows[v] & ubit) res.push_back(v);
+    }
+    erase_assigned(res, assign, level);
+    return;
+  }
+  if (cur == 0) return;
+  const auto& n0 = *bl.l[0];
+  st.iops += iops_of(cur, n0.size());
+  std::size_t k = 1;
+  if (n0.size() >= memo_min()) {
+    // column ∩ N_0 from the memo
+    const auto& f = col_list(c, bl.who[0], u);
+    cur = f.size();
+    if (cur == 0) return;
+    if (bl.m >= 2) {  // ∩ N_1 from the shorter side
+      const auto& n1 = *bl.l[1];
+      st.iops += iops_of(cur, n1.size());
+      const bool f_small = f.size() <= n1.size();
+      const auto& small = f_small ? f : n1;
+      const auto& large = f_small ? n1 : f;
+      gallop_intersect(small, large, res, [&](std::uint32_t x) { return f_small || (rows[x] & ubit); });
+      k = 2;
+    } else {
+      res.assign(f.begin(), f.end());
+    }
+    cur = res.size();
+  } else {
+    for (std::uint32_t x : n0) {
+      if (rows[x] & ubit) res.push_back(x);
+    }
+    cur = res.size();
+  }
+  for (; k < bl.m && cur != 0; ++k) {
+    const auto& nk = *bl.l[k];
+    st.iops += iops_of(cur, nk.size());
+    tmp.clear();
+    const bool res_small = res.size() <= nk.size();
+    gallop_intersect(res_small ? res : nk, res_small ? nk : res, tmp, [](std::uint32_t) { return true; });
+    res.swap(tmp);
+    cur = res.size();
+  }
+  erase_assigned(res, assign, level);
 }
 
-// run_match_task (matcher.cpp:219-310) with workers = 1, no coalescing.
-std::uint64_t run_task(const Ctx& c, const Task& t, Stats& st) {
-  const Query& q = c.qs.q;
-  const Update& up = c.ups[t.upd];
-  const std::vector<std::uint32_t>& order = c.qs.orders[t.edge];
-  std::size_t n = order.size();
-  std::uint32_t assign[32];
-  std::uint32_t image[32];
-  assign[0] = t.flipped ? up.v : up.u;
-  assign[1] = t.flipped ? up.u : up.v;
-  ++st.tasks;
+// dedupe_by_order (matcher.cpp:110-117) for one query edge's image: rejected
+// iff the pair is a same-kind update of the batch with a lower order.  A pair
+// with an endpoint outside the batch cannot be in the UpdateIndex.
+inline bool edge_hidden(const Ctx& c, std::uint32_t x, std::uint32_t y, std::uint32_t anchor_order) {
+  if (!c.endpoint[x] || !c.endpoint[y]) return false;
+  auto it = c.order_by_pair.find(pair_key(x, y));
+  return it != c.order_by_pair.end() && it->second < anchor_order;
+}
+
+struct TaskRun {
+  const Ctx* c = nullptr;
+  const std::vector<std::uint32_t>* order = nullptr;
+  std::uint32_t anchor_order = 0;
+  std::size_t n = 0;
+  std::vector<std::uint32_t> pos_of;  // query vertex -> position in order
+};
+
+// Per-thread accumulators (padded against false sharing).
+struct alignas(64) ThreadAcc {
+  Stats st;
   std::uint64_t count = 0;
-  auto emit = [&]() {
-    for (std::size_t i = 0; i < n; ++i) image[order[i]] = assign[i];
-    if (dedupe(c, image, up.order)) {
-      ++count;
-      ++st.emitted;
-    }
-  };
-  if (n <= 2) {
-    emit();
-    return count;
+};
+
+// The final level of run_match_task (matcher.cpp:258-309): every candidate is
+// one dfs_visit and one emit_with_joins -> dedupe_by_order (matcher.cpp:169-217);
+// the edges not incident to the last position are the same for every
+// candidate, so they are checked once for the prefix.
+void count_last(const TaskRun& tr, const std::uint32_t* assign, const std::vector<std::uint32_t>& last,
+                Stats& st, std::uint64_t& count) {
+  const Ctx& c = *tr.c;
+  const Query& q = c.qs.q;
+  st.visits += last.size();
+  if (last.empty()) return;
+  const std::uint32_t ul = (*tr.order)[tr.n - 1];
+  for (const QEdge& e : q.edges) {
+    if (e.a == ul || e.b == ul) continue;
+    if (edge_hidden(c, assign[tr.pos_of[e.a]], assign[tr.pos_of[e.b]], tr.anchor_order)) return;
   }
-  std::vector<std::vector<std::uint32_t>> levels(n);
-  std::vector<std::size_t> cursor(n, 0);
-  gen_candidates(c, order, assign, 2, levels[2], st);
-  if (!t.whole) {  // shard restriction: level-2 values inside the owned driver range
-    std::erase_if(levels[2], [&](std::uint32_t v) { return v < t.lo || v > t.hi; });
-  }
-  std::size_t l = 2;
-  while (true) {
-    while (cursor[l] >= levels[l].size()) {
-      if (l == 2) return count;
-      --l;
+  std::uint64_t ok = 0;
+  for (std::uint32_t x : last) {
+    bool pass = true;
+    if (c.endpoint[x]) {
+      for (const QEdge& e : q.edges) {
+        if (e.a != ul && e.b != ul) continue;
+        std::uint32_t other = assign[tr.pos_of[e.a == ul ? e.b : e.a]];
+        if (edge_hidden(c, x, other, tr.anchor_order)) {
+          pass = false;
+          break;
+        }
+      }
     }
-    std::uint32_t cand = levels[l][cursor[l]++];
-    ++st.visits;
-    assign[l] = cand;
-    if (l + 1 == n) {
-      emit();
+    ok += pass;
+  }
+  st.emitted += ok;
+  count += ok;
+}
+
+// The last position L of the order: gen_candidates for L, then count_last.
+// With one backward neighbour x (every query edge of π[L] goes to it) and a
+// long N(x), the candidate set is column(u) ∩ N(x) minus the assigned
+// vertices, so its size is the memoised count minus the assigned vertices in
+// it, and the matches dedupe_by_order rejects are the candidates c whose edge
+// (x, c) is a same-kind update of lower order: they are enumerated from x's
+// updates instead of from N(x).  Same counts and MatchStats as the list path.
+void count_level_last(const TaskRun& tr, std::uint32_t* assign, std::size_t L, Stats& st,
+                      std::uint64_t& count) {
+  const Ctx& c = *tr.c;
+  const auto& order = *tr.order;
+  const std::uint32_t u = order[L];
+  const Query& q = c.qs.q;
+  if (c.fast && std::popcount(q.adjmask[u]) == 1) {
+    std::size_t i0 = 0;
+    while (!q.adjacent(order[i0], u)) ++i0;
+    const std::uint32_t x = assign[i0];
+    const auto& nx = c.g.adj[x];
+    if (nx.size() >= memo_min()) {
+      ++st.calls;
+      st.balg += 4ull * nx.size();
+      const std::uint64_t col = c.qs.colsize[u];
+      if (col == 0) return;
+      st.iops += iops_of(col, nx.size());
+      const std::uint32_t ubit = 1u << u;
+      std::uint64_t k = col_list(c, x, u).size();
+      for (std::size_t i = 0; i < L; ++i) {
+        std::uint32_t a = assign[i];
+        if ((c.qs.rows[a] & ubit) && std::binary_search(nx.begin(), nx.end(), a)) --k;
+      }
+      st.visits += k;
+      if (k == 0) return;
+      for (const QEdge& e : q.edges) {
+        if (e.a == u || e.b == u) continue;
+        if (edge_hidden(c, assign[tr.pos_of[e.a]], assign[tr.pos_of[e.b]], tr.anchor_order)) return;
+      }
+      std::uint64_t hidden = 0;
+      c.upd_adj.for_each(x, [&](std::uint32_t y, std::uint32_t ord) {
+        if (ord >= tr.anchor_order || !(c.qs.rows[y] & ubit)) return;
+        for (std::size_t i = 0; i < L; ++i) {
+          if (assign[i] == y) return;
+        }
+        ++hidden;
+      });
+      st.emitted += k - hidden;
+      count += k - hidden;
+      return;
+    }
+  }
+  static thread_local std::vector<std::uint32_t> last;
+  gen_candidates(c, order, assign, L, last, st);
+  count_last(tr, assign, last, st, count);
+}
+
+// The DFS below `level` over that level's candidates.  The subtrees of the two
+// shallowest levels run as separate OpenMP tasks, so a hub-anchored task
+// spreads over the threads (the results are sums).
+void dfs(const TaskRun& tr, std::uint32_t* assign, std::size_t level, const std::uint32_t* cands,
+         std::size_t ncands, ThreadAcc* acc) {
+  const std::size_t n = tr.n;
+  const bool spawn = level + 2 < n && ncands > 1 && (level == 2 || (level == 3 && ncands > 64));
+  if (spawn) {
+    const std::size_t grain = level == 2 ? 1 : 16;
+    for (std::size_t b = 0; b < ncands; b += grain) {
+      std::size_t e = std::min(ncands, b + grain);
+      std::array<std::uint32_t, 32> a{};
+      std::copy(assign, assign + level, a.begin());
+      std::vector<std::uint32_t> part(cands + b, cands + e);
+#pragma omp task firstprivate(a, part, level) shared(tr) untied
+      dfs(tr, a.data(), level, part.data(), part.size(), acc);
+    }
+    return;
+  }
+  std::vector<std::uint32_t> next;
+  for (std::size_t k = 0; k < ncands; ++k) {
+    ThreadAcc& me = acc[omp_get_thread_num()];
+    assign[level] = cands[k];
+    ++me.st.visits;
+    if (level + 2 == n) {
+      count_level_last(tr, assign, level + 1, me.st, me.count);
       continue;
     }
-    gen_candidates(c, order, assign, l + 1, levels[l + 1], st);
-    if (levels[l + 1].empty()) continue;
-    cursor[l + 1] = 0;
-    ++l;
+    gen_candidates(*tr.c, *tr.order, assign, level + 1, next, me.st);
+    if (!next.empty()) {
+      std::vector<std::uint32_t> mine;
+      mine.swap(next);
+      dfs(tr, assign, level + 1, mine.data(), mine.size(), acc);
+      next.swap(mine);
+    }
   }
-  (void)q;
 }
 
 // Level-2 driver of a task: the smallest-degree backward neighbour of
@@ -316,14 +606,58 @@ std::uint32_t driver_vertex(const Graph& g, const QState& qs, const Task& t, con
   return b0 ? a0 : a1;
 }
 
+// run_match_task (matcher.cpp:219-310) for one anchor task, coalesce off:
+// level-2 candidates (matcher.cpp:243-247), then the DFS.
+void run_task(const Ctx& c, const Task& t, TaskRun& tr, ThreadAcc* acc) {
+  const Update& up = c.ups[t.upd];
+  const std::vector<std::uint32_t>& order = c.qs.orders[t.edge];
+  const std::size_t n = order.size();
+  tr.c = &c;
+  tr.order = &order;
+  tr.anchor_order = up.order;
+  tr.n = n;
+  tr.pos_of.assign(c.qs.q.n, 0);
+  for (std::size_t i = 0; i < n; ++i) tr.pos_of[order[i]] = std::uint32_t(i);
+  ThreadAcc& me = acc[omp_get_thread_num()];
+  ++me.st.tasks;
+  std::array<std::uint32_t, 32> assign{};
+  assign[0] = t.flipped ? up.v : up.u;
+  assign[1] = t.flipped ? up.u : up.v;
+  if (n <= 2) {
+    // a 2-vertex query's only match is the anchor itself (emit at matcher.cpp:237-241)
+    bool hidden = false;
+    for (const QEdge& e : c.qs.q.edges) {
+      hidden = hidden || edge_hidden(c, assign[tr.pos_of[e.a]], assign[tr.pos_of[e.b]], tr.anchor_order);
+    }
+    if (!hidden) {
+      ++me.count;
+      ++me.st.emitted;
+    }
+    return;
+  }
+  std::vector<std::uint32_t> l2;
+  gen_candidates(c, order, assign.data(), 2, l2, me.st);
+  if (!t.whole) {  // shard restriction: level-2 values inside the owned driver range
+    std::erase_if(l2, [&](std::uint32_t v) { return v < t.lo || v > t.hi; });
+  }
+  if (n == 3) {
+    count_last(tr, assign.data(), l2, me.st, me.count);
+    return;
+  }
+  dfs(tr, assign.data(), 2, l2.data(), l2.size(), acc);
+}
+
 std::uint64_t run_phase(orc_engine* h, QState& qs, const std::vector<Update>& ups, bool inserts,
                         std::uint32_t nthreads, std::uint32_t rank, std::uint32_t world,
                         Stats& total) {
   const Graph& g = h->g;
   const Query& q = qs.q;
   std::unordered_map<std::uint64_t, std::uint32_t> order_by_pair;  // UpdateIndex::build
+  std::vector<std::uint8_t> endpoint(g.labels.size(), 0);
   for (const Update& up : ups) {
-    if (up.insert == inserts) order_by_pair.emplace(pair_key(up.u, up.v), up.order);
+    if (up.insert != inserts) continue;
+    order_by_pair.emplace(pair_key(up.u, up.v), up.order);
+    endpoint[up.u] = endpoint[up.v] = 1;
   }
   // match_phase task construction (matcher.cpp:334-354).
   std::vector<Task> tasks;
@@ -381,24 +715,32 @@ std::uint64_t run_phase(orc_engine* h, QState& qs, const std::vector<Update>& up
     }
     tasks.swap(mine);
   }
-  Ctx ctx{g, qs, ups, order_by_pair};
-  std::atomic<std::size_t> next{0};
-  std::atomic<std::uint64_t> count{0};
-  std::vector<Stats> per(std::max(1u, nthreads));
-  auto worker = [&](std::size_t w) {
-    std::uint64_t local = 0;
-    for (std::size_t i; (i = next.fetch_add(1)) < tasks.size();) local += run_task(ctx, tasks[i], per[w]);
-    count += local;
-  };
-  if (nthreads <= 1 || tasks.size() < 2) {
-    worker(0);
-  } else {
-    std::vector<std::thread> th;
-    for (std::size_t w = 0; w < nthreads; ++w) th.emplace_back(worker, w);
-    for (auto& t : th) t.join();
+  UpdAdj upd_adj;
+  for (const Update& up : ups) {
+    if (up.insert != inserts) continue;
+    upd_adj.e.push_back({(std::uint64_t(up.u) << 32) | up.v, up.order});
+    upd_adj.e.push_back({(std::uint64_t(up.v) << 32) | up.u, up.order});
   }
-  for (auto& s : per) total.add(s);
-  return count.load();
+  std::sort(upd_adj.e.begin(), upd_adj.e.end());
+  bool fast = g.elab.empty();
+  for (const QEdge& e : q.edges) fast = fast && e.label == kNone;
+  qs.memo->reset(g.labels.size(), q.n);
+  Ctx ctx{g, qs, ups, order_by_pair, endpoint, upd_adj, *qs.memo, fast};
+  const std::uint32_t nt = std::max(1u, nthreads);
+  std::vector<ThreadAcc> acc(nt);
+  std::vector<TaskRun> runs(tasks.size());
+#pragma omp parallel num_threads(nt)
+#pragma omp single
+  for (std::size_t i = 0; i < tasks.size(); ++i) {
+#pragma omp task firstprivate(i) shared(ctx, tasks, runs, acc) untied
+    run_task(ctx, tasks[i], runs[i], acc.data());
+  }
+  std::uint64_t count = 0;
+  for (auto& a : acc) {
+    total.add(a.st);
+    count += a.count;
+  }
+  return count;
 }
 
 void insert_sorted(std::vector<std::uint32_t>& v, std::uint32_t x) {
@@ -423,24 +765,48 @@ orc_engine* orc_create(std::uint32_t nv, const std::uint32_t* vlabels, std::uint
     Graph& g = h->g;
     g.labels.assign(vlabels, vlabels + nv);
     g.adj.assign(nv, {});
-    std::vector<std::uint64_t> keys;
-    keys.reserve(2 * ne);
-    for (std::uint64_t i = 0; i < ne; ++i) {  // graph.cpp:52-68
-      std::uint32_t u = eu[i], v = ev[i];
-      if (u == v) throw std::invalid_argument("self-loop edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
-      if (u >= nv || v >= nv) throw std::invalid_argument("edge references unknown vertex");
-      keys.push_back((std::uint64_t(u) << 32) | v);
-      keys.push_back((std::uint64_t(v) << 32) | u);
-      if (elab && elab[i] != kNone) g.elab[pair_key(u, v)] = elab[i];
+    // graph.cpp:52-68 (self-loops, unknown vertices and duplicates rejected),
+    // built in parallel: degree count, fill, per-list sort
+    std::uint64_t first_bad = ne;
+#pragma omp parallel for reduction(min : first_bad) schedule(static)
+    for (std::uint64_t i = 0; i < ne; ++i) {
+      if (eu[i] == ev[i] || eu[i] >= nv || ev[i] >= nv) first_bad = std::min(first_bad, i);
     }
-    std::sort(keys.begin(), keys.end());
-    for (std::size_t i = 1; i < keys.size(); ++i) {
-      if (keys[i] == keys[i - 1]) throw std::invalid_argument("duplicate edge");
+    if (first_bad < ne) {
+      std::uint32_t u = eu[first_bad], v = ev[first_bad];
+      if (u == v) throw std::invalid_argument("self-loop edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
+      throw std::invalid_argument("edge references unknown vertex");
+    }
+    if (elab) {
+      for (std::uint64_t i = 0; i < ne; ++i) {
+        if (elab[i] != kNone) g.elab[pair_key(eu[i], ev[i])] = elab[i];
+      }
     }
     std::vector<std::uint64_t> deg(nv, 0);
-    for (auto k : keys) ++deg[k >> 32];
-    for (std::uint32_t v = 0; v < nv; ++v) g.adj[v].reserve(deg[v]);
-    for (auto k : keys) g.adj[k >> 32].push_back(std::uint32_t(k));
+#pragma omp parallel for schedule(static)
+    for (std::uint64_t i = 0; i < ne; ++i) {
+      std::atomic_ref<std::uint64_t>(deg[eu[i]]).fetch_add(1, std::memory_order_relaxed);
+      std::atomic_ref<std::uint64_t>(deg[ev[i]]).fetch_add(1, std::memory_order_relaxed);
+    }
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (std::uint64_t v = 0; v < nv; ++v) {
+      g.adj[v].resize(deg[v]);
+      deg[v] = 0;
+    }
+#pragma omp parallel for schedule(static)
+    for (std::uint64_t i = 0; i < ne; ++i) {
+      std::uint32_t u = eu[i], v = ev[i];
+      g.adj[u][std::atomic_ref<std::uint64_t>(deg[u]).fetch_add(1, std::memory_order_relaxed)] = v;
+      g.adj[v][std::atomic_ref<std::uint64_t>(deg[v]).fetch_add(1, std::memory_order_relaxed)] = u;
+    }
+    int dup = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(| : dup)
+    for (std::uint64_t v = 0; v < nv; ++v) {
+      auto& a = g.adj[v];
+      std::sort(a.begin(), a.end());
+      for (std::size_t i = 1; i < a.size(); ++i) dup |= a[i] == a[i - 1];
+    }
+    if (dup) throw std::invalid_argument("duplicate edge");
     return h;
   } catch (const std::exception& e) {
     set_err(err, errcap, e.what());
@@ -501,13 +867,14 @@ int orc_add_query(orc_engine* h, std::uint32_t n, const std::uint32_t* qlabels, 
     std::size_t V = g.labels.size();
     qs.vcnt.assign(V * G, 0);
     qs.rows.assign(V, 0);
-    qs.columns.assign(n, {});
-    for (std::uint32_t v = 0; v < V; ++v) {
-      qs.encode_vertex(g, v, &qs.vcnt[std::size_t(v) * G]);
-      qs.rows[v] = qs.compute_row(g, v);
-      for (std::uint32_t u = 0; u < n; ++u) {
-        if ((qs.rows[v] >> u) & 1u) qs.columns[u].push_back(v);
-      }
+    qs.colsize.assign(n, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (std::size_t v = 0; v < V; ++v) {
+      qs.encode_vertex(g, std::uint32_t(v), &qs.vcnt[v * G]);
+      qs.rows[v] = qs.compute_row(g, std::uint32_t(v));
+    }
+    for (std::size_t v = 0; v < V; ++v) {
+      for (std::uint32_t r = qs.rows[v]; r; r &= r - 1) ++qs.colsize[std::countr_zero(r)];
     }
     for (std::uint32_t e = 0; e < m; ++e) qs.orders.push_back(matching_order(qs, e));
     h->queries.push_back(std::move(qs));
@@ -598,8 +965,8 @@ int orc_apply_batch(orc_engine* h, std::uint64_t n, const std::uint32_t* uu,
         if (before == after) continue;
         qs.rows[v] = after;
         for (std::uint32_t u = 0; u < qs.q.n; ++u) {
-          if (((after & ~before) >> u) & 1u) insert_sorted(qs.columns[u], v);
-          else if (((before & ~after) >> u) & 1u) erase_sorted(qs.columns[u], v);
+          if (((after & ~before) >> u) & 1u) ++qs.colsize[u];
+          else if (((before & ~after) >> u) & 1u) --qs.colsize[u];
         }
       }
     }
