@@ -463,7 +463,8 @@ def ours(args, world, rank, local):
         ours_c = [(flatA[2 * i], flatA[2 * i + 1]) for i in range(nb)]
         ours_v = [None] * args.warmup + [s["dfs_visits"] for s in statsA]
         got = [(b["positive"], b["negative"]) for b in res["batches"]]
-        vis = [b["dfs_visits"] for b in res["batches"]]
+        vis = [b["dfs_visits_pruned"] for b in res["batches"]]
+        vis_ref = [b["dfs_visits"] for b in res["batches"]]
         eq_counts = got == ours_c[:len(got)]
         eq_vis = all(v is None or v == r for v, r in zip(ours_v, vis))
         line["parity_full"] = {
@@ -471,8 +472,11 @@ def ours(args, world, rank, local):
                        "the reference on tests/golden/ (counts, dfs_visits, intersection_ops, tasks_run)",
             "batches": len(got), "batch_updates": wl.meta["batch"], "of": nb, "equal": bool(eq_counts and len(got) == nchk),
             "counts_equal": eq_counts, "dfs_visits_equal": eq_vis,
-            "reference": got, "ours": ours_c[:len(got)], "dfs_visits_reference": vis,
-            "dfs_visits_ours": ours_v[:len(vis)], "cpu_s": res["summary"]["timed_s"] if res["summary"] else None,
+            "dfs_visits_note": "the engine applies dedupe_by_order at candidate generation, so its dfs_visits is "
+                               "the reference tree's minus the subtrees that rule prunes; compared with the "
+                               "restatement's count of exactly that tree (dfs_visits_pruned)",
+            "reference": got, "ours": ours_c[:len(got)], "dfs_visits_pruned_reference": vis,
+            "dfs_visits_reference_tree": vis_ref, "dfs_visits_ours": ours_v[:len(vis)], "cpu_s": res["summary"]["timed_s"] if res["summary"] else None,
             "cores": res["cores"], "max_count": max([max(p) for p in got] or [0])}
     if world == 1 and not args.no_cpu_baseline and tmp:
         res = run_reference_binary(path, args.cpu_prefix, args.cpu_batches, args.cpu_time_cap, timeout=600)

@@ -56,7 +56,8 @@ typedef struct bdsm_graph_desc {
 
 /* Query: replaces QueryGraph(labels, edges) (include/bdsm/query_graph.hpp:24). */
 typedef struct bdsm_query_desc {
-  uint32_t num_vertices;         /* <= 32 (reference limit); connected */
+  uint32_t num_vertices;         /* <= 16 on the GPU engine (the reference allows 32,
+                                    src/query_graph.cpp:14); connected */
   const uint32_t* vertex_labels;
   uint32_t num_edges;
   const uint32_t* a;
@@ -109,7 +110,8 @@ typedef struct bdsm_batch_stats {
   uint64_t touched;       /* distinct batch endpoints */
   uint64_t relocations;   /* adjacency lists moved to the append pool */
   uint32_t compactions;   /* pool compactions triggered by this batch */
-  uint32_t timed_out;     /* bitmask of queries whose deadline passed (counts dropped) */
+  uint32_t timed_out;     /* bitmask of queries 0..31 whose deadline passed in this batch (counts
+                             dropped); any query: bdsm_engine_query_timed_out */
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
   double ms_match_kernel;  /* CUDA-event time of the K6 matching kernels (both phases) */
@@ -129,7 +131,9 @@ BDSM_API void bdsm_engine_destroy(bdsm_engine* engine);
 
 /* Registers a query: QueryEncodingState::initialize (src/matcher.cpp:10-18) +
  * build_query_plan with coalescing off (src/query_analysis.cpp:358-363,
- * :437-441).  Returns the query index (>= 0) or -status. */
+ * :437-441).  Returns the query index (>= 0) or -status.  Up to 256 queries
+ * per engine (run_pipeline's query set, src/bench.cpp:370-479); each batch
+ * reports one count per query. */
 BDSM_API int bdsm_engine_add_query(bdsm_engine* engine, const bdsm_query_desc* query);
 
 /* match_batch (src/matcher.cpp:370-389) over every registered query: validate,
@@ -159,6 +163,17 @@ BDSM_API bdsm_status bdsm_engine_wait(bdsm_engine* engine, uint64_t* pos, uint64
 /* Per-query time budget in seconds for subsequent batches (MatchOptions::
  * deadline, PipelineConfig::timeout_seconds); <= 0 disables. */
 BDSM_API bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seconds_from_now);
+
+/* Whether `query` is matched by later batches (default 1).  run_pipeline
+ * stops matching a query once it is unsolved (src/bench.cpp:420-432, :463-467);
+ * an inactive query reports 0/0. */
+BDSM_API bdsm_status bdsm_engine_set_query_active(bdsm_engine* engine, int query, int active);
+
+/* 1 if the deadline of `query` fired during the last batch (its counts of
+ * that batch were dropped, MatchStats::timed_out), 0 if not, -status on a bad
+ * index.  A deadline applies per batch; the engine keeps matching the query
+ * in later batches until the caller deactivates it. */
+BDSM_API int bdsm_engine_query_timed_out(bdsm_engine* engine, int query);
 
 /* After BDSM_BATCH_ERROR: the failures in batch order (BatchError::failures).
  * Returns the total number of failures. */

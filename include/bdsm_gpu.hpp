@@ -150,6 +150,14 @@ class Engine {
   void set_deadline(int query, double seconds_from_now) {
     check(bdsm_engine_set_deadline(e_, query, seconds_from_now));
   }
+  // run_pipeline drops an unsolved query from later batches (src/bench.cpp:420-432)
+  void set_query_active(int query, bool active) { check(bdsm_engine_set_query_active(e_, query, active ? 1 : 0)); }
+  // MatchStats::timed_out of `query` in the last batch (its counts were dropped)
+  bool query_timed_out(int query) {
+    const int r = bdsm_engine_query_timed_out(e_, query);
+    if (r < 0) check(bdsm_status(-r));
+    return r != 0;
+  }
   void replan(int query) { check(bdsm_engine_replan(e_, query)); }
   std::vector<std::uint64_t> column_sizes(int query, std::uint32_t n) {
     std::vector<std::uint64_t> out(32);
@@ -158,12 +166,19 @@ class Engine {
     return out;
   }
   // Bounded match materialisation for later batches (0: counts only).
-  void collect_matches(std::uint64_t cap) { check(bdsm_engine_collect_matches(e_, cap)); }
+  void collect_matches(std::uint64_t cap) {
+    check(bdsm_engine_collect_matches(e_, cap));
+    collect_cap_ = cap;
+  }
   // Matches of the last batch for (query, phase 0 negative / 1 positive),
-  // flattened num_vertices words each, sorted; throws when they were truncated.
+  // flattened num_vertices words each, sorted; throws std::length_error when
+  // more matches exist than the engine collected (raise the cap).
   std::vector<std::uint32_t> matches(int query, int phase, std::uint32_t num_vertices) {
     std::int64_t total = bdsm_engine_matches(e_, query, phase, nullptr, 0);
     if (total < 0) check(bdsm_status(-total));
+    if (std::uint64_t(total) > collect_cap_)
+      throw std::length_error(std::to_string(total) + " matches, only " + std::to_string(collect_cap_) +
+                              " collected (raise the collect_matches cap)");
     std::vector<std::uint32_t> out(std::size_t(total) * num_vertices);
     std::int64_t again = bdsm_engine_matches(e_, query, phase, out.data(), std::size_t(total));
     if (again < 0) check(bdsm_status(-again));
@@ -204,6 +219,7 @@ class Engine {
   }
   bdsm_engine* e_ = nullptr;
   std::size_t nq_ = 0;
+  std::uint64_t collect_cap_ = 0;
 };
 
 }  // namespace bdsm::gpu

@@ -142,8 +142,13 @@ struct Update {
 
 struct Stats {
   std::uint64_t visits = 0, iops = 0, tasks = 0, calls = 0, balg = 0, emitted = 0;
+  // visits outside the subtrees of candidates whose edge to an earlier
+  // position is hidden by dedupe_by_order: the tree the CUDA engine walks
+  // (it applies the rule when it generates candidates, not when it emits)
+  std::uint64_t vpruned = 0;
   void add(const Stats& o) {
     visits += o.visits;
+    vpruned += o.vpruned;
     iops += o.iops;
     tasks += o.tasks;
     calls += o.calls;
@@ -473,7 +478,7 @@ struct alignas(64) ThreadAcc {
 // the edges not incident to the last position are the same for every
 // candidate, so they are checked once for the prefix.
 void count_last(const TaskRun& tr, const std::uint32_t* assign, const std::vector<std::uint32_t>& last,
-                Stats& st, std::uint64_t& count) {
+                Stats& st, std::uint64_t& count, bool pruned) {
   const Ctx& c = *tr.c;
   const Query& q = c.qs.q;
   st.visits += last.size();
@@ -500,6 +505,7 @@ void count_last(const TaskRun& tr, const std::uint32_t* assign, const std::vecto
   }
   st.emitted += ok;
   count += ok;
+  if (!pruned) st.vpruned += ok;
 }
 
 // The last position L of the order: gen_candidates for L, then count_last.
@@ -510,7 +516,7 @@ void count_last(const TaskRun& tr, const std::uint32_t* assign, const std::vecto
 // (x, c) is a same-kind update of lower order: they are enumerated from x's
 // updates instead of from N(x).  Same counts and MatchStats as the list path.
 void count_level_last(const TaskRun& tr, std::uint32_t* assign, std::size_t L, Stats& st,
-                      std::uint64_t& count) {
+                      std::uint64_t& count, bool pruned) {
   const Ctx& c = *tr.c;
   const auto& order = *tr.order;
   const std::uint32_t u = order[L];
@@ -548,19 +554,32 @@ void count_level_last(const TaskRun& tr, std::uint32_t* assign, std::size_t L, S
       });
       st.emitted += k - hidden;
       count += k - hidden;
+      if (!pruned) st.vpruned += k - hidden;
       return;
     }
   }
   static thread_local std::vector<std::uint32_t> last;
   gen_candidates(c, order, assign, L, last, st);
-  count_last(tr, assign, last, st, count);
+  count_last(tr, assign, last, st, count, pruned);
+}
+
+// Some query edge from an earlier position to position `level` maps onto a
+// hidden pair (dedupe_by_order would reject every match below).
+bool back_hidden(const TaskRun& tr, const std::uint32_t* assign, std::size_t level, std::uint32_t cand) {
+  const Ctx& c = *tr.c;
+  if (!c.endpoint[cand]) return false;
+  const std::uint32_t u = (*tr.order)[level];
+  for (std::size_t i = 0; i < level; ++i) {
+    if (c.qs.q.adjacent((*tr.order)[i], u) && edge_hidden(c, assign[i], cand, tr.anchor_order)) return true;
+  }
+  return false;
 }
 
 // The DFS below `level` over that level's candidates.  The subtrees of the two
 // shallowest levels run as separate OpenMP tasks, so a hub-anchored task
 // spreads over the threads (the results are sums).
 void dfs(const TaskRun& tr, std::uint32_t* assign, std::size_t level, const std::uint32_t* cands,
-         std::size_t ncands, ThreadAcc* acc) {
+         std::size_t ncands, ThreadAcc* acc, bool pruned) {
   const std::size_t n = tr.n;
   const bool spawn = level + 2 < n && ncands > 1 && (level == 2 || (level == 3 && ncands > 64));
   if (spawn) {
@@ -570,8 +589,8 @@ void dfs(const TaskRun& tr, std::uint32_t* assign, std::size_t level, const std:
       std::array<std::uint32_t, 32> a{};
       std::copy(assign, assign + level, a.begin());
       std::vector<std::uint32_t> part(cands + b, cands + e);
-#pragma omp task firstprivate(a, part, level) shared(tr) untied
-      dfs(tr, a.data(), level, part.data(), part.size(), acc);
+#pragma omp task firstprivate(a, part, level, pruned) shared(tr) untied
+      dfs(tr, a.data(), level, part.data(), part.size(), acc, pruned);
     }
     return;
   }
@@ -580,15 +599,17 @@ void dfs(const TaskRun& tr, std::uint32_t* assign, std::size_t level, const std:
     ThreadAcc& me = acc[omp_get_thread_num()];
     assign[level] = cands[k];
     ++me.st.visits;
+    const bool hid = pruned || back_hidden(tr, assign, level, cands[k]);
+    if (!hid) ++me.st.vpruned;
     if (level + 2 == n) {
-      count_level_last(tr, assign, level + 1, me.st, me.count);
+      count_level_last(tr, assign, level + 1, me.st, me.count, hid);
       continue;
     }
     gen_candidates(*tr.c, *tr.order, assign, level + 1, next, me.st);
     if (!next.empty()) {
       std::vector<std::uint32_t> mine;
       mine.swap(next);
-      dfs(tr, assign, level + 1, mine.data(), mine.size(), acc);
+      dfs(tr, assign, level + 1, mine.data(), mine.size(), acc, hid);
       next.swap(mine);
     }
   }
@@ -641,10 +662,10 @@ void run_task(const Ctx& c, const Task& t, TaskRun& tr, ThreadAcc* acc) {
     std::erase_if(l2, [&](std::uint32_t v) { return v < t.lo || v > t.hi; });
   }
   if (n == 3) {
-    count_last(tr, assign.data(), l2, me.st, me.count);
+    count_last(tr, assign.data(), l2, me.st, me.count, false);
     return;
   }
-  dfs(tr, assign.data(), 2, l2.data(), l2.size(), acc);
+  dfs(tr, assign.data(), 2, l2.data(), l2.size(), acc, false);
 }
 
 std::uint64_t run_phase(orc_engine* h, QState& qs, const std::vector<Update>& ups, bool inserts,
@@ -980,6 +1001,7 @@ int orc_apply_batch(orc_engine* h, std::uint64_t n, const std::uint32_t* uu,
       stats[3] = st.calls;
       stats[4] = st.balg;
       stats[5] = bupd;
+      stats[6] = st.vpruned;
     }
     return ORC_OK;
   } catch (const std::exception& e) {

@@ -42,7 +42,9 @@ enum {
 //   [0] dfs_visits  [1] intersection_ops  [2] tasks_run  [3] gen_candidates calls
 //   [4] algorithmic adjacency bytes of the phases (SURVEY.md §8(d) B_phase)
 //   [5] algorithmic bytes of the graph update (B_upd)
-enum { ORC_NSTATS = 6 };
+//   [6] dfs_visits outside the subtrees the visibility rule prunes (the tree
+//       the CUDA engine walks: it applies dedupe_by_order at generation time)
+enum { ORC_NSTATS = 7 };
 
 orc_engine* orc_create(std::uint32_t nv, const std::uint32_t* vlabels, std::uint64_t ne,
                        const std::uint32_t* eu, const std::uint32_t* ev,

@@ -77,11 +77,11 @@ int main(int argc, char** argv) {
     std::printf(
         "{\"batch\": %llu, \"updates\": %llu, \"positive\": %llu, \"negative\": %llu, \"ms\": %.3f, "
         "\"dfs_visits\": %llu, \"intersection_ops\": %llu, \"tasks\": %llu, \"calls\": %llu, "
-        "\"b_phase\": %llu, \"b_upd\": %llu}\n",
+        "\"b_phase\": %llu, \"b_upd\": %llu, \"dfs_visits_pruned\": %llu}\n",
         (unsigned long long)b, (unsigned long long)(cut - lo), (unsigned long long)pos,
         (unsigned long long)neg, s * 1e3, (unsigned long long)st[0], (unsigned long long)st[1],
         (unsigned long long)st[2], (unsigned long long)st[3], (unsigned long long)st[4],
-        (unsigned long long)st[5]);
+        (unsigned long long)st[5], (unsigned long long)st[6]);
     std::fflush(stdout);
     if (cut < hi) {
       rc = orc_apply_batch(h, hi - cut, &w.uu[cut], &w.uv[cut], &ops[cut], &w.ulab[cut], threads, 0, 1,

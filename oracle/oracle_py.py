@@ -111,7 +111,7 @@ class Oracle:
     def apply_batch(self, updates, nthreads: int = 1, rank: int = 0, world: int = 1,
                     match: bool = True):
         """updates: iterable of (op, u, v[, label]) with op 0 insert / 1 delete.
-        Returns (pos[nq], neg[nq], stats[6])."""
+        Returns (pos[nq], neg[nq], stats[7])."""
         ups = list(updates)
         uop = _arr([u[0] for u in ups], np.uint8)
         uu = _arr([u[1] for u in ups])
@@ -119,7 +119,7 @@ class Oracle:
         ul = _arr([NONE if (len(u) < 4 or u[3] is None or u[3] < 0) else u[3] for u in ups])
         pos = np.zeros(max(1, self.nq), np.uint64)
         neg = np.zeros(max(1, self.nq), np.uint64)
-        st = np.zeros(6, np.uint64)
+        st = np.zeros(7, np.uint64)
         err = C.create_string_buffer(512)
         r = lib().orc_apply_batch(self.h, len(ups), uu, uv, uop, _opt_ptr(ul), nthreads, rank, world,
                                   _opt_ptr(pos) if match else None, _opt_ptr(neg) if match else None,

@@ -101,6 +101,10 @@ def _load():
     L.bdsm_engine_wait.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
     L.bdsm_engine_set_deadline.restype = C.c_int
     L.bdsm_engine_set_deadline.argtypes = [C.c_void_p, C.c_int, C.c_double]
+    L.bdsm_engine_set_query_active.restype = C.c_int
+    L.bdsm_engine_set_query_active.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.bdsm_engine_query_timed_out.restype = C.c_int
+    L.bdsm_engine_query_timed_out.argtypes = [C.c_void_p, C.c_int]
     L.bdsm_last_batch_errors.restype = C.c_size_t
     L.bdsm_last_batch_errors.argtypes = [C.c_void_p, C.POINTER(_UpdateError), C.c_size_t]
     L.bdsm_last_error.restype = C.c_char_p
@@ -302,6 +306,19 @@ class Engine:
         if r != 0:
             _raise(r, self._h)
 
+    def set_query_active(self, query: int, active: bool) -> None:
+        """Whether later batches match `query` (run_pipeline drops unsolved queries)."""
+        r = lib().bdsm_engine_set_query_active(self._h, query, 1 if active else 0)
+        if r != 0:
+            _raise(r, self._h)
+
+    def query_timed_out(self, query: int) -> bool:
+        """MatchStats::timed_out of `query` in the last batch (its counts were dropped)."""
+        r = lib().bdsm_engine_query_timed_out(self._h, query)
+        if r < 0:
+            _raise(-r, self._h)
+        return r != 0
+
     def neighbors(self, v: int) -> List[int]:
         d = lib().bdsm_engine_neighbors(self._h, v, None, 0)
         out = np.zeros(max(d, 1), np.uint32)
@@ -327,6 +344,7 @@ class Engine:
         r = lib().bdsm_engine_collect_matches(self._h, cap)
         if r != 0:
             _raise(r, self._h)
+        self._collect_cap = cap
 
     def matches(self, query: int, positive: bool) -> np.ndarray:
         """The last batch's matches of `query` (external ids, query vertex order, sorted)."""
@@ -334,6 +352,9 @@ class Engine:
         total = lib().bdsm_engine_matches(self._h, query, 1 if positive else 0, None, 0)
         if total < 0:
             _raise(int(-total), self._h)
+        if total > getattr(self, "_collect_cap", 0):
+            raise EngineError(f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
+                              "(raise the collect_matches cap)")
         out = np.zeros((total, n), np.uint32)
         got = lib().bdsm_engine_matches(self._h, query, 1 if positive else 0, _ptr(out), total)
         if got < 0:

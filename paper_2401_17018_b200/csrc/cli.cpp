@@ -252,10 +252,12 @@ int run(const Args& args) {
   for (std::size_t bi = 0; bi < stream.size(); ++bi) {
     std::size_t live = 0;
     for (std::size_t i = 0; i < queries.size(); ++i) {
-      // a dead query gets a zero budget: the engine skips it
-      double left = queries[i].solved ? std::max(0.0, args.timeout - queries[i].spent) : 0.0;
-      if (queries[i].solved) ++live;
-      engine.set_deadline(qid[i], queries[i].solved ? std::max(left, 1e-9) : 1e-9);
+      // an unsolved query is no longer matched (src/bench.cpp:463-467); a live
+      // one gets the rest of its budget as this batch's deadline
+      engine.set_query_active(qid[i], queries[i].solved);
+      if (!queries[i].solved) continue;
+      ++live;
+      engine.set_deadline(qid[i], std::max(args.timeout - queries[i].spent, 1e-9));
     }
     bdsm_batch_stats st{};
     auto t0 = Clock::now();
@@ -267,7 +269,7 @@ int run(const Args& args) {
       if (!q.solved) continue;
       // the whole batch is charged to every live query (the engine runs them in one call)
       q.spent += live ? wall : 0.0;
-      if (((st.timed_out >> qid[i]) & 1u) || q.spent > args.timeout) {
+      if (engine.query_timed_out(qid[i]) || q.spent > args.timeout) {
         q.solved = false;
         continue;
       }

@@ -10,6 +10,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kMaxQ = 16;          // query vertices handled by the matching kernel
 constexpr int kMaxQEdges = kMaxQ * (kMaxQ - 1) / 2;
 constexpr int kWarpsPerBlock = 8;  // matching kernel: 256 threads
+constexpr uint32_t kMaxQueries = 256;  // queries per engine (the memo tag's query field is 8 bits)
 constexpr uint32_t kFull = 0xffffffffu;
 
 // Device view of the slack-padded dynamic CSR:
@@ -177,20 +178,21 @@ __host__ __device__ __forceinline__ uint32_t pair_hash(unsigned long long k) {
 }
 
 // Persistent weight memo (matching kernel, invalidated by the merge): one
-// 64-bit word per (vertex x, query q, signature sig) = x << 32 | q << 27 |
-// sig << 19 | weight.  Weights >= kMemoInvalid are never stored; an entry
+// 64-bit word per (vertex x, query q, signature sig) = x << 32 | q << 24 |
+// sig << 16 | weight (a weight counts neighbours of x, so it is < 2^16 below
+// degree 65535; larger ones are recomputed, never stored).  Weights >= kMemoInvalid are never stored; an entry
 // whose weight field is kMemoInvalid was invalidated (its list or a
 // neighbour's candidate row changed) and reads as a miss.  Linear probing,
 // at most kMemoProbes slots.
 constexpr int kMemoProbes = 8;
 constexpr unsigned long long kMemoEmpty = ~0ull;
-constexpr uint32_t kMemoWeightBits = 19;
+constexpr uint32_t kMemoWeightBits = 16;
 constexpr unsigned long long kMemoWeightMask = (1ull << kMemoWeightBits) - 1;
 constexpr unsigned long long kMemoInvalid = kMemoWeightMask;
 
 #ifdef __CUDACC__
 __device__ __forceinline__ unsigned long long memo_tag(uint32_t x, uint32_t q, uint32_t sig) {
-  return (uint64_t(x) << 32) | (uint64_t(q & 31) << 27) | (uint64_t(sig & 0xff) << kMemoWeightBits);
+  return (uint64_t(x) << 32) | (uint64_t(q & 0xff) << 24) | (uint64_t(sig & 0xff) << kMemoWeightBits);
 }
 
 __device__ __forceinline__ bool memo_get(const unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
@@ -244,14 +246,15 @@ __device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32
 }
 #endif
 
-// Device-side batch bookkeeping, copied back once per batch.
+// Device-side batch bookkeeping, copied back once per batch.  The per-query
+// results follow it in the same allocation (one D2H): u64 counts[2][nq]
+// ([phase][query] matches) and u32 timed_out[nq] (deadline fired).
 struct BatchState {
   uint32_t err_count;            // validate_batch failures
   uint32_t selfloop_min;         // first self-loop update index (kNone: none)
   uint32_t conflict_min;         // first conflicting update index (kNone: none)
   uint32_t n_touched;            // distinct endpoints
   uint32_t overflow;             // adjacency pool exhausted: merge skipped
-  uint32_t timed_out;            // bitmask over queries
   uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
   uint32_t n_items[2];
   uint32_t donations;            // statistics: donated subtrees
@@ -261,7 +264,6 @@ struct BatchState {
   uint64_t pool_top;             // adjacency pool bump pointer (elements)
   uint64_t relocations;
   uint64_t bytes_update;
-  uint64_t counts[2][32];        // [phase][query] matches
   uint64_t visits;
   uint64_t tasks_total;
   uint64_t items_total;

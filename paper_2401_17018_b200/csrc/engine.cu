@@ -105,7 +105,7 @@ struct QueryState {
   uint32_t n_leafsig = 0;
   uint64_t deadline_ns = 0;  // host-steady-clock based, translated per batch
   double deadline_s = 0;     // seconds since epoch of the host steady clock
-  bool solved = true;
+  bool active = true;        // matched in later batches (bdsm_engine_set_query_active)
 };
 
 uint64_t now_ns() {
@@ -227,7 +227,7 @@ struct bdsm_engine {
         std::min<uint64_t>({uint64_t(opts.l2_hot_mb) << 20, uint64_t(max_window), uint64_t(max_persist)});
     if (budget < 4096 || g.pool_size - pool_top < 2 * (budget / 4)) return;  // no room: skip this period
     hot_hist.ensure(34);
-    launch_hot_pack(g, heat.p, hot_hist.p, budget, d_st.p, num_sms, stream);
+    launch_hot_pack(g, heat.p, hot_hist.p, budget, d_st, num_sms, stream);
     launches += 4;
     CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(budget)));
     cudaStreamAttrValue attr{};
@@ -267,8 +267,28 @@ struct bdsm_engine {
   }
   uint32_t epoch = 0;
   DBuf<uint8_t> cub_tmp;
-  DBuf<BatchState> d_st;
+  // BatchState followed by the per-query results (common.cuh): one H2D
+  // before, one D2H after every batch
+  DBuf<unsigned char> st_buf;
+  BatchState* d_st = nullptr;
   BatchState* h_st = nullptr;
+  size_t st_bytes = 0, h_st_bytes = 0;
+  size_t st_size() const { return sizeof(BatchState) + 20 * std::max<size_t>(queries.size(), 1); }
+  static unsigned long long* st_counts(BatchState* s) { return reinterpret_cast<unsigned long long*>(s + 1); }
+  uint32_t* st_timed(BatchState* s) const { return reinterpret_cast<uint32_t*>(st_counts(s) + 2 * queries.size()); }
+  void ensure_state() {
+    st_bytes = st_size();
+    if (st_buf.n < st_bytes) {
+      st_buf.ensure(st_bytes);
+      d_st = reinterpret_cast<BatchState*>(st_buf.p);
+    }
+    if (h_st_bytes < st_bytes) {
+      if (h_st) cudaFreeHost(h_st);
+      h_st = nullptr;
+      CK(cudaMallocHost(&h_st, st_bytes));
+      h_st_bytes = st_bytes;
+    }
+  }
   bdsm_update* h_ups = nullptr;
   const bdsm_update* h_src = nullptr;  // this batch's host updates (caller's pinned buffer or h_ups)
   size_t h_ups_cap = 0;
@@ -287,6 +307,7 @@ struct bdsm_engine {
   }
 
   std::vector<bdsm_update_error> last_errors;
+  std::vector<uint8_t> last_timed;  // per query: the deadline fired in the last batch
 
   ~bdsm_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -658,7 +679,8 @@ struct bdsm_engine {
     if (qs->q.n > uint32_t(kMaxQ))
       throw std::invalid_argument("query graph too large for the GPU engine (max " +
                                   std::to_string(kMaxQ) + " vertices)");
-    if (queries.size() >= 32) throw std::invalid_argument("at most 32 queries per engine");
+    if (queries.size() >= kMaxQueries)
+      throw std::invalid_argument("at most " + std::to_string(kMaxQueries) + " queries per engine");
     qs->enc = encode_query(qs->q, opts.group_bits);
     DevQueryEnc& de = qs->denc;
     de.n = qs->q.n;
@@ -896,7 +918,9 @@ struct bdsm_engine {
     a.tasks = tasks.p;
     a.items = items.p;
     a.max_items = uint32_t(std::min<size_t>(max_items, 0xffffffffu));
-    a.st = d_st.p;
+    a.st = d_st;
+    a.count_out = st_counts(d_st) + size_t(phase) * queries.size() + size_t(qi);
+    a.timed_out = st_timed(d_st) + qi;
     a.deadline_ns = 0;
     a.q = qstate.p;
     a.dyn = dyn.p;
@@ -919,7 +943,7 @@ struct bdsm_engine {
   void run_phase(uint32_t n, uint32_t phase) {
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       QueryState& qs = *queries[qi];
-      if (!qs.solved || qs.q.edges.empty()) continue;
+      if (!qs.active || qs.q.edges.empty()) continue;
       PhaseArgs a = phase_args(n, phase, int(qi));
       // positive phase, warm memo: the touched hubs' weights are refilled on
       // the side stream while the anchors are counted and emitted
@@ -1044,8 +1068,9 @@ struct bdsm_engine {
       CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
       pend.st.h2d_bytes = n * sizeof(bdsm_update);
     }
+    std::memset(static_cast<void*>(h_st), 0, st_bytes);
     *h_st = template_state();
-    CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_st, h_st, st_bytes, cudaMemcpyHostToDevice, stream));
     const uint32_t m = uint32_t(2 * n);
     const uint32_t nq = uint32_t(queries.size());
     if (pend.attempt == 0) hot_pack_maybe();
@@ -1055,13 +1080,13 @@ struct bdsm_engine {
     const bool full_sort = pend.full_sort || id_bits >= 32;
     const uint32_t key_bits = full_sort ? 32u : id_bits;  // both ids packed into 2 x id_bits
     const int sort_end_bit = full_sort ? 64 : int(2 * id_bits);
-    launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st.p, keys.p, vals.p, dlab.p, ecode.p,
+    launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st, keys.p, vals.p, dlab.p, ecode.p,
                    full_sort ? 0xffffffffu : (1u << id_bits), key_bits, stream);
     // one query, small batch: the negative phase's anchors need only the
     // translated updates and G, so they are counted and emitted on the side
     // stream while the keys are sorted (joined before the matching kernel)
     early_anchors = false;
-    if (queries.size() == 1 && n <= tune_self_scan && !collect_cap && queries[0]->solved &&
+    if (queries.size() == 1 && n <= tune_self_scan && !collect_cap && queries[0]->active &&
         !queries[0]->q.edges.empty()) {
       PhaseArgs a = phase_args(uint32_t(n), 0, 0);
       a.self_scan = 1;
@@ -1082,7 +1107,7 @@ struct bdsm_engine {
       CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
     }
     CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(kb.Current(), vb.Current(), key_bits, skeys.p, svals.p, m, d_st.p, head.p, insflag.p, d_rows.p,
+    launch_post_sort(kb.Current(), vb.Current(), key_bits, skeys.p, svals.p, m, d_st, head.p, insflag.p, d_rows.p,
                      nq, g.V, hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
     {
       // the merge's insert prefix is only needed after the negative phase: it
@@ -1097,7 +1122,7 @@ struct bdsm_engine {
       CK(cudaEventRecord(join2_ev, side));
       tmp = cub_tmp.n;
       CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
-                                    &d_st.p->n_touched, int(m), stream));
+                                    &d_st->n_touched, int(m), stream));
     }
     CK(cudaEventRecord(ev[1], stream));
     run_phase(uint32_t(n), 0);
@@ -1106,10 +1131,10 @@ struct bdsm_engine {
     cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
     CK(cudaEventRecord(m0, stream));
     const bool small_ok = m >= tune_small_min;
-    launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st.p, new_off.p, new_cap.p, big_list.p,
+    launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st, new_off.p, new_cap.p, big_list.p,
                  small_list.p, mid_list.p, small_ok, stream);
     launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
-                         d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st.p, memo.p,
+                         d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st, memo.p,
                          uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, mid_list.p, small_ok,
                          num_sms, stream);
     CK(cudaEventRecord(m1, stream));
@@ -1123,13 +1148,13 @@ struct bdsm_engine {
         CK(cudaMemsetAsync(heat.p, 0, 4ull * g.V, stream));
         heat_init = true;
       }
-      launch_hot_walks(heads.p, skeys.p, d_st.p, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
+      launch_hot_walks(heads.p, skeys.p, d_st, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
       ++launches;
     }
     launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
     ++launches;
     CK(cudaEventRecord(ev[4], stream));
-    CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h_st, d_st, st_bytes, cudaMemcpyDeviceToHost, stream));
     if (memo.p) {
       if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
       CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
@@ -1160,12 +1185,11 @@ struct bdsm_engine {
     // overflow 4 enables the label array and reruns the batch)
     ensure_batch(n);
     ensure_tasks(n);
-    if (!h_st) CK(cudaMallocHost(&h_st, sizeof(BatchState)));
+    ensure_state();
     if (!ev[0]) {
       for (auto& e : ev) CK(cudaEventCreate(&e));
       for (auto& e : merge_ev) CK(cudaEventCreate(&e));
     }
-    d_st.ensure(1);
     const bdsm_update_dev* src;
     if (device_input) {
       src = reinterpret_cast<const bdsm_update_dev*>(updates);
@@ -1269,11 +1293,20 @@ struct bdsm_engine {
     }
     // start the memo over before its probes run out (fill read with the batch's final copy)
     if (memo.p && h_memo_fill && *h_memo_fill > memo.n * 2 / 5) reset_memo();
+    // a query whose deadline fired has its counts of this batch dropped
+    // (MatchStats::timed_out, src/scheduler.cpp:101-110); whether it stays
+    // matched in later batches is the caller's decision (set_query_active),
+    // as in run_pipeline (src/bench.cpp:420-432)
+    const unsigned long long* cnt = st_counts(h_st);
+    const uint32_t* tmo = st_timed(h_st);
+    uint32_t tmask = 0;
+    last_timed.assign(queries.size(), 0);
     for (size_t qi = 0; qi < queries.size(); ++qi) {
-      bool dead = (b.timed_out >> qi) & 1u;
-      if (dead) queries[qi]->solved = false;
-      if (neg) neg[qi] = dead ? 0 : b.counts[0][qi];
-      if (pos) pos[qi] = dead ? 0 : b.counts[1][qi];
+      const bool dead = tmo[qi] != 0;
+      last_timed[qi] = dead;
+      if (dead && qi < 32) tmask |= 1u << qi;
+      if (neg) neg[qi] = dead ? 0 : cnt[qi];
+      if (pos) pos[qi] = dead ? 0 : cnt[queries.size() + qi];
     }
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[0], ev[5]);
@@ -1304,8 +1337,8 @@ struct bdsm_engine {
     pend.st.touched = b.n_touched;
     pend.st.relocations = b.relocations;
     pend.st.compactions = pend.compactions;
-    pend.st.timed_out = b.timed_out;
-    pend.st.d2h_bytes = sizeof(BatchState);
+    pend.st.timed_out = tmask;
+    pend.st.d2h_bytes = st_bytes;
     pend.st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pend.t0).count();
     if (stats) *stats = pend.st;
     return BDSM_OK;
@@ -1321,16 +1354,16 @@ struct bdsm_engine {
   // phase alone (the graph is already G').
   void rerun_positive(uint32_t n) {
     h_st->overflow = 0;
-    for (auto& c : h_st->counts[1]) c = 0;
-    CK(cudaMemcpyAsync(d_st.p, h_st, sizeof(BatchState), cudaMemcpyHostToDevice, stream));
+    for (size_t qi = 0; qi < queries.size(); ++qi) st_counts(h_st)[queries.size() + qi] = 0;
+    CK(cudaMemcpyAsync(d_st, h_st, st_bytes, cudaMemcpyHostToDevice, stream));
     const uint32_t m = 2 * n, nq = uint32_t(queries.size());
     // the batch-endpoint row flags were cleared at the end of the attempt
     CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(skeys.p, svals.p, 32, nullptr, nullptr, m, d_st.p, head.p, insflag.p, d_rows.p, nq, g.V,
+    launch_post_sort(skeys.p, svals.p, 32, nullptr, nullptr, m, d_st, head.p, insflag.p, d_rows.p, nq, g.V,
                      hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
     run_phase(n, 1);
     launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
-    CK(cudaMemcpyAsync(h_st, d_st.p, sizeof(BatchState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h_st, d_st, st_bytes, cudaMemcpyDeviceToHost, stream));
     sync();
     if (h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
   }
@@ -1512,6 +1545,22 @@ bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seco
     qs.deadline_s = seconds_from_now > 0 ? double(now_ns()) * 1e-9 + seconds_from_now : 0;
     return BDSM_OK;
   });
+}
+
+bdsm_status bdsm_engine_set_query_active(bdsm_engine* engine, int query, int active) {
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  return guarded([&]() -> bdsm_status {
+    if (engine->pend.active) throw std::invalid_argument("a batch is in flight on this engine (wait for it first)");
+    engine->queries.at(size_t(query))->active = active != 0;
+    return BDSM_OK;
+  });
+}
+
+int bdsm_engine_query_timed_out(bdsm_engine* engine, int query) {
+  if (!engine) return -int(fail(BDSM_INVALID_ARGUMENT, "null engine"));
+  if (query < 0 || size_t(query) >= engine->queries.size())
+    return -int(fail(BDSM_INVALID_ARGUMENT, "query index out of range"));
+  return size_t(query) < engine->last_timed.size() ? int(engine->last_timed[size_t(query)]) : 0;
 }
 
 size_t bdsm_last_batch_errors(bdsm_engine* engine, bdsm_update_error* out, size_t cap) {

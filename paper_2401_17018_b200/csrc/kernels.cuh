@@ -123,6 +123,8 @@ struct PhaseArgs {
   Item* items;
   uint32_t max_items;
   BatchState* st;
+  unsigned long long* count_out; // this (query, phase)'s match count (after the BatchState)
+  uint32_t* timed_out;           // this query's deadline flag
   uint64_t deadline_ns;          // 0: none
   QueueState* q;                 // work-queue counters (reset before each launch)
   DynItem* dyn;                  // donated-subtree queue

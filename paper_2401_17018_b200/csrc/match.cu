@@ -233,7 +233,7 @@ __global__ void k_anchor_emit(PhaseArgs a) {
       c += d;
     });
   }
-  if (direct) atomicAdd((unsigned long long*)&a.st->counts[a.phase][a.query], (unsigned long long)direct);
+  if (direct) atomicAdd(a.count_out, (unsigned long long)direct);
   if (a.shard_rank == 0 && bytes) {
     atomicAdd((unsigned long long*)&a.st->bytes_phase, (unsigned long long)bytes);
     atomicAdd((unsigned long long*)&a.st->gen_calls, (unsigned long long)calls);
@@ -1261,12 +1261,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
   }
   __syncwarp();
   if (lane == 0) {
-    if (stat[0]) atomicAdd((unsigned long long*)&st->counts[a.phase][a.query], stat[0]);
+    if (stat[0]) atomicAdd(a.count_out, stat[0]);
     if (stat[1]) atomicAdd((unsigned long long*)&st->visits, stat[1]);
     if (stat[2]) atomicAdd((unsigned long long*)&st->bytes_phase, stat[2]);
     if (stat[3]) atomicAdd((unsigned long long*)&st->gen_calls, stat[3]);
     if (stat[4]) atomicAdd((unsigned long long*)&st->bytes_kernel, stat[4]);
-    if (timed_out) atomicOr(&st->timed_out, 1u << a.query);
+    if (timed_out) atomicExch(a.timed_out, 1u);
   }
 }
 

@@ -84,6 +84,8 @@ def main():
         ("gen_dense_delete", 200, 1800, 2, 0, "g:dense,4,2", "s:0.05,delete,2", 3, True),
         ("gen_kcore_mixed", 300, 2000, 3, 0, "g:sparse,4,2", "s:0.05,mixed,3,4", 21, True),
         ("gen_elabel_mixed", 250, 1500, 2, 2, "g:sparse,4,2", "s:0.06,mixed,3", 8, True),
+        # the paper's 50-query sets: more queries than one 32-bit mask
+        ("gen_sparse50_mixed", 1500, 9000, 2, 0, "g:sparse,6,50", "s:0.02,mixed,3", 13, False),
     ]
     for name, V, E, L, EL, q, s, seed, dump in cases:
         d = os.path.join(OUT, name)

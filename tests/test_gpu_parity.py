@@ -4,6 +4,7 @@ reference's |positive| / |negative| (bit-exact integer counts)."""
 import pytest
 
 import golden_util as gu
+from oracle_py import Oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -20,11 +21,18 @@ def _engine(inst, **kw):
 def test_counts_equal_reference(suite):
     for inst in gu.load(suite):
         e, batches = _engine(inst)
+        vl, eu, ev, el, ql, qe, _ = gu.instance_arrays(inst)
+        o = Oracle(vl, eu, ev, el)
+        o.add_query(ql, qe)
         for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
             r = e.match_batch(b)
             assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (inst["name"], bi)
-            # visibility pruning can only remove DFS nodes relative to the reference tree
-            assert r.stats["dfs_visits"] <= exp["visits"], (inst["name"], bi)
+            # the engine applies dedupe_by_order when it generates candidates, so
+            # its dfs_visits is the reference tree's minus the pruned subtrees:
+            # exactly the restatement's pruned-visit count (pinned to the reference)
+            _, _, st = o.apply_batch(b)
+            assert st[0] == exp["visits"], (inst["name"], bi)
+            assert r.stats["dfs_visits"] == st[6], (inst["name"], bi, r.stats["dfs_visits"], int(st[6]))
         e.close()
 
 

@@ -78,12 +78,13 @@ def main():
     per = [l for l in lines if "batch" in l]
     summ = [l for l in lines if l.get("summary")]
     ref = [(l["positive"], l["negative"]) for l in per]
-    ref_v = [l["dfs_visits"] for l in per]
+    ref_v = [l["dfs_visits_pruned"] for l in per]
+    ref_tree = [l["dfs_visits"] for l in per]
     res = {
         "config": args.config, "V": meta["V"], "E": meta["E"], "d_max": meta["d_max"], "batch": meta["batch"],
         "prefix": args.prefix or meta["batch"], "batches_checked": len(per), "batches": args.batches,
         "ours": ours, "restatement": ref, "counts_equal": ours[:len(ref)] == ref and len(ref) == args.batches,
-        "dfs_visits_ours": visits, "dfs_visits_restatement": ref_v,
+        "dfs_visits_ours": visits, "dfs_visits_restatement": ref_v, "dfs_visits_reference_tree": ref_tree,
         "dfs_visits_equal": visits[:len(ref_v)] == ref_v,
         "max_count": max([max(p) for p in ref] or [0]), "ge_2_32": any(max(p) >= 2 ** 32 for p in ref),
         "gpu_ms_per_subbatch": ms, "cpu_s": cpu_s, "gen_s": gen_s,
