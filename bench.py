@@ -179,6 +179,81 @@ def cpu_model():
     return None
 
 
+def so_sha():
+    import hashlib
+    import paper_2401_17018_b200 as bd
+    with open(bd.lib_path(), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def physical_roofline(config, mk, mg, bker, bphase_ref, bupd, peak, peak_kind, step_ms, batch):
+    """Roofline of the dominant kernel (k_wbm) from PHYSICAL bytes: the DRAM
+    traffic per step of its launches in the committed ncu metrics capture of
+    this build (profiles/traffic_<config>.json, tools/ncu_traffic.py) over its
+    live CUDA-event time per step.  SURVEY.md §8(d)'s algorithmic figures (4 B
+    per element of every backward list of a GenCandidates call) are reported
+    beside it as equivalents: the kernel reads label sub-ranges, bitmap words
+    and memoised weights, not whole lists, so those exceed any physical roof."""
+    prof = os.path.join("profiles", f"traffic_{config.lower()}.json")
+    tr, sha = None, so_sha()
+    try:
+        with open(os.path.join(REPO, prof)) as f:
+            tr = json.load(f)
+    except (OSError, ValueError):
+        pass
+    roof = {"bound": "hbm", "kernel": "k_wbm (K6 matching, negative + positive launch per step)", "peak": peak,
+            "unit": "GB/s", "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+            "ms_per_step_live": mk, "share_of_step": mk / step_ms if step_ms else None,
+            "algorithmic_equivalent": {
+                "bytes_kernel_per_step": bker,
+                "bytes_kernel_equivalent_GBps": bker / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
+                "reference_tree_bytes_per_step": bphase_ref,
+                "reference_tree_equivalent_GBps": bphase_ref / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
+                "note": "SURVEY.md §8(d): 4 B x backward-list degrees per GenCandidates call, on the calls the "
+                        "kernel makes (bytes_kernel) and on the reference DFS tree (B_phase); not physical"}}
+    w = tr["kernels"].get("k_wbm") if tr else None
+    if w:
+        dram = w["dram_bytes_per_step"]
+        achieved = dram / (mk / 1e3) / 1e9 if mk > 0 else 0.0
+        roof.update({
+            "achieved": achieved, "frac": achieved / peak,
+            "traffic": dram / max(w["launches_per_step"], 1), "traffic_per_step": dram,
+            "traffic_source": f"{prof}: dram__bytes_read.sum + dram__bytes_write.sum of the step's k_wbm launches "
+                              f"(ncu metrics pass, build {tr.get('build')}, this build {sha}, "
+                              f"{'same' if tr.get('build') == sha else 'DIFFERENT'} build)",
+            "ncu_ms_per_step": w["ms_per_step"], "frac_at_ncu_time": w["dram_GBps"] / peak,
+            "l2": {"bytes_per_step": w["l2_bytes_per_step"],
+                   "achieved_GBps": w["l2_bytes_per_step"] / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
+                   "note": "lts__t_bytes.sum (all L2 traffic) of the same launches over the live time: the "
+                           "re-read working set is L2-resident, the kernel is bound by dependent L2 round trips"},
+        })
+        m = tr["kernels"]
+        merge = {k: m[k] for k in ("k_alloc", "k_merge_refresh", "k_merge_small", "k_merge_big", "k_finish_big")
+                 if k in m}
+        if merge:
+            md = sum(v["dram_bytes_per_step"] for v in merge.values())
+            roof["merge"] = {"kernels": sorted(merge), "dram_bytes_per_step": md, "b_upd_per_step": bupd,
+                             "dram_over_b_upd": md / bupd if bupd else None, "ms_per_step_live": mg,
+                             "dram_GBps_live": md / (mg / 1e3) / 1e9 if mg > 0 else 0.0}
+    else:
+        achieved = bker / (mk / 1e3) / 1e9 if mk > 0 else 0.0
+        roof.update({"achieved": achieved, "frac": achieved / peak, "traffic": None,
+                     "traffic_source": f"no ncu capture at {prof}: achieved is the algorithmic bytes_kernel "
+                                       "figure, not physical"})
+    return roof
+
+
+def spawn_ranks(n: int) -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("spawning", n, "ranks:", " ".join(cmd))
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -195,10 +270,15 @@ def main():
                     help="batches checked against the CPU restatement at full size (-1: all; 0: off)")
     ap.add_argument("--parity-timeout", type=float, default=600.0)
     ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--coalesce", action="store_true", help="exact coalesced search (counts unchanged)")
     ap.add_argument("--l2-hot-mb", type=int, default=0, help="K8 hot-list L2 persistence budget (0: off)")
     args = ap.parse_args()
 
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # plain `python bench.py --gpus N`: start the N ranks here (one process
+        # per GPU, torch.distributed.run on 127.0.0.1) and relay rank 0's line
+        return spawn_ranks(args.gpus)
     if args.steps < 1 or args.warmup < 3:
         log("warmup must be >= 3 and steps >= 1")
     ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
@@ -232,7 +312,9 @@ def config_dict(args, wl, world):
             "batch_mode": m["mode"], "query_vertices": len(wl.qlabels), "query_edges": len(wl.qedges),
             "query_labels": wl.qlabels, "query": wl.qedges, "seeds": m["seeds"],
             "l2": "flushed (256 MiB write) before every timed step",
-            "parallelism": f"replicated graph, work units split over {world} GPU(s)" if world > 1 else "1 GPU"}
+            "parallelism": f"replicated graph, work units split over {world} GPU(s)" if world > 1 else "1 GPU",
+            "coalesce": "exact (one search per automorphism orbit of directed query edges)" if args.coalesce
+                        else "off"}
 
 
 def reference_arm(args, world, rank):
@@ -282,10 +364,10 @@ def ours(args, world, rank, local):
 
     t0 = time.time()
     engA = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
-                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb)
+                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb, coalesce=args.coalesce)
     engA.add_query(wl.qlabels, wl.qedges)
     engB = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
-                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb)
+                     chunk=args.chunk, l2_hot_mb=args.l2_hot_mb, coalesce=args.coalesce)
     engB.add_query(wl.qlabels, wl.qedges)
     log(f"engines built in {time.time() - t0:.1f}s")
 
@@ -384,44 +466,11 @@ def ours(args, world, rank, local):
     peak, peak_kind = peaks()
     mk = statistics.mean(s["ms_match_kernel"] for s in statsA)
     mg = statistics.mean(s["ms_merge_kernel"] for s in statsA)
-    # algorithmic bytes of the GenCandidates calls the kernel makes (SURVEY.md
-    # §8(d) per-call figure); the reference DFS tree's B_phase is reported beside
-    bphase = statistics.mean(s["bytes_kernel"] for s in statsA)
+    bker = statistics.mean(s["bytes_kernel"] for s in statsA)
     bphase_ref = statistics.mean(s["bytes_phase"] for s in statsA)
     bupd = statistics.mean(s["bytes_update"] for s in statsA)
-    kern = {
-        "k_wbm (K6 matching, both phases)": (bphase, mk),
-        "k_alloc+k_merge_refresh (K3+K4)": (bupd, mg),
-    }
-    dom = max(kern, key=lambda k: kern[k][1])
-    traffic = None  # DRAM bytes per launch of k_wbm from the committed ncu --set full capture
-    traffic_l2 = None
-    try:
-        with open(os.path.join(REPO, "profiles", "wbm_traffic.json")) as f:
-            tr = json.load(f)
-        if dom.startswith(tr["kernel"]):
-            traffic = tr["dram_bytes_per_launch"]
-            traffic_l2 = {k: tr[k] for k in ("l2_read_bytes_per_launch", "l2_throughput_pct_of_peak", "note") if k in tr}
-    except (OSError, KeyError, ValueError):
-        pass
-    ab, at = kern[dom]
-    achieved = ab / (at / 1e3) / 1e9 if at > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-            "traffic_source": "profiles/wbm_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, one launch)",
-            "physical": traffic_l2,
-            "algorithmic_bytes_per_launch": ab, "ms_per_launch": at,
-            "algorithmic_bytes": "4 B x backward-neighbour degrees per GenCandidates call made by k_wbm "
-                                 "(SURVEY.md §8(d)), per step (negative + positive launch)",
-            "note": "SURVEY.md §8(d) counts 4 B per element of every backward list of a GenCandidates call; the "
-                    "kernel reads only the label sub-range of the driver list and one bitmap word or a few search "
-                    "probes of the others, so achieved/peak can exceed 1 — the physically moved bytes are under "
-                    "'physical' (ncu: L2 and DRAM traffic of the profiled launch)",
-            "reference_tree_bytes_per_step": bphase_ref,
-            "reference_tree_equivalent_GBps": bphase_ref / (mk / 1e3) / 1e9 if mk > 0 else 0.0,
-            "other": {k: {"bytes": v[0], "ms": v[1], "GB/s": (v[0] / (v[1] / 1e3) / 1e9 if v[1] > 0 else 0)}
-                      for k, v in kern.items() if k != dom},
-            "share_of_step": at / statistics.mean(dev_ms)}
+    roof = physical_roofline(args.config, mk, mg, bker, bphase_ref, bupd, peak, peak_kind,
+                             statistics.mean(dev_ms), wl.meta["batch"])
 
     line = {
         "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -441,8 +490,18 @@ def ours(args, world, rank, local):
         "per_step": [{"ms": s["ms_device"], "neg_ms": s["ms_negative"], "merge_ms": s["ms_update"],
                       "pos_ms": s["ms_positive"], "match_kernel_ms": s["ms_match_kernel"],
                       "dfs_visits": s["dfs_visits"], "tasks": s["tasks"], "items": s["work_items"],
-                      "touched": s["touched"], "relocations": s["relocations"]} for s in statsA],
+                      "touched": s["touched"], "relocations": s["relocations"], "attempts": s["attempts"],
+                      "reruns": s["reruns"], "compactions": s["compactions"]} for s in statsA],
+        "attempts_per_step": [s["attempts"] for s in statsA],
     }
+    if world > 1:
+        import torch.distributed as dist
+        ndev = torch.cuda.device_count()
+        line["comm"] = {"backend": dist.get_backend(), "ranks": dist.get_world_size(), "devices": ndev,
+                        "step": ("NCCL broadcast of the batch, replicated apply, own share of the work units, "
+                                 "NCCL all-reduce of the counts" if dist.get_backend() == "nccl" else
+                                 "functional run: ranks share the visible device(s); counts summed over gloo "
+                                 "after the timed region")}
     if world == 1 and not args.no_cpu_baseline and wl.meta["E"] > 500_000_000:
         # the reference's PMA alone needs ~69 GB at the
         # Friendster shape plus sort keys and an edge hash set
@@ -466,7 +525,9 @@ def ours(args, world, rank, local):
         vis = [b["dfs_visits_pruned"] for b in res["batches"]]
         vis_ref = [b["dfs_visits"] for b in res["batches"]]
         eq_counts = got == ours_c[:len(got)]
-        eq_vis = all(v is None or v == r for v, r in zip(ours_v, vis))
+        # with exact coalescing the engine walks one tree per automorphism orbit,
+        # so only the counts are comparable
+        eq_vis = None if args.coalesce else all(v is None or v == r for v, r in zip(ours_v, vis))
         line["parity_full"] = {
             "checker": "oracle/oracle_bench: count-only CPU restatement of match_batch (coalesce off), pinned to "
                        "the reference on tests/golden/ (counts, dfs_visits, intersection_ops, tasks_run)",

@@ -67,7 +67,11 @@ typedef struct bdsm_query_desc {
 
 typedef struct bdsm_options {
   uint32_t group_bits;   /* NLF counter width M (reference default 2; PipelineConfig::group_bits) */
-  uint32_t coalesce;     /* must be 0: coalesced search is not exact in the reference (F1) */
+  uint32_t coalesce;     /* 1: exact coalesced search (MatchOptions::coalesce, src/matcher.cpp:119-140, done
+                            right): one anchored orientation per automorphism orbit of directed query
+                            edges, counted with the orbit size — the counts equal coalesce 0 on every
+                            batch (the reference's version misses matches).  dfs_visits
+                            then describe the search done, not the reference tree. */
   int32_t device;        /* CUDA device ordinal */
   uint32_t shard_rank;   /* multi-GPU: this rank's share of the work units */
   uint32_t shard_world;  /* 0 or 1 = whole batch */
@@ -97,7 +101,7 @@ typedef struct bdsm_update_error {
  * device timing and the SURVEY.md §8(d) algorithmic byte counts). */
 typedef struct bdsm_batch_stats {
   double ms_total;        /* host wall time of the call */
-  double ms_device;       /* CUDA-event time of the whole device sequence */
+  double ms_device;       /* CUDA-event time of the whole device sequence, every attempt and rerun */
   double ms_negative;     /* matching kernel, negative phase(s) */
   double ms_update;       /* sort + merge + refresh */
   double ms_positive;     /* matching kernel, positive phase(s) */
@@ -121,6 +125,9 @@ typedef struct bdsm_batch_stats {
   uint64_t bytes_kernel;   /* 4 B x backward degrees of the GenCandidates calls the kernel actually made
                               (bytes_phase counts them on the reference's DFS tree; the kernel counts
                               independent query tails once per prefix instead of enumerating them) */
+  uint32_t attempts;       /* device launches of the whole batch sequence (> 1: pool compaction, work-item
+                              regrowth, edge-label array or full-width sort rerun); ms_device spans all */
+  uint32_t reruns;         /* positive-phase reruns after a work-item regrowth (inside ms_device) */
 } bdsm_batch_stats;
 
 /* Engine lifecycle.  Replaces LabeledGraph::build_from_edges plus the
@@ -203,6 +210,14 @@ BDSM_API uint32_t bdsm_engine_num_vertices(bdsm_engine* engine);
 /* Rebuild the plan of a query from the current candidate columns
  * (drift replanning, src/bench.cpp:451-453). */
 BDSM_API bdsm_status bdsm_engine_replan(bdsm_engine* engine, int query);
+
+/* Host-only planner: the automorphism orbits of the query's directed edges
+ * (d = 2*edge + flip; flip 0 = (a, b), 1 = (b, a)) used by exact coalescing.
+ * mult[d] = orbit size when d is its orbit's representative (its lowest
+ * index), 0 otherwise; all 1 when the query has more than 20,000
+ * automorphisms (the reference's KDegenOptions limit).  mult has 2*num_edges
+ * entries.  Returns the number of automorphisms (or 0 when truncated), -status. */
+BDSM_API int64_t bdsm_plan_edge_orbits(const bdsm_query_desc* query, uint32_t* mult);
 
 /* Multi-GPU work split: owner rank of each work unit given
  * its cost, in canonical order.  owner = floor(world * prefix / total).

@@ -69,7 +69,7 @@ class _Stats(C.Structure):
                 ("relocations", C.c_uint64), ("compactions", C.c_uint32), ("timed_out", C.c_uint32),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("ms_match_kernel", C.c_double),
                 ("ms_merge_kernel", C.c_double), ("kernel_launches", C.c_uint32), ("cub_launches", C.c_uint32),
-                ("bytes_kernel", C.c_uint64)]
+                ("bytes_kernel", C.c_uint64), ("attempts", C.c_uint32), ("reruns", C.c_uint32)]
 
 
 _lib = None
@@ -133,6 +133,8 @@ def _load():
     L.bdsm_engine_matches.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]
     L.bdsm_engine_tail.restype = C.c_int
     L.bdsm_engine_tail.argtypes = [C.c_void_p, C.c_int, C.c_uint32]
+    L.bdsm_plan_edge_orbits.restype = C.c_int64
+    L.bdsm_plan_edge_orbits.argtypes = [C.c_void_p, C.c_void_p]
     L.bdsm_version.restype = C.c_char_p
     L.bdsm_version.argtypes = []
     _lib = L
@@ -221,14 +223,14 @@ class Engine:
 
     def __init__(self, vertex_labels, src, dst, edge_labels=None, *, group_bits: int = 2, device: int = 0,
                  shard_rank: int = 0, shard_world: int = 1, slack: float = 0.25, pool_reserve: float = 0.5,
-                 chunk: int = 32, zero_copy: bool = False, l2_hot_mb: int = 0):
+                 chunk: int = 32, zero_copy: bool = False, l2_hot_mb: int = 0, coalesce: bool = False):
         L = lib()
         self._vl = _u32(vertex_labels)
         s, d = _u32(src), _u32(dst)
         el = None if edge_labels is None else _u32(edge_labels)
         desc = _GraphDesc(len(self._vl), self._vl.ctypes.data, len(s), s.ctypes.data, d.ctypes.data,
                           None if el is None else el.ctypes.data)
-        opts = _Options(group_bits, 0, device, shard_rank, shard_world, slack, pool_reserve, chunk,
+        opts = _Options(group_bits, 1 if coalesce else 0, device, shard_rank, shard_world, slack, pool_reserve, chunk,
                         1 if zero_copy else 0, l2_hot_mb)
         h = C.c_void_p()
         st = L.bdsm_engine_create(C.byref(desc), C.byref(opts), C.byref(h))
@@ -417,6 +419,23 @@ class Engine:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def plan_edge_orbits(labels: Sequence[int], edges) -> Tuple[List[int], int]:
+    """Exact-coalescing plan of a query (host only): per directed edge
+    d = 2*edge + flip the multiplicity its search stands for (orbit size for an
+    orbit's representative, 0 for the others), and the automorphism count
+    (0: more than 20,000, no coalescing)."""
+    L = lib()
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.uint32))
+    ea = np.ascontiguousarray(np.asarray([e[0] for e in edges], dtype=np.uint32))
+    eb = np.ascontiguousarray(np.asarray([e[1] for e in edges], dtype=np.uint32))
+    desc = _QueryDesc(len(lab), _ptr(lab), len(ea), _ptr(ea), _ptr(eb), None)
+    mult = np.zeros(max(2 * len(ea), 1), np.uint32)
+    r = L.bdsm_plan_edge_orbits(C.byref(desc), _ptr(mult))
+    if r < 0:
+        _raise(int(-r))
+    return mult[:2 * len(ea)].tolist(), int(r)
 
 
 def shard_owners(costs: Sequence[int], world: int) -> List[int]:

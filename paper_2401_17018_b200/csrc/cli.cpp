@@ -16,8 +16,10 @@
 // `bdsm generate` (not in the reference) runs only the seeded generators and
 // writes query_<i>.txt / stream.txt as `bdsm run` would, without a GPU.
 //
-// GPU-build differences: --coalesce defaults to off and "on" runs the exact
-// search (the reference's coalesced search misses matches);
+// GPU-build differences: --coalesce defaults to off and "on" runs the EXACT
+// coalesced search (one search per automorphism orbit of directed query
+// edges, counted with the orbit size: the counts equal "off"; the reference's
+// coalesced search misses matches);
 // --workers/--group-size/--stealing are accepted and ignored (the device
 // schedules its own warps); utilization.csv reports the device.
 #include <sys/stat.h>
@@ -185,8 +187,6 @@ int run(const Args& args) {
   if (args.stealing != "off" && args.stealing != "passive" && args.stealing != "active")
     throw std::invalid_argument("unknown stealing mode: " + args.stealing);  // src/scheduler.cpp:16
   if (args.coalesce != "on" && args.coalesce != "off") throw std::invalid_argument("--coalesce wants on|off");
-  if (args.coalesce == "on")
-    std::cerr << "note: coalesced search is not exact in the reference (SURVEY.md F1); running the exact search\n";
   if (!args.dump_plan.empty())
     throw std::runtime_error("--dump-plan is not supported by the GPU build (plan_to_json is a debug dump)");
 
@@ -197,6 +197,7 @@ int run(const Args& args) {
   bdsm_options opts = Engine::defaults();
   opts.group_bits = args.group_bits;
   opts.device = args.device;
+  opts.coalesce = args.coalesce == "on" ? 1u : 0u;
   Engine engine(g.vertices, g.edges, opts);
   std::vector<QueryRun> queries;
   if (!args.query.empty()) {

@@ -104,6 +104,8 @@ struct AnchorEdge {
   uint32_t la, lb;               // labels of query endpoints a, b
   uint32_t elab;                 // query edge label (kNone: unlabelled)
   uint32_t prog;                 // EdgeProg index
+  uint32_t mult[2];              // per orientation (0: a->u, 1: a->v): matches each found one stands for
+                                 // (1 without coalescing; the orbit size / 0 with exact coalescing, planner.hpp)
 };
 
 // One anchor: (update, query edge, orientation) with its level-2 driver length.
@@ -113,6 +115,7 @@ struct Task {
   uint32_t flip;
   uint32_t d;                    // level-2 driver range length (0 for 2-vertex queries)
   uint32_t base;                 // start of that range in the driver list (label sub-range)
+  uint32_t mult;                 // AnchorEdge::mult of this orientation
 };
 
 // One work unit: a chunk [begin, begin + chunk) of a task's level-2 driver.

@@ -93,6 +93,8 @@ struct QueryState {
   DBuf<uint64_t> colsize;
   DBuf<EdgeProg> progs;
   DBuf<AnchorEdge> anchors;
+  DBuf<AnchorEdge> anchors_co;   // exact coalescing: one directed edge per automorphism orbit (planner.hpp)
+  uint32_t coalesce_gain = 1;    // directed edges per searched one (diagnostics)
   std::vector<std::vector<uint32_t>> orders;
   std::vector<uint32_t> tails;  // EdgeProg::tail per query edge
   bool has_leaf = false;         // some program weights leaves of its last DFS level (memo in use)
@@ -769,7 +771,21 @@ struct bdsm_engine {
         leafsigs.push_back(ls);
       }
       const QEdge& qe = qs.q.edges[e];
-      anchors.push_back({qs.q.labels[qe.a], qs.q.labels[qe.b], qe.label, e});
+      anchors.push_back({qs.q.labels[qe.a], qs.q.labels[qe.b], qe.label, e, {1u, 1u}});
+    }
+    // exact coalesced search (bdsm_options.coalesce): the same programs, one
+    // anchored orientation per orbit of directed query edges, weighted by the
+    // orbit size
+    std::vector<AnchorEdge> anchors_co = anchors;
+    {
+      const std::vector<uint32_t> mult = directed_edge_orbits(qs.q);
+      uint32_t searched = 0;
+      for (size_t e = 0; e < anchors_co.size(); ++e) {
+        anchors_co[e].mult[0] = mult[2 * e];
+        anchors_co[e].mult[1] = mult[2 * e + 1];
+        searched += (mult[2 * e] != 0) + (mult[2 * e + 1] != 0);
+      }
+      qs.coalesce_gain = searched ? uint32_t(2 * anchors_co.size() / searched) : 1;
     }
     qs.has_leaf = !leafsigs.empty();
     qs.n_leafsig = uint32_t(leafsigs.size());
@@ -785,9 +801,12 @@ struct bdsm_engine {
                          stream));
     qs.progs.ensure(std::max<size_t>(progs.size(), 1));
     qs.anchors.ensure(std::max<size_t>(anchors.size(), 1));
+    qs.anchors_co.ensure(std::max<size_t>(anchors.size(), 1));
     if (!progs.empty()) {
       CK(cudaMemcpyAsync(qs.progs.p, progs.data(), sizeof(EdgeProg) * progs.size(), cudaMemcpyHostToDevice, stream));
       CK(cudaMemcpyAsync(qs.anchors.p, anchors.data(), sizeof(AnchorEdge) * anchors.size(),
+                         cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(qs.anchors_co.p, anchors_co.data(), sizeof(AnchorEdge) * anchors_co.size(),
                          cudaMemcpyHostToDevice, stream));
     }
     sync();
@@ -897,7 +916,8 @@ struct bdsm_engine {
     a.ups = ups.p;
     a.n_ups = n;
     a.dlab = dlab.p;
-    a.anchors = qs.anchors.p;
+    // materialised matches (--dump-matches) need every anchored orientation
+    a.anchors = opts.coalesce && !collect_cap ? qs.anchors_co.p : qs.anchors.p;
     a.n_anchor = uint32_t(qs.q.edges.size());
     a.progs = qs.progs.p;
     a.rows = qs.rows.p;
@@ -1051,6 +1071,7 @@ struct bdsm_engine {
     std::chrono::steady_clock::time_point t0;
     bdsm_batch_stats st{};
     uint32_t compactions = 0;
+    uint32_t reruns = 0;  // positive-phase reruns (work items regrown after the merge)
     int attempt = 0;
     bool full_sort = false;  // rerun with the 64-bit key sort (an id beyond the sorted bits)
   };
@@ -1063,7 +1084,9 @@ struct bdsm_engine {
     kev_used = 0;
     launches = 0;
     cub_calls = 0;
-    CK(cudaEventRecord(ev[0], stream));
+    // ms_device spans every attempt of the batch (first attempt's start to the
+    // last event of the last attempt or rerun), host-side regrowth included
+    if (pend.attempt == 0) CK(cudaEventRecord(ev[0], stream));
     if (!device_input) {
       CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
       pend.st.h2d_bytes = n * sizeof(bdsm_update);
@@ -1337,6 +1360,8 @@ struct bdsm_engine {
     pend.st.touched = b.n_touched;
     pend.st.relocations = b.relocations;
     pend.st.compactions = pend.compactions;
+    pend.st.attempts = uint32_t(pend.attempt + 1);
+    pend.st.reruns = pend.reruns;
     pend.st.timed_out = tmask;
     pend.st.d2h_bytes = st_bytes;
     pend.st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pend.t0).count();
@@ -1364,6 +1389,8 @@ struct bdsm_engine {
     run_phase(n, 1);
     launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
     CK(cudaMemcpyAsync(h_st, d_st, st_bytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ev[5], stream));
+    ++pend.reruns;
     sync();
     if (h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
   }
@@ -1462,7 +1489,6 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
       if (o.chunk == 0) o.chunk = 32;
       if (o.shard_world == 0) o.shard_world = 1;
     }
-    if (o.coalesce) throw std::invalid_argument("coalesced search is not supported: it is not exact in the reference (SURVEY.md F1)");
     if (o.shard_rank >= o.shard_world) throw std::invalid_argument("shard_rank must be < shard_world");
     if (o.chunk % 8 != 0) throw std::invalid_argument("chunk must be a multiple of 8");
     e->opts = o;
@@ -1664,6 +1690,24 @@ int bdsm_plan_order(const bdsm_query_desc* query, const uint64_t* column_sizes, 
     return BDSM_OK;
   });
   return st == BDSM_OK ? r : -int(st);
+}
+
+int64_t bdsm_plan_edge_orbits(const bdsm_query_desc* query, uint32_t* mult) {
+  int64_t r = -int64_t(BDSM_INVALID_ARGUMENT);
+  bdsm_status st = guarded([&]() -> bdsm_status {
+    if (!query || !mult) throw std::invalid_argument("null argument");
+    std::vector<uint32_t> labels(query->vertex_labels, query->vertex_labels + query->num_vertices);
+    std::vector<QEdge> edges;
+    for (uint32_t i = 0; i < query->num_edges; ++i)
+      edges.push_back({query->a[i], query->b[i], query->edge_labels ? query->edge_labels[i] : kNone});
+    HostQuery q(std::move(labels), std::move(edges));
+    const std::vector<uint32_t> m = directed_edge_orbits(q);
+    std::copy(m.begin(), m.end(), mult);
+    std::vector<std::vector<uint32_t>> autos;
+    r = automorphisms(q, 20000, autos) ? int64_t(autos.size()) : 0;
+    return BDSM_OK;
+  });
+  return st == BDSM_OK ? r : -int64_t(st);
 }
 
 int bdsm_engine_tail(bdsm_engine* engine, int query, uint32_t edge) {

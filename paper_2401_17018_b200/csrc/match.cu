@@ -93,8 +93,8 @@ __device__ __forceinline__ void for_each_anchor(const PhaseArgs& a, uint32_t i, 
   for (uint32_t e = 0; e < a.n_anchor; ++e) {
     AnchorEdge ae = a.anchors[e];
     if (ae.elab != el) continue;
-    if (ae.la == lu && ae.lb == lv) f(ae.prog, 0u, up);
-    if (ae.la == lv && ae.lb == lu) f(ae.prog, 1u, up);
+    if (ae.mult[0] && ae.la == lu && ae.lb == lv) f(ae.prog, 0u, up, ae.mult[0]);
+    if (ae.mult[1] && ae.la == lv && ae.lb == lu) f(ae.prog, 1u, up, ae.mult[1]);
   }
 }
 
@@ -104,7 +104,7 @@ __global__ void k_anchor_count(PhaseArgs a) {
     uint32_t nt = 0, ni = 0;
     uint64_t cost = 0;
     if (i < a.n_ups) {
-      for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up) {
+      for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up, uint32_t) {
         ++nt;
         if (a.qn <= 2) {
           cost += 1;
@@ -198,10 +198,10 @@ __global__ void k_anchor_emit(PhaseArgs a) {
     const AnchorCount off = a.self_scan ? self_off : a.upd_off[i];
     uint32_t t = off.tasks, it = off.items;
     uint64_t c = off.cost;
-    for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up) {
+    for_each_anchor(a, i, [&](uint32_t prog, uint32_t flip, const bdsm_update_dev& up, uint32_t mult) {
       if (a.qn <= 2) {
         uint32_t owner = a.shard_world > 1 ? uint32_t((unsigned __int128)c * a.shard_world / total_cost) : 0;
-        if (owner == a.shard_rank) ++direct;
+        if (owner == a.shard_rank) direct += mult;
         if (owner == a.shard_rank && a.match_out) {  // materialise the 2-vertex match
           const EdgeProg& p = a.progs[prog];
           const unsigned long long k = atomicAdd(a.match_count, 1ull);
@@ -210,14 +210,14 @@ __global__ void k_anchor_emit(PhaseArgs a) {
             a.match_out[k * 2 + p.order[1]] = flip ? up.u : up.v;
           }
         }
-        a.tasks[t++] = Task{i, prog, flip, 0, 0};
+        a.tasks[t++] = Task{i, prog, flip, 0, 0, mult};
         c += 1;
         return;
       }
       const EdgeProg& p = a.progs[prog];
       uint32_t m0 = flip ? up.v : up.u, m1 = flip ? up.u : up.v, base, d;
       level2_range(p, m0, m1, a.g, &base, &d);
-      a.tasks[t] = Task{i, prog, flip, d, base};
+      a.tasks[t] = Task{i, prog, flip, d, base, mult};
       // level-2 GenCandidates call of this anchor (SURVEY.md §8(d) B_phase)
       uint32_t bm = p.lv[2].backmask;
       if (bm & 1u) bytes += 4ull * a.g.deg[m0];
@@ -1147,7 +1147,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
           }
           // per-lane accumulators, summed across the warp once at the end
           unsigned long long* la = s_lacc[w][lane];
-          la[0] += prod;
+          la[0] += prod * task.mult;
           la[1] += vis;
           la[2] += bb;
           la[3] += cc;
@@ -1164,7 +1164,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
           const unsigned long long pm = __popc(m);
           if (pm && lane == 0) {
             const TailFactor tf = s_tail[w];
-            stat[0] += pm * tf.f;
+            stat[0] += pm * tf.f * task.mult;
             stat[1] += pm * tf.v;
             stat[2] += pm * tf.b;
             stat[3] += pm * tf.c;

@@ -175,6 +175,81 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
   return p;
 }
 
+namespace {
+
+// Backtracking over label-, degree- and edge-label-preserving vertex
+// permutations, adjacency checked against every vertex already mapped (the
+// pruning of the reference's automorphism_backtrack, src/query_analysis.cpp:43-80).
+void auto_backtrack(const HostQuery& q, std::vector<uint32_t>& image, uint32_t used, uint32_t depth,
+                    std::vector<std::vector<uint32_t>>& out, size_t limit, bool& truncated) {
+  if (truncated) return;
+  if (depth == q.n) {
+    if (out.size() >= limit) {
+      truncated = true;
+      return;
+    }
+    out.push_back(image);
+    return;
+  }
+  for (uint32_t c = 0; c < q.n; ++c) {
+    if ((used >> c) & 1u) continue;
+    if (q.labels[c] != q.labels[depth] || q.degree[c] != q.degree[depth]) continue;
+    bool ok = true;
+    for (uint32_t j = 0; j < depth && ok; ++j) {
+      const bool e0 = q.adjacent(depth, j), e1 = q.adjacent(c, image[j]);
+      ok = e0 == e1 && (!e0 || q.edge_label(depth, j) == q.edge_label(c, image[j]));
+    }
+    if (!ok) continue;
+    image[depth] = c;
+    auto_backtrack(q, image, used | (1u << c), depth + 1, out, limit, truncated);
+    if (truncated) return;
+  }
+}
+
+}  // namespace
+
+bool automorphisms(const HostQuery& q, size_t limit, std::vector<std::vector<uint32_t>>& out) {
+  out.clear();
+  std::vector<uint32_t> image(q.n, 0);
+  bool truncated = false;
+  auto_backtrack(q, image, 0, 0, out, limit, truncated);
+  return !truncated;
+}
+
+std::vector<uint32_t> directed_edge_orbits(const HostQuery& q, size_t limit) {
+  const size_t m = q.edges.size();
+  std::vector<uint32_t> mult(2 * m, 1);
+  std::vector<std::vector<uint32_t>> autos;
+  if (!automorphisms(q, limit, autos)) return mult;  // too symmetric to enumerate: every edge its own orbit
+  auto dir_index = [&](uint32_t x, uint32_t y) -> uint32_t {
+    for (uint32_t e = 0; e < m; ++e) {
+      if (q.edges[e].a == x && q.edges[e].b == y) return 2 * e;
+      if (q.edges[e].a == y && q.edges[e].b == x) return 2 * e + 1;
+    }
+    throw std::logic_error("automorphism does not preserve the edge set");
+  };
+  // union-find over directed edges d = 2e + flip, flip 0 = (a, b), 1 = (b, a)
+  std::vector<uint32_t> parent(2 * m);
+  for (uint32_t d = 0; d < 2 * m; ++d) parent[d] = d;
+  auto find = [&](uint32_t d) {
+    while (parent[d] != d) d = parent[d] = parent[parent[d]];
+    return d;
+  };
+  for (const auto& phi : autos) {
+    for (uint32_t e = 0; e < m; ++e) {
+      const uint32_t x = q.edges[e].a, y = q.edges[e].b;
+      const uint32_t fwd = find(2 * e), f2 = find(dir_index(phi[x], phi[y]));
+      const uint32_t rev = find(2 * e + 1), r2 = find(dir_index(phi[y], phi[x]));
+      parent[std::max(fwd, f2)] = std::min(fwd, f2);
+      const uint32_t rr = find(rev), rr2 = find(r2);
+      parent[std::max(rr, rr2)] = std::min(rr, rr2);
+    }
+  }
+  std::fill(mult.begin(), mult.end(), 0u);
+  for (uint32_t d = 0; d < 2 * m; ++d) ++mult[find(d)];
+  return mult;
+}
+
 void shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners) {
   if (world <= 1) {
     std::fill(owners, owners + n, 0u);

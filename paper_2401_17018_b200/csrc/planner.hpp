@@ -55,6 +55,23 @@ EdgeProg build_program(const HostQuery& q, uint32_t query_index, const std::vect
                        const std::vector<std::pair<uint32_t, uint32_t>>& label_range,
                        const std::vector<uint32_t>& label_class);
 
+// Automorphisms of q (vertex permutations preserving labels, adjacency and
+// edge labels), at most `limit` (the reference's KDegenOptions limit is
+// 20,000, include/bdsm/query_analysis.hpp:42-45); false when truncated.
+bool automorphisms(const HostQuery& q, size_t limit, std::vector<std::vector<uint32_t>>& out);
+
+// Exact coalescing.  Directed query edge d = 2e + flip
+// (flip 0: (a, b), 1: (b, a)) anchors the matches M with M(d) = the update's
+// (u, v).  For an automorphism phi, M -> M o phi^-1 maps the matches anchored
+// at d one-to-one onto those anchored at phi(d), with the same image edge set
+// (so the same lowest-order decision, src/matcher.cpp:110-117).  Counting one
+// representative per orbit of directed edges and multiplying by the orbit
+// size therefore equals the coalesce-off count on every batch (unlike the
+// reference's coalesced_expand).  Returns mult[d] = orbit size
+// for the representative (lowest d) of each orbit, 0 for the others; all 1
+// when the automorphisms exceed `limit`.
+std::vector<uint32_t> directed_edge_orbits(const HostQuery& q, size_t limit = 20000);
+
 // Canonical split of work units over ranks: owner = floor(world * prefix / total).
 void shard_owners(const uint64_t* costs, size_t n, uint32_t world, uint32_t* owners);
 

@@ -113,3 +113,17 @@ def test_cli_batch_error(tmp_path):
     r = subprocess.run([CLI, "run", "--graph", g, "--query", q, "--stream", str(s), "--out", str(tmp_path / "o")],
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 1 and r.stderr.startswith("error: batch rejected: 1 invalid update(s)"), r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gen_sparse_mixed", "gen_sparse50_mixed", "gen_dense_delete", "fig1_s3"])
+def test_cli_exact_coalescing_matches_reference(name, tmp_path):
+    """`--coalesce on` runs the exact coalesced search: the reference's
+    coalesce-off deltas (the reference's own coalesced search misses matches)."""
+    meta = case(name)
+    out = str(tmp_path / "out")
+    r = subprocess.run([CLI, "run"] + cli_args(name, meta, out) + ["--coalesce", "on"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == meta["summary"].replace("OUT/", out + "/")
+    assert read(os.path.join(out, "deltas.csv")) == read(os.path.join(GOLD, name, "ref", "deltas.csv"))

@@ -394,3 +394,71 @@ def test_deadline_marks_query_unsolved():
     assert r.positive[q0] == 0 and r.negative[q0] == 0
     assert (r.positive[q1], r.negative[q1]) == (inst["expect"][0]["pos"], inst["expect"][0]["neg"])
     e.close()
+
+
+@pytest.mark.parametrize("suite", gu.SUITES)
+def test_exact_coalescing_equals_reference(suite):
+    """Exact coalesced search: one anchored orientation per
+    automorphism orbit of directed query edges, weighted by the orbit size;
+    the counts must equal the reference's coalesce-off counts on every batch
+    (the reference's own coalesced search misses matches, F1)."""
+    for inst in gu.load(suite):
+        e, batches = _engine(inst, coalesce=True)
+        for bi, (b, exp) in enumerate(zip(batches, inst["expect"])):
+            r = e.match_batch(b)
+            assert (r.positive[0], r.negative[0]) == (exp["pos"], exp["neg"]), (inst["name"], bi)
+        e.close()
+
+
+def test_exact_coalescing_unlabelled_cliques_and_cycles():
+    """Symmetric unlabelled queries (the C5 sweep shapes): coalesced == plain on
+    a random mixed stream, with 20x / 10x fewer anchored searches."""
+    import numpy as np
+    import paper_2401_17018_b200 as bd
+    rng = np.random.default_rng(11)
+    V, E = 400, 6000
+    pairs = set()
+    while len(pairs) < E:
+        a, b = (int(x) for x in rng.integers(0, V, 2))
+        if a != b:
+            pairs.add((min(a, b), max(a, b)))
+    pairs = sorted(pairs)
+    eu = np.array([p[0] for p in pairs], np.uint32)
+    ev = np.array([p[1] for p in pairs], np.uint32)
+    vl = np.zeros(V, np.uint32)
+    queries = [[(i, j) for i in range(4) for j in range(i + 1, 4)],  # K4
+               [(i, (i + 1) % 5) for i in range(5)],                 # C5
+               [(0, 1), (1, 2), (2, 3), (3, 0), (0, 2)]]             # diamond
+    plain = bd.Engine(vl, eu, ev)
+    co = bd.Engine(vl, eu, ev, coalesce=True)
+    o = Oracle(vl, eu, ev)
+    for qe in queries:
+        n = max(max(x) for x in qe) + 1
+        plain.add_query([0] * n, qe)
+        co.add_query([0] * n, qe)
+        o.add_query([0] * n, qe)
+    present = set(pairs)
+    for _ in range(3):
+        batch, used = [], set()
+        while len(batch) < 60:
+            if rng.random() < 0.4:
+                k = pairs[int(rng.integers(0, len(pairs)))]
+                if k not in present or k in used:
+                    continue
+                batch.append((1, k[0], k[1]))
+            else:
+                a, b = (int(x) for x in rng.integers(0, V, 2))
+                k = (min(a, b), max(a, b))
+                if a == b or k in present or k in used:
+                    continue
+                batch.append((0, a, b))
+            used.add((min(batch[-1][1], batch[-1][2]), max(batch[-1][1], batch[-1][2])))
+        rp, rc = plain.match_batch(batch), co.match_batch(batch)
+        exp = o.apply_batch(batch)
+        assert (rc.positive, rc.negative) == (rp.positive, rp.negative) == (exp[0], exp[1])
+        assert rc.stats["tasks"] < rp.stats["tasks"]
+        for op, a, b in batch:
+            k = (min(a, b), max(a, b))
+            (present.add if op == 0 else present.discard)(k)
+    plain.close()
+    co.close()

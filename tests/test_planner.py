@@ -82,3 +82,44 @@ def test_disconnected_query_rejected():
     cs = np.ones(3, np.uint64)
     out = np.zeros(32, np.uint32)
     assert L.bdsm_plan_order(C.byref(d), cs.ctypes.data, 0, out.ctypes.data, None) == -2
+
+
+def _orbits(labels, edges):
+    import paper_2401_17018_b200 as bd
+    return bd.plan_edge_orbits(labels, edges)
+
+
+def test_edge_orbits_known_groups():
+    """Exact coalescing plan: orbits of directed query edges under Aut(Q)."""
+    k5 = [(i, j) for i in range(5) for j in range(i + 1, 5)]
+    mult, n_aut = _orbits([0] * 5, k5)
+    assert n_aut == 120 and sorted(m for m in mult if m) == [20]  # S5: one orbit of all 20
+    c5 = [(i, (i + 1) % 5) for i in range(5)]
+    mult, n_aut = _orbits([0] * 5, c5)
+    assert n_aut == 10 and sorted(m for m in mult if m) == [10]   # D5
+    # path a-b-c with equal labels: swapping a, c; orbits {(a,b),(c,b)}, {(b,a),(b,c)}
+    mult, n_aut = _orbits([7, 7, 7], [(0, 1), (1, 2)])
+    assert n_aut == 2 and mult == [2, 2, 0, 0]
+    # labels break the symmetry: every directed edge searched once
+    mult, n_aut = _orbits([1, 2, 3], [(0, 1), (1, 2)])
+    assert n_aut == 1 and mult == [1, 1, 1, 1]
+    # Fig. 1 query (labels A, B, B, C): u1/u2 are not interchangeable (u3 hangs on u1)
+    mult, n_aut = _orbits([1, 2, 2, 4], [(0, 1), (0, 2), (1, 2), (1, 3)])
+    assert n_aut == 1 and all(m == 1 for m in mult)
+    # a triangle with one distinct label: swap of the two equal ones
+    mult, n_aut = _orbits([1, 1, 2], [(0, 1), (1, 2), (0, 2)])
+    assert n_aut == 2 and sum(mult) == 6 and max(mult) == 2
+
+
+def test_edge_orbits_partition_every_direction():
+    import random
+    rng = random.Random(5)
+    for _ in range(200):
+        n = rng.randint(2, 7)
+        edges = [(rng.randrange(i), i) for i in range(1, n)]
+        extra = [(i, j) for i in range(n) for j in range(i + 1, n) if (i, j) not in edges and rng.random() < 0.3]
+        edges += extra
+        labels = [rng.randrange(2) for _ in range(n)]
+        mult, n_aut = _orbits(labels, edges)
+        assert sum(mult) == 2 * len(edges)
+        assert n_aut >= 1

@@ -101,22 +101,30 @@ def rmat_graph(scale: int, E: int, seed: int, device, probs=(0.57, 0.19, 0.19, 0
         mult *= 1.5
 
 
+def _host_cdf(V: int, E: int, dmax: int, gamma: float) -> np.ndarray:
+    """Chung-Lu endpoint CDF: power-law expected degrees w_i ~ (i+1)^(-1/(gamma-1)),
+    scaled to mean 2E/V under the cap dmax; float64 on the host (sequential sums)."""
+    alpha = 1.0 / (gamma - 1.0)
+    w = (np.arange(V, dtype=np.float64) + 1.0) ** (-alpha)
+    target = 2.0 * E / V
+    for _ in range(50):  # scale to the mean degree under the cap
+        w = w * (target * V / float(w.sum()))
+        w = np.minimum(w, float(dmax))
+        if abs(float(w.sum()) / V - target) < 1e-3 * target:
+            break
+    cdf = np.cumsum(w)
+    return cdf / cdf[-1]
+
+
 def chung_lu_graph(V: int, E: int, seed: int, device, dmax: int, gamma: float):
     """Power-law expected degrees w_i ~ (i+i0)^(-1/(gamma-1)), mean 2E/V, capped
     at dmax; one guaranteed edge per vertex (no isolated vertices), the rest
     sampled with both endpoints proportional to w; ids randomly permuted."""
     g = _gen(seed, device)
-    alpha = 1.0 / (gamma - 1.0)
-    i = torch.arange(V, dtype=torch.float64, device=device)
-    w = (i + 1.0) ** (-alpha)
-    target = 2.0 * E / V
-    for _ in range(50):  # scale to the mean degree under the cap
-        w = w * (target * V / float(w.sum()))
-        w = torch.clamp(w, max=float(dmax))
-        if abs(float(w.sum()) / V - target) < 1e-3 * target:
-            break
-    cdf = torch.cumsum(w, 0)
-    cdf = (cdf / cdf[-1]).to(torch.float64)
+    # weights and CDF on the host: numpy's sequential float64 sums are
+    # reproducible across devices and boxes, a device scan's association
+    # order is not (and the CDF decides every endpoint draw)
+    cdf = torch.from_numpy(_host_cdf(V, E, dmax, gamma)).to(device)
     perm = torch.randperm(V, generator=g, device=device)
 
     def draw(n):
@@ -148,20 +156,7 @@ def chung_lu_keys(V: int, E: int, seed: int, device, dmax: int, gamma: float, ch
     removed, so exactly E edges.  Returns the sorted int64 keys (one array of
     8 B per edge instead of the per-step copies of the small-shape path)."""
     g = _gen(seed, device)
-    alpha = 1.0 / (gamma - 1.0)
-    # weights and CDF on the host: numpy's sequential float64 sums are
-    # reproducible, a device scan's association order is not (and the CDF
-    # decides every endpoint draw)
-    w = (np.arange(V, dtype=np.float64) + 1.0) ** (-alpha)
-    target = 2.0 * E / V
-    for _ in range(50):
-        w = w * (target * V / float(w.sum()))
-        w = np.minimum(w, float(dmax))
-        if abs(float(w.sum()) / V - target) < 1e-3 * target:
-            break
-    cdf_h = np.cumsum(w)
-    cdf = torch.from_numpy(cdf_h / cdf_h[-1]).to(device)
-    del w, cdf_h
+    cdf = torch.from_numpy(_host_cdf(V, E, dmax, gamma)).to(device)
     perm = torch.randperm(V, generator=g, device=device)
 
     def keys_of(u, v):
