@@ -137,8 +137,10 @@ class Engine {
 
   // Pipelined match_batch (run_pipeline's stage overlap, src/bench.cpp:370-564):
   // submit returns once the batch is enqueued; wait returns its counts.
-  void submit(const std::vector<EdgeUpdate>& batch) {
-    const std::vector<bdsm_update> ups = pack(batch);
+  void submit(const std::vector<EdgeUpdate>& batch) { submit_packed(pack(batch)); }
+  // the same with a batch already packed (so the caller can pack batch i+1
+  // while batch i runs)
+  void submit_packed(const std::vector<bdsm_update>& ups) {
     check(bdsm_engine_submit_batch(e_, ups.data(), ups.size()));
   }
   std::vector<Counts> wait(bdsm_batch_stats* stats = nullptr) {
@@ -189,7 +191,6 @@ class Engine {
   std::size_t query_count() const { return nq_; }
   bdsm_engine* handle() { return e_; }
 
- private:
   static std::vector<bdsm_update> pack(const std::vector<EdgeUpdate>& batch) {
     std::vector<bdsm_update> ups;
     ups.reserve(batch.size());
@@ -198,6 +199,8 @@ class Engine {
                      u.is_insert() && u.edge_label ? *u.edge_label : BDSM_NO_LABEL});
     return ups;
   }
+
+ private:
   std::vector<Counts> counts(const std::vector<std::uint64_t>& pos, const std::vector<std::uint64_t>& neg) const {
     std::vector<Counts> out(nq_);
     for (std::size_t i = 0; i < nq_; ++i) out[i] = {pos[i], neg[i]};

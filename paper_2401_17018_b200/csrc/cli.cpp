@@ -250,7 +250,12 @@ int run(const Args& args) {
   };
   std::vector<Stage> stages;
   double busy = 0, total = 0;
-  for (std::size_t bi = 0; bi < stream.size(); ++bi) {
+  // run_pipeline (src/bench.cpp:370-564): by default the stages overlap —
+  // batch i+1 is packed on the host while batch i runs on the device, and
+  // batch i's report is written while batch i+1 runs (the reference's
+  // preprocess / match / postprocess threads); --no-pipeline runs them in turn.
+  const bool pipelined = !args.no_pipeline && stream.size() > 1;
+  auto prepare = [&](std::size_t bi) {  // deadlines and the live set of batch bi
     std::size_t live = 0;
     for (std::size_t i = 0; i < queries.size(); ++i) {
       // an unsolved query is no longer matched (src/bench.cpp:463-467); a live
@@ -260,10 +265,27 @@ int run(const Args& args) {
       ++live;
       engine.set_deadline(qid[i], std::max(args.timeout - queries[i].spent, 1e-9));
     }
+    (void)bi;
+    return live;
+  };
+  std::vector<bdsm_update> packed = stream.empty() ? std::vector<bdsm_update>() : Engine::pack(stream[0]);
+  std::size_t live = 0;
+  Clock::time_point t_submit;
+  double host_pre = 0;
+  if (!stream.empty()) {
+    live = prepare(0);
+    t_submit = Clock::now();
+    engine.submit_packed(packed);
+  }
+  for (std::size_t bi = 0; bi < stream.size(); ++bi) {
+    // preprocess stage of batch bi+1, overlapped with batch bi on the device
+    std::vector<bdsm_update> next;
+    auto tp = Clock::now();
+    if (pipelined && bi + 1 < stream.size()) next = Engine::pack(stream[bi + 1]);
+    host_pre = since(tp);
     bdsm_batch_stats st{};
-    auto t0 = Clock::now();
-    std::vector<bdsm::gpu::Counts> c = engine.match_batch(stream[bi], &st);
-    double wall = since(t0);
+    std::vector<bdsm::gpu::Counts> c = engine.wait(&st);
+    double wall = since(t_submit);
     Delta d;
     for (std::size_t i = 0; i < queries.size(); ++i) {
       QueryRun& q = queries[i];
@@ -288,9 +310,9 @@ int run(const Args& args) {
         q.plan_cols = now;
       }
     }
+    // the materialised matches of batch bi are read before batch bi+1 reuses the buffers
+    std::vector<std::string> dump;
     if (args.dump_matches) {  // src/bench.cpp:484-491 (format_match, src/matcher.cpp:391-398)
-      mkdirs(args.out);
-      std::ofstream mf(join(args.out, "matches_batch" + std::to_string(bi) + ".txt"));
       for (std::size_t i = 0; i < queries.size(); ++i) {
         if (!queries[i].solved) continue;
         const std::uint32_t n = std::uint32_t(queries[i].q.labels.size());
@@ -299,15 +321,34 @@ int run(const Args& args) {
           if (m.size() / std::max<std::uint32_t>(n, 1) > dump_cap)
             throw std::runtime_error("too many matches to dump (raise BDSM_DUMP_CAP)");
           for (std::size_t k = 0; k + n <= m.size(); k += n) {
-            mf << (phase ? '+' : '-');
-            for (std::uint32_t u = 0; u < n; ++u) mf << " u" << u << ":v" << m[k + u];
-            mf << '\n';
+            std::string line(1, phase ? '+' : '-');
+            for (std::uint32_t u = 0; u < n; ++u) line += " u" + std::to_string(u) + ":v" + std::to_string(m[k + u]);
+            dump.push_back(std::move(line));
           }
         }
       }
     }
+    // submit batch bi+1 before the postprocess stage of batch bi
+    if (bi + 1 < stream.size()) {
+      live = prepare(bi + 1);
+      if (!pipelined) {
+        auto tq = Clock::now();
+        next = Engine::pack(stream[bi + 1]);
+        host_pre = since(tq);
+      }
+      t_submit = Clock::now();
+      engine.submit_packed(next);
+    }
+    // postprocess stage of batch bi (overlapped with batch bi+1 when pipelined)
+    if (args.dump_matches) {
+      mkdirs(args.out);
+      std::ofstream mf(join(args.out, "matches_batch" + std::to_string(bi) + ".txt"));
+      for (const std::string& line : dump) mf << line << '\n';
+    }
     deltas.push_back(d);
-    stages.push_back({st.ms_update * 1e-3, (st.ms_negative + st.ms_positive) * 1e-3});
+    // preprocess = the graph update (device merge + refresh) and the host
+    // packing of the batch; match = the two matching phases (src/bench.cpp:394-402, :470)
+    stages.push_back({st.ms_update * 1e-3 + host_pre, (st.ms_negative + st.ms_positive) * 1e-3});
     busy += (st.ms_match_kernel + st.ms_merge_kernel) * 1e-3;
     total += wall;
   }
