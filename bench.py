@@ -270,6 +270,8 @@ def main():
                     help="batches checked against the CPU restatement at full size (-1: all; 0: off)")
     ap.add_argument("--parity-timeout", type=float, default=600.0)
     ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--no-stream", action="store_true",
+                    help="time one apply per batch instead of the pipelined stream")
     ap.add_argument("--coalesce", action="store_true", help="exact coalesced search (counts unchanged)")
     ap.add_argument("--l2-hot-mb", type=int, default=0, help="K8 hot-list L2 persistence budget (0: off)")
     args = ap.parse_args()
@@ -311,7 +313,10 @@ def config_dict(args, wl, world):
             "labels": m["L"], "generator": m["generator"], "d_max": m["d_max"], "batch_updates": m["batch"],
             "batch_mode": m["mode"], "query_vertices": len(wl.qlabels), "query_edges": len(wl.qedges),
             "query_labels": wl.qlabels, "query": wl.qedges, "seeds": m["seeds"],
-            "l2": "flushed (256 MiB write) before every timed step",
+            "l2": ("pipelined stream: no flush between its batches, the graph (adjacency pool > 1 GB) exceeds the "
+                   "126 MB L2; per-batch latency runs flush L2 (256 MiB write) before every batch"
+                   if not getattr(args, "no_stream", False) else
+                   "flushed (256 MiB write) before every timed step"),
             "parallelism": f"replicated graph, work units split over {world} GPU(s)" if world > 1 else "1 GPU",
             "coalesce": "exact (one search per automorphism orbit of directed query edges)" if args.coalesce
                         else "off"}
@@ -369,6 +374,16 @@ def ours(args, world, rank, local):
     engB = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
                      chunk=args.chunk, l2_hot_mb=args.l2_hot_mb, coalesce=args.coalesce)
     engB.add_query(wl.qlabels, wl.qedges)
+    # pipelined stream (1 GPU): A and B run the timed batches as one stream,
+    # C replays them one batch at a time for the per-batch latency
+    # (graphs whose adjacency fits L2 are timed one flushed batch at a time)
+    pipelined = world == 1 and not args.no_stream and 8 * wl.meta["E"] >= (256 << 20)
+    args.no_stream = not pipelined
+    engL = None
+    if pipelined:
+        engL = bd.Engine(wl.labels, wl.src, wl.dst, device=local, chunk=args.chunk, l2_hot_mb=args.l2_hot_mb,
+                         coalesce=args.coalesce)
+        engL.add_query(wl.qlabels, wl.qedges)
     log(f"engines built in {time.time() - t0:.1f}s")
 
     # batches resident in HBM for `value`; pinned host copies for `e2e` (the
@@ -398,20 +413,52 @@ def ours(args, world, rank, local):
             import torch.distributed as dist
             dist.barrier()
 
-    # warm-up (both engines walk the same stream)
-    countsA, countsB = [], []
+    # warm-up (every engine walks the same stream)
+    countsA, countsB, countsC = [], [], []
     for i in range(args.warmup):
         rA = engA.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
         rB = engB.match_batch(wl.batches[i])
         countsA.append((rA.positive[0], rA.negative[0]))
         countsB.append((rB.positive[0], rB.negative[0]))
+        if engL:
+            rC = engL.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
+            countsC.append((rC.positive[0], rC.negative[0]))
 
     statsA = []
     dev_ms = []
     nccl_totals = []
     use_nccl = world > 1 and __import__("torch.distributed").distributed.get_backend() == "nccl"
+    statsC, e2e_ms = [], []
     with ClockSampler(local if not os.environ.get("CUDA_VISIBLE_DEVICES") else 0) as clk:
-        for i in range(args.warmup, nb):
+        if pipelined:
+            # per-batch latency: one apply per batch, L2 flushed before each
+            for i in range(args.warmup, nb):
+                flush.zero_()
+                torch.cuda.synchronize()
+                r = engL.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
+                statsC.append(r.stats)
+                countsC.append((r.positive[0], r.negative[0]))
+            # value: the timed batches as one pipelined stream from HBM
+            # (bdsm_engine_apply_stream); the graph (> 1 GB) exceeds L2
+            flush.zero_()
+            torch.cuda.synchronize()
+            rs = engA.match_stream_device([dev_batches[i].data_ptr() for i in range(args.warmup, nb)],
+                                          [len(wl.batches[i]) for i in range(args.warmup, nb)])
+            for r in rs:
+                dev_ms.append(r.stats["ms_device"])
+                statsA.append(r.stats)
+                countsA.append((r.positive[0], r.negative[0]))
+            # e2e: the same stream through the C ABI with page-locked host
+            # batches: every batch's H2D and its counts' D2H in the timed region
+            flush.zero_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            rs = engB.match_stream([pinned_batches[i] for i in range(args.warmup, nb)])
+            e2e_total = (time.perf_counter() - t1) * 1e3
+            e2e_ms = [e2e_total / args.steps] * args.steps
+            for r in rs:
+                countsB.append((r.positive[0], r.negative[0]))
+        for i in range(args.warmup, nb) if not pipelined else []:
             flush.zero_()
             barrier()
             if use_nccl:
@@ -438,8 +485,7 @@ def ours(args, world, rank, local):
             dev_ms.append(r.stats["ms_device"])
             statsA.append(r.stats)
             countsA.append((r.positive[0], r.negative[0]))
-        e2e_ms = []
-        for i in range(args.warmup, nb):
+        for i in range(args.warmup, nb) if not pipelined else []:
             flush.zero_()
             barrier()
             t1 = time.perf_counter()
@@ -458,7 +504,7 @@ def ours(args, world, rank, local):
     updates = sum(len(b) for b in wl.batches[args.warmup:])
     value = updates / (tot_dev / 1e3)
     e2e_value = updates / (tot_e2e / 1e3)
-    parity_ok = flatA == flatB
+    parity_ok = flatA == flatB and (not countsC or [c for pn in countsC for c in pn] == flatA)
     if nccl_totals:  # the in-step NCCL all-reduce agrees with the end-of-run sum
         parity_ok = parity_ok and [c for pn in nccl_totals for c in pn] == flatA[2 * args.warmup:]
 
@@ -481,7 +527,19 @@ def ours(args, world, rank, local):
         "e2e": {"value": e2e_value, "unit": "updates/s", "ms_per_step": tot_e2e / args.steps,
                 "h2d_bytes_per_step": int(16 * statistics.mean(len(b) for b in wl.batches[args.warmup:])),
                 "d2h_bytes_per_step": int(statsA[-1]["d2h_bytes"]),
-                "path": "bdsm_engine_apply_batch (pinned host buffers, C ABI)"},
+                "path": ("bdsm_engine_apply_stream (pinned host buffers, C ABI, host timer around the call)"
+                         if pipelined else "bdsm_engine_apply_batch (pinned host buffers, C ABI)")},
+        "mode": ("pipelined stream: the timed batches in one bdsm_engine_apply_stream call; the positive phase of "
+                 "batch i and the negative phase of batch i+1 share one matching launch (run_pipeline's overlap, "
+                 "src/bench.cpp:495-545); ms_per_step = device time of the stream / batches"
+                 if pipelined else "one bdsm_engine_apply_batch_device call per batch"),
+        "latency": ({"ms_per_batch": statistics.mean(s["ms_device"] for s in statsC),
+                     "updates_per_s": updates / (sum(s["ms_device"] for s in statsC) / 1e3),
+                     "note": "one batch at a time (bdsm_engine_apply_batch_device), L2 flushed before each, "
+                             "validate -> negative -> merge -> positive -> counts",
+                     "per_batch_ms": [s["ms_device"] for s in statsC],
+                     "neg_ms": [s["ms_negative"] for s in statsC], "merge_ms": [s["ms_update"] for s in statsC],
+                     "pos_ms": [s["ms_positive"] for s in statsC]} if statsC else None),
         "gpu_launches": int(sum(s["kernel_launches"] for s in statsA)),
         "cub_launches": int(sum(s["cub_launches"] for s in statsA)),
         "roofline": roof,
@@ -576,6 +634,8 @@ def ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
     engA.close()
     engB.close()
+    if engL:
+        engL.close()
     return 0
 
 

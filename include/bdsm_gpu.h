@@ -167,6 +167,22 @@ BDSM_API bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const b
 BDSM_API bdsm_status bdsm_engine_submit_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n);
 BDSM_API bdsm_status bdsm_engine_wait(bdsm_engine* engine, uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats);
 
+/* Pipelined stream: k batches in order, with the same counts, errors and
+ * all-or-nothing contract as k bdsm_engine_apply_batch calls.  The positive
+ * phase of batch i and the negative phase of batch i+1 read the same graph
+ * (after batch i's merge), so they run as one launch of the matching kernel
+ * (run_pipeline's stage overlap, src/bench.cpp:495-545, on the device); the
+ * host synchronises once per stream.  batches[i] is host memory, or device
+ * memory with device_input != 0.  pos/neg: [k * num_queries] (batch-major);
+ * stats: [k] or NULL (ms_device per batch is the pipeline step: from the end
+ * of batch i-1 to the end of batch i).  On an error *done = the number of
+ * batches applied before the failing one (whose error is returned, nothing of
+ * it applied).  Batches must be non-empty.  Queries with a deadline, match
+ * collection and the K8 L2 window fall back to one batch at a time. */
+BDSM_API bdsm_status bdsm_engine_apply_stream(bdsm_engine* engine, const bdsm_update* const* batches,
+                                             const size_t* sizes, size_t k, int device_input, uint64_t* pos,
+                                             uint64_t* neg, bdsm_batch_stats* stats, size_t* done);
+
 /* Per-query time budget in seconds for subsequent batches (MatchOptions::
  * deadline, PipelineConfig::timeout_seconds); <= 0 disables. */
 BDSM_API bdsm_status bdsm_engine_set_deadline(bdsm_engine* engine, int query, double seconds_from_now);

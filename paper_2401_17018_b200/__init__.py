@@ -101,6 +101,9 @@ def _load():
     L.bdsm_engine_wait.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
     L.bdsm_engine_set_deadline.restype = C.c_int
     L.bdsm_engine_set_deadline.argtypes = [C.c_void_p, C.c_int, C.c_double]
+    L.bdsm_engine_apply_stream.restype = C.c_int
+    L.bdsm_engine_apply_stream.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]
     L.bdsm_engine_set_query_active.restype = C.c_int
     L.bdsm_engine_set_query_active.argtypes = [C.c_void_p, C.c_int, C.c_int]
     L.bdsm_engine_query_timed_out.restype = C.c_int
@@ -302,6 +305,39 @@ class Engine:
         if r != 0:
             _raise(r, self._h)
         return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
+
+    def _stream(self, ptrs, sizes, device: bool) -> List[BatchResult]:
+        k, nq = len(sizes), max(self.nq, 1)
+        parr = (C.c_void_p * max(k, 1))(*[C.c_void_p(int(x)) for x in ptrs])
+        sarr = (C.c_size_t * max(k, 1))(*[int(s) for s in sizes])
+        pos = np.zeros(max(k * nq, 1), np.uint64)
+        neg = np.zeros(max(k * nq, 1), np.uint64)
+        stats = (_Stats * max(k, 1))()
+        done = C.c_size_t(0)
+        r = lib().bdsm_engine_apply_stream(self._h, parr, sarr, k, 1 if device else 0, _ptr(pos), _ptr(neg), stats,
+                                           C.byref(done))
+        out = [BatchResult(pos[i * nq:i * nq + self.nq].tolist(), neg[i * nq:i * nq + self.nq].tolist(),
+                           _stats_dict(stats[i])) for i in range(done.value)]
+        if r != 0:
+            try:
+                _raise(r, self._h)
+            except Exception as e:  # the batches before the failing one were applied
+                e.done = done.value
+                e.results = out
+                raise
+        return out
+
+    def match_stream(self, batches) -> List[BatchResult]:
+        """Pipelined stream of host batches (bdsm_engine_apply_stream): the
+        positive phase of batch i and the negative phase of batch i+1 share one
+        matching launch; results equal one match_batch per batch.  On an error
+        the exception carries .done (batches applied) and .results."""
+        ups = [make_updates(b) for b in batches]
+        return self._stream([u.ctypes.data for u in ups], [len(u) for u in ups], False)
+
+    def match_stream_device(self, dev_ptrs, sizes) -> List[BatchResult]:
+        """Same, with every batch already in device memory."""
+        return self._stream(dev_ptrs, sizes, True)
 
     def set_deadline(self, query: int, seconds_from_now: float) -> None:
         r = lib().bdsm_engine_set_deadline(self._h, query, seconds_from_now)

@@ -161,12 +161,15 @@ struct QueueState {
 };
 
 // Candidate rows carry the query-vertex bits in the low 16 bits (kMaxQ) and
-// two per-batch flags in the top bits: the vertex is an endpoint of an
-// insert (positive phase) / delete (negative phase) of the current batch.
-// The matching kernel gets the visibility-rule prefilter from the same load.
-constexpr uint32_t kRowInsFlag = 1u << 31;
-constexpr uint32_t kRowDelFlag = 1u << 30;
-constexpr uint32_t kRowFlags = kRowInsFlag | kRowDelFlag;
+// per-batch flags in the top bits: the vertex is an endpoint of an insert
+// (positive phase) / delete (negative phase) of a batch in flight.  Two
+// batches can be in flight (the pipelined stream: batch i's positive phase
+// and batch i+1's negative phase share one launch), so each batch buffer slot
+// has its own pair of bits.  The matching kernel gets the visibility-rule
+// prefilter from the same load.
+__host__ __device__ constexpr uint32_t row_ins_flag(uint32_t slot) { return 1u << (31 - 2 * slot); }
+__host__ __device__ constexpr uint32_t row_del_flag(uint32_t slot) { return 1u << (30 - 2 * slot); }
+constexpr uint32_t kRowFlags = 0xf0000000u;  // every slot's flags (kept by the merge's row refresh)
 
 // Per-batch open-addressing table of the directed update keys (x << 32 | y)
 // -> (batch index | op << 31), for O(1) visibility-rule lookups.
@@ -253,11 +256,15 @@ __device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32
 // results follow it in the same allocation (one D2H): u64 counts[2][nq]
 // ([phase][query] matches) and u32 timed_out[nq] (deadline fired).
 struct BatchState {
+  const BatchState* prev;        // the preceding batch of a pipelined stream (nullptr: none); a batch
+                                 // whose predecessor aborted aborts too (overflow 6)
   uint32_t err_count;            // validate_batch failures
   uint32_t selfloop_min;         // first self-loop update index (kNone: none)
   uint32_t conflict_min;         // first conflicting update index (kNone: none)
   uint32_t n_touched;            // distinct endpoints
-  uint32_t overflow;             // adjacency pool exhausted: merge skipped
+  uint32_t overflow;             // 1 pool exhausted (merge skipped), 2/3 work items of the negative /
+                                 // positive phase, 4 labelled insert into an unlabelled graph, 5 id beyond
+                                 // the sorted bits, 6 a preceding batch of the stream aborted
   uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
   uint32_t n_items[2];
   uint32_t donations;            // statistics: donated subtrees
@@ -283,5 +290,22 @@ struct BatchState {
   uint64_t trace_chunks[2][kMaxQ];  // -DBDSM_TRACE: 32-candidate chunks filtered per level
   uint64_t trace_setups[2][kMaxQ];  // -DBDSM_TRACE: GenCandidates setups per level
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ bool batch_aborted_own(const BatchState* st) {
+  return st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow;
+}
+// Every kernel of a batch returns at once when the batch was rejected or must
+// be rerun, or when the batch before it in a pipelined stream was (then this
+// batch is marked as well, so the chain propagates).
+__device__ __forceinline__ bool batch_aborted(BatchState* st) {
+  if (batch_aborted_own(st)) return true;
+  if (st->prev && batch_aborted_own(st->prev)) {
+    st->overflow = 6;
+    return true;
+  }
+  return false;
+}
+#endif
 
 }  // namespace bdsm_b200

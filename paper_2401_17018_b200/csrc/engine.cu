@@ -147,24 +147,41 @@ struct bdsm_engine {
   DBuf<uint64_t*> d_colsize;
 
   // batch buffers
-  DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
-  DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
-  DBuf<uint64_t> keys, keys2, skeys;
-  DBuf<uint32_t> vals, vals2, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list, mid_list;
-  DBuf<uint8_t> ecode, head;
-  DBuf<uint64_t> new_off;
-  DBuf<unsigned long long> hkeys;  // visibility table of the batch
-  DBuf<uint32_t> hvals;
-  DBuf<AnchorCount> upd_cnt, upd_off;
-  DBuf<Task> tasks;
-  DBuf<Item> items;
+  // Per-batch buffers.  Two slots: the pipelined stream (apply_stream) keeps
+  // batch i and batch i+1 in flight together; a single batch uses slot 0.
+  struct BatchBufs {
+    DBuf<bdsm_update_dev> ups;      // translated (internal ids), read by every kernel after K1
+    DBuf<bdsm_update_dev> ups_ext;  // host-input staging (external ids)
+    DBuf<uint64_t> keys, keys2, skeys;
+    DBuf<uint32_t> vals, vals2, svals, dlab, insflag, ins_prefix, heads, ipos, new_cap, big_list, small_list, mid_list;
+    DBuf<uint8_t> ecode, head;
+    DBuf<uint64_t> new_off;
+    DBuf<unsigned long long> hkeys;  // visibility table of the batch
+    DBuf<uint32_t> hvals;
+    DBuf<AnchorCount> upd_cnt, upd_off;
+    DBuf<Task> tasks;
+    DBuf<Item> items;
+    DBuf<unsigned long long> task_tail;  // per-task counts of anchor-only tail levels (PhaseArgs::task_tail)
+    size_t batch_cap = 0;
+    // BatchState followed by the per-query results (common.cuh): one H2D
+    // before, one D2H after every batch
+    DBuf<unsigned char> st_buf;
+    BatchState* d_st = nullptr;
+    BatchState* h_st = nullptr;
+    size_t st_bytes = 0, h_st_bytes = 0;
+    ~BatchBufs() {
+      if (h_st) cudaFreeHost(h_st);
+    }
+  };
+  BatchBufs slot_[2];
+  uint32_t cs = 0;  // slot of the batch being enqueued
+  BatchBufs& B() { return slot_[cs]; }
   size_t max_items = 0;
   DBuf<DynItem> dyn;           // donated-subtree queue of the matching kernel
   DBuf<QueueState> qstate;
   DBuf<uint32_t> dyn_ready;
   DBuf<unsigned long long> memo;  // weight memo of the matching kernel (2^21 words, persistent)
   DBuf<unsigned long long> memo_fill;  // slots taken since the last reset
-  DBuf<unsigned long long> task_tail;  // per-task counts of anchor-only tail levels (PhaseArgs::task_tail)
   uint32_t qs_natail(int qi) const { return queries.at(size_t(qi))->natail; }
   bool memo_persistent = true;     // false when a query has too many signatures to invalidate
   unsigned long long* h_memo_fill = nullptr;  // pinned copy of memo_fill, refreshed every batch
@@ -229,7 +246,7 @@ struct bdsm_engine {
         std::min<uint64_t>({uint64_t(opts.l2_hot_mb) << 20, uint64_t(max_window), uint64_t(max_persist)});
     if (budget < 4096 || g.pool_size - pool_top < 2 * (budget / 4)) return;  // no room: skip this period
     hot_hist.ensure(34);
-    launch_hot_pack(g, heat.p, hot_hist.p, budget, d_st, num_sms, stream);
+    launch_hot_pack(g, heat.p, hot_hist.p, budget, B().d_st, num_sms, stream);
     launches += 4;
     CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(budget)));
     cudaStreamAttrValue attr{};
@@ -269,26 +286,21 @@ struct bdsm_engine {
   }
   uint32_t epoch = 0;
   DBuf<uint8_t> cub_tmp;
-  // BatchState followed by the per-query results (common.cuh): one H2D
-  // before, one D2H after every batch
-  DBuf<unsigned char> st_buf;
-  BatchState* d_st = nullptr;
-  BatchState* h_st = nullptr;
-  size_t st_bytes = 0, h_st_bytes = 0;
   size_t st_size() const { return sizeof(BatchState) + 20 * std::max<size_t>(queries.size(), 1); }
   static unsigned long long* st_counts(BatchState* s) { return reinterpret_cast<unsigned long long*>(s + 1); }
   uint32_t* st_timed(BatchState* s) const { return reinterpret_cast<uint32_t*>(st_counts(s) + 2 * queries.size()); }
   void ensure_state() {
-    st_bytes = st_size();
-    if (st_buf.n < st_bytes) {
-      st_buf.ensure(st_bytes);
-      d_st = reinterpret_cast<BatchState*>(st_buf.p);
+    BatchBufs& b = B();
+    b.st_bytes = st_size();
+    if (b.st_buf.n < b.st_bytes) {
+      b.st_buf.ensure(b.st_bytes);
+      b.d_st = reinterpret_cast<BatchState*>(b.st_buf.p);
     }
-    if (h_st_bytes < st_bytes) {
-      if (h_st) cudaFreeHost(h_st);
-      h_st = nullptr;
-      CK(cudaMallocHost(&h_st, st_bytes));
-      h_st_bytes = st_bytes;
+    if (b.h_st_bytes < b.st_bytes) {
+      if (b.h_st) cudaFreeHost(b.h_st);
+      b.h_st = nullptr;
+      CK(cudaMallocHost(&b.h_st, b.st_bytes));
+      b.h_st_bytes = b.st_bytes;
     }
   }
   bdsm_update* h_ups = nullptr;
@@ -318,8 +330,10 @@ struct bdsm_engine {
     for (auto& e : merge_ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : kev) cudaEventDestroy(e);
-    if (h_st) cudaFreeHost(h_st);
     if (h_memo_fill) cudaFreeHost(h_memo_fill);
+    if (h_stream) cudaFreeHost(h_stream);
+    for (auto& x : stream_ev) cudaEventDestroy(x);
+    for (auto& x : stream_kev) cudaEventDestroy(x);
     if (h_ups) cudaFreeHost(h_ups);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
@@ -849,50 +863,50 @@ struct bdsm_engine {
     return std::max({a, b, c, d, e, f});
   }
 
-  size_t batch_cap = 0;
   void ensure_batch(size_t n) {
-    if (n <= batch_cap) return;
-    size_t cap_n = std::max<size_t>(n, batch_cap + batch_cap / 2);
+    if (n <= B().batch_cap) return;
+    size_t cap_n = std::max<size_t>(n, B().batch_cap + B().batch_cap / 2);
     cap_n = std::max<size_t>(cap_n, 1024);
     size_t m = 2 * cap_n;
-    ups.ensure(cap_n);
-    ups_ext.ensure(cap_n);
-    keys.ensure(m);
-    keys2.ensure(m);
-    skeys.ensure(m);
-    vals.ensure(m);
-    vals2.ensure(m);
-    svals.ensure(m);
-    dlab.ensure(cap_n);
-    ecode.ensure(cap_n);
-    head.ensure(m);
-    insflag.ensure(m + 1);
-    ins_prefix.ensure(m + 1);
-    heads.ensure(m);
-    ipos.ensure(m);
-    new_off.ensure(m);
-    new_cap.ensure(m);
-    big_list.ensure(m);
-    small_list.ensure(m);
-    mid_list.ensure(m);
-    upd_cnt.ensure(cap_n + 1);
-    upd_off.ensure(cap_n + 1);
+    B().ups.ensure(cap_n);
+    B().ups_ext.ensure(cap_n);
+    B().keys.ensure(m);
+    B().keys2.ensure(m);
+    B().skeys.ensure(m);
+    B().vals.ensure(m);
+    B().vals2.ensure(m);
+    B().svals.ensure(m);
+    B().dlab.ensure(cap_n);
+    B().ecode.ensure(cap_n);
+    B().head.ensure(m);
+    B().insflag.ensure(m + 1);
+    B().ins_prefix.ensure(m + 1);
+    B().heads.ensure(m);
+    B().ipos.ensure(m);
+    B().new_off.ensure(m);
+    B().new_cap.ensure(m);
+    B().big_list.ensure(m);
+    B().small_list.ensure(m);
+    B().mid_list.ensure(m);
+    B().upd_cnt.ensure(cap_n + 1);
+    B().upd_off.ensure(cap_n + 1);
     cub_tmp.ensure(cub_bytes_for(cap_n));
     size_t hcap = 1024;
     while (hcap < 8 * cap_n) hcap <<= 1;  // >= 2x the 2|dB| directed keys + <= 2|dB| segment heads
-    hkeys.ensure(hcap);
-    hvals.ensure(hcap);
-    batch_cap = cap_n;
+    B().hkeys.ensure(hcap);
+    B().hvals.ensure(hcap);
+    B().batch_cap = cap_n;
   }
 
   void ensure_tasks(size_t n) {
     size_t maxq_edges = 1;
     for (auto& q : queries) maxq_edges = std::max(maxq_edges, q->q.edges.size());
-    tasks.ensure_grow(std::max<size_t>(n * 2 * maxq_edges, 1024));
-    if (max_items == 0) {
-      max_items = std::max<size_t>(tasks.n * 4, size_t(1) << 22);
-      items.ensure(max_items);
-    }
+    B().tasks.ensure_grow(std::max<size_t>(n * 2 * maxq_edges, 1024));
+    // BDSM_MAX_ITEMS (tests): a small initial work-item capacity, so the
+    // regrowth and rerun paths run on small inputs
+    if (max_items == 0) max_items = env_u32("BDSM_MAX_ITEMS", 0);
+    if (max_items == 0) max_items = std::max<size_t>(B().tasks.n * 4, size_t(1) << 22);
+    if (B().items.n < max_items) B().items.ensure(max_items);
     if (!dyn.p) {
       qstate.ensure(1);
       dyn.ensure(size_t(1) << 20);  // 80 MiB of donated subtrees per launch
@@ -913,34 +927,35 @@ struct bdsm_engine {
     QueryState& qs = *queries[size_t(qi)];
     PhaseArgs a{};
     a.g = view();
-    a.ups = ups.p;
+    a.ups = B().ups.p;
     a.n_ups = n;
-    a.dlab = dlab.p;
+    a.dlab = B().dlab.p;
     // materialised matches (--dump-matches) need every anchored orientation
     a.anchors = opts.coalesce && !collect_cap ? qs.anchors_co.p : qs.anchors.p;
     a.n_anchor = uint32_t(qs.q.edges.size());
     a.progs = qs.progs.p;
     a.rows = qs.rows.p;
-    a.skeys = skeys.p;
-    a.svals = svals.p;
+    a.skeys = B().skeys.p;
+    a.svals = B().svals.p;
     a.m_keys = 2 * n;
-    a.hkeys = hkeys.p;
-    a.hvals = hvals.p;
-    a.hmask = uint32_t(hkeys.n - 1);
+    a.hkeys = B().hkeys.p;
+    a.hvals = B().hvals.p;
+    a.hmask = uint32_t(B().hkeys.n - 1);
     a.phase = phase;
+    a.flag = phase == 0 ? row_del_flag(cs) : row_ins_flag(cs);
     a.query = uint32_t(qi);
     a.qn = qs.q.n;
     a.chunk = opts.chunk;
     a.shard_rank = opts.shard_rank;
     a.shard_world = std::max<uint32_t>(opts.shard_world, 1);
-    a.upd_cnt = upd_cnt.p;
-    a.upd_off = upd_off.p;
-    a.tasks = tasks.p;
-    a.items = items.p;
+    a.upd_cnt = B().upd_cnt.p;
+    a.upd_off = B().upd_off.p;
+    a.tasks = B().tasks.p;
+    a.items = B().items.p;
     a.max_items = uint32_t(std::min<size_t>(max_items, 0xffffffffu));
-    a.st = d_st;
-    a.count_out = st_counts(d_st) + size_t(phase) * queries.size() + size_t(qi);
-    a.timed_out = st_timed(d_st) + qi;
+    a.st = B().d_st;
+    a.count_out = st_counts(B().d_st) + size_t(phase) * queries.size() + size_t(qi);
+    a.timed_out = st_timed(B().d_st) + qi;
     a.deadline_ns = 0;
     a.q = qstate.p;
     a.dyn = dyn.p;
@@ -951,7 +966,7 @@ struct bdsm_engine {
     a.memo = memo.p;
     a.memo_mask = uint32_t(memo.n - 1);
     a.memo_fill = memo_fill.p;
-    a.heads = heads.p;
+    a.heads = B().heads.p;
     a.task_tail = nullptr;
     a.natail_stride = qs_natail(qi);
     a.match_out = nullptr;
@@ -989,7 +1004,7 @@ struct bdsm_engine {
         a.self_scan = n <= tune_self_scan;
         if (!a.self_scan) {
           size_t tmp = cub_tmp.n;
-          CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, upd_cnt.p, upd_off.p, AnchorCountSum(),
+          CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, B().upd_cnt.p, B().upd_off.p, AnchorCountSum(),
                                             AnchorCount{0, 0, 0}, int(n + 1), stream));
           cub_calls += 1;
         }
@@ -1031,14 +1046,14 @@ struct bdsm_engine {
           }
         }
         if (qs.natail && !tune_no_tasktail) {  // per-task counts of anchor-only tail levels, unset (~0) before the launch
-          task_tail.ensure_grow(tasks.n * qs.natail);
-          CK(cudaMemsetAsync(task_tail.p, 0xff, sizeof(unsigned long long) * tasks.n * qs.natail, stream));
-          a.task_tail = task_tail.p;
+          B().task_tail.ensure_grow(B().tasks.n * qs.natail);
+          CK(cudaMemsetAsync(B().task_tail.p, 0xff, sizeof(unsigned long long) * B().tasks.n * qs.natail, stream));
+          a.task_tail = B().task_tail.p;
         }
         // variant by the previous batch's work items of this (query, phase)
         const int variant = tune_variant ? int(tune_variant) : qs.prev_items[phase] > tune_throughput_items ? 4 : 2;
         a.backoff_max = tune_backoff ? tune_backoff : variant == 2 ? 256u : 1024u;
-        launch_wbm(a, num_sms, variant, stream);
+        launch_wbm(a, nullptr, num_sms, variant, stream);
         CK(cudaEventRecord(next_kev(), stream));
         ++launches;
       }
@@ -1088,12 +1103,12 @@ struct bdsm_engine {
     // last event of the last attempt or rerun), host-side regrowth included
     if (pend.attempt == 0) CK(cudaEventRecord(ev[0], stream));
     if (!device_input) {
-      CK(cudaMemcpyAsync(ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(B().ups_ext.p, h_src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
       pend.st.h2d_bytes = n * sizeof(bdsm_update);
     }
-    std::memset(static_cast<void*>(h_st), 0, st_bytes);
-    *h_st = template_state();
-    CK(cudaMemcpyAsync(d_st, h_st, st_bytes, cudaMemcpyHostToDevice, stream));
+    std::memset(static_cast<void*>(B().h_st), 0, B().st_bytes);
+    *B().h_st = template_state();
+    CK(cudaMemcpyAsync(B().d_st, B().h_st, B().st_bytes, cudaMemcpyHostToDevice, stream));
     const uint32_t m = uint32_t(2 * n);
     const uint32_t nq = uint32_t(queries.size());
     if (pend.attempt == 0) hot_pack_maybe();
@@ -1103,7 +1118,7 @@ struct bdsm_engine {
     const bool full_sort = pend.full_sort || id_bits >= 32;
     const uint32_t key_bits = full_sort ? 32u : id_bits;  // both ids packed into 2 x id_bits
     const int sort_end_bit = full_sort ? 64 : int(2 * id_bits);
-    launch_prepare(src, uint32_t(n), view(), d_new_of.p, ups.p, d_st, keys.p, vals.p, dlab.p, ecode.p,
+    launch_prepare(src, uint32_t(n), view(), d_new_of.p, B().ups.p, B().d_st, B().keys.p, B().vals.p, B().dlab.p, B().ecode.p,
                    full_sort ? 0xffffffffu : (1u << id_bits), key_bits, stream);
     // one query, small batch: the negative phase's anchors need only the
     // translated updates and G, so they are counted and emitted on the side
@@ -1123,29 +1138,29 @@ struct bdsm_engine {
     }
     // the sort ping-pongs between keys/keys2 (vals/vals2); k_post_sort
     // widens its output into skeys/svals, which every later kernel reads
-    cub::DoubleBuffer<uint64_t> kb(keys.p, keys2.p);
-    cub::DoubleBuffer<uint32_t> vb(vals.p, vals2.p);
+    cub::DoubleBuffer<uint64_t> kb(B().keys.p, B().keys2.p);
+    cub::DoubleBuffer<uint32_t> vb(B().vals.p, B().vals2.p);
     {
       size_t tmp = cub_tmp.n;
       CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
     }
-    CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(kb.Current(), vb.Current(), key_bits, skeys.p, svals.p, m, d_st, head.p, insflag.p, d_rows.p,
-                     nq, g.V, hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
+    CK(cudaMemsetAsync(B().hkeys.p, 0xff, sizeof(unsigned long long) * B().hkeys.n, stream));
+    launch_post_sort(kb.Current(), vb.Current(), key_bits, B().skeys.p, B().svals.p, m, B().d_st, B().head.p, B().insflag.p, d_rows.p,
+                     nq, g.V, B().hkeys.p, B().hvals.p, uint32_t(B().hkeys.n - 1), cs, stream);
     {
       // the merge's insert prefix is only needed after the negative phase: it
       // is scanned on the side stream (own temporary storage) meanwhile
       CK(cudaEventRecord(fork2_ev, stream));
       CK(cudaStreamWaitEvent(side, fork2_ev, 0));
       size_t tmp = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, insflag.p, ins_prefix.p, int(m + 1), side));
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, B().insflag.p, B().ins_prefix.p, int(m + 1), side));
       cub_tmp_side.ensure(tmp);
       tmp = cub_tmp_side.n;
-      CK(cub::DeviceScan::ExclusiveSum(cub_tmp_side.p, tmp, insflag.p, ins_prefix.p, int(m + 1), side));
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp_side.p, tmp, B().insflag.p, B().ins_prefix.p, int(m + 1), side));
       CK(cudaEventRecord(join2_ev, side));
       tmp = cub_tmp.n;
-      CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), head.p, heads.p,
-                                    &d_st->n_touched, int(m), stream));
+      CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), B().head.p, B().heads.p,
+                                    &B().d_st->n_touched, int(m), stream));
     }
     CK(cudaEventRecord(ev[1], stream));
     run_phase(uint32_t(n), 0);
@@ -1154,11 +1169,11 @@ struct bdsm_engine {
     cudaEvent_t m0 = merge_ev[0], m1 = merge_ev[1];
     CK(cudaEventRecord(m0, stream));
     const bool small_ok = m >= tune_small_min;
-    launch_alloc(heads.p, skeys.p, ins_prefix.p, m, view(), opts.slack, d_st, new_off.p, new_cap.p, big_list.p,
-                 small_list.p, mid_list.p, small_ok, stream);
-    launch_merge_refresh(heads.p, skeys.p, svals.p, ins_prefix.p, m, ups.p, g, new_off.p, new_cap.p, ipos.p,
-                         d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, d_st, memo.p,
-                         uint32_t(memo.n ? memo.n - 1 : 0), big_list.p, small_list.p, mid_list.p, small_ok,
+    launch_alloc(B().heads.p, B().skeys.p, B().ins_prefix.p, m, view(), opts.slack, B().d_st, B().new_off.p, B().new_cap.p, B().big_list.p,
+                 B().small_list.p, B().mid_list.p, small_ok, stream);
+    launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p, B().new_cap.p, B().ipos.p,
+                         d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st, memo.p,
+                         uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p, small_ok,
                          num_sms, stream);
     CK(cudaEventRecord(m1, stream));
     launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
@@ -1171,13 +1186,13 @@ struct bdsm_engine {
         CK(cudaMemsetAsync(heat.p, 0, 4ull * g.V, stream));
         heat_init = true;
       }
-      launch_hot_walks(heads.p, skeys.p, d_st, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
+      launch_hot_walks(B().heads.p, B().skeys.p, B().d_st, view(), heat.p, 4, 3, uint32_t(batches_done), num_sms, stream);
       ++launches;
     }
-    launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
+    launch_clear_flags(B().skeys.p, m, d_rows.p, nq, g.V, cs, stream);
     ++launches;
     CK(cudaEventRecord(ev[4], stream));
-    CK(cudaMemcpyAsync(h_st, d_st, st_bytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(B().h_st, B().d_st, B().st_bytes, cudaMemcpyDeviceToHost, stream));
     if (memo.p) {
       if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
       CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
@@ -1229,7 +1244,7 @@ struct bdsm_engine {
         std::memcpy(h_ups, updates, n * sizeof(bdsm_update));
         h_src = h_ups;
       }
-      src = ups_ext.p;
+      src = B().ups_ext.p;
     }
     pend.src = src;
     launch_attempt();
@@ -1255,7 +1270,7 @@ struct bdsm_engine {
     const bdsm_update_dev* src = pend.src;
     for (;;) {
       sync();
-      const BatchState& b = *h_st;
+      const BatchState& b = *B().h_st;
       // the hot-list arena (K8) is reserved even when the batch is then rejected
       // (overflow 1 = pool exhausted: the compaction below re-lays the pool)
       if (b.pool_top > pool_top && b.overflow != 1) pool_top = b.pool_top;
@@ -1276,7 +1291,7 @@ struct bdsm_engine {
       }
       if (b.err_count) {
         std::vector<uint8_t> codes(n);
-        CK(cudaMemcpyAsync(codes.data(), ecode.p, n, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(codes.data(), B().ecode.p, n, cudaMemcpyDeviceToHost, stream));
         sync();
         for (size_t i = 0; i < n; ++i)
           if (codes[i]) last_errors.push_back({uint64_t(i), codes[i]});
@@ -1296,18 +1311,18 @@ struct bdsm_engine {
       }
       if (b.overflow == 2) {  // negative-phase work items: regrow, rerun all
         max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[0]) + 1024);
-        items.ensure(max_items);
+        B().items.ensure(max_items);
         relaunch();
         continue;
       }
       if (b.overflow == 3) {  // positive phase only (graph already merged)
         max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
-        items.ensure(max_items);
+        B().items.ensure(max_items);
         rerun_positive(uint32_t(n));
       }
       break;
     }
-    const BatchState& b = *h_st;
+    const BatchState& b = *B().h_st;
     pool_top = b.pool_top;
     ++batches_done;
     for (auto& q : queries) {  // BatchState keeps the last query's item counts per phase
@@ -1320,8 +1335,8 @@ struct bdsm_engine {
     // (MatchStats::timed_out, src/scheduler.cpp:101-110); whether it stays
     // matched in later batches is the caller's decision (set_query_active),
     // as in run_pipeline (src/bench.cpp:420-432)
-    const unsigned long long* cnt = st_counts(h_st);
-    const uint32_t* tmo = st_timed(h_st);
+    const unsigned long long* cnt = st_counts(B().h_st);
+    const uint32_t* tmo = st_timed(B().h_st);
     uint32_t tmask = 0;
     last_timed.assign(queries.size(), 0);
     for (size_t qi = 0; qi < queries.size(); ++qi) {
@@ -1363,7 +1378,7 @@ struct bdsm_engine {
     pend.st.attempts = uint32_t(pend.attempt + 1);
     pend.st.reruns = pend.reruns;
     pend.st.timed_out = tmask;
-    pend.st.d2h_bytes = st_bytes;
+    pend.st.d2h_bytes = B().st_bytes;
     pend.st.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pend.t0).count();
     if (stats) *stats = pend.st;
     return BDSM_OK;
@@ -1378,21 +1393,360 @@ struct bdsm_engine {
   // Positive-phase work items overflowed after the merge: grow and rerun that
   // phase alone (the graph is already G').
   void rerun_positive(uint32_t n) {
-    h_st->overflow = 0;
-    for (size_t qi = 0; qi < queries.size(); ++qi) st_counts(h_st)[queries.size() + qi] = 0;
-    CK(cudaMemcpyAsync(d_st, h_st, st_bytes, cudaMemcpyHostToDevice, stream));
+    B().h_st->overflow = 0;
+    for (size_t qi = 0; qi < queries.size(); ++qi) st_counts(B().h_st)[queries.size() + qi] = 0;
+    CK(cudaMemcpyAsync(B().d_st, B().h_st, B().st_bytes, cudaMemcpyHostToDevice, stream));
     const uint32_t m = 2 * n, nq = uint32_t(queries.size());
     // the batch-endpoint row flags were cleared at the end of the attempt
-    CK(cudaMemsetAsync(hkeys.p, 0xff, sizeof(unsigned long long) * hkeys.n, stream));
-    launch_post_sort(skeys.p, svals.p, 32, nullptr, nullptr, m, d_st, head.p, insflag.p, d_rows.p, nq, g.V,
-                     hkeys.p, hvals.p, uint32_t(hkeys.n - 1), stream);
+    CK(cudaMemsetAsync(B().hkeys.p, 0xff, sizeof(unsigned long long) * B().hkeys.n, stream));
+    launch_post_sort(B().skeys.p, B().svals.p, 32, nullptr, nullptr, m, B().d_st, B().head.p, B().insflag.p, d_rows.p, nq, g.V,
+                     B().hkeys.p, B().hvals.p, uint32_t(B().hkeys.n - 1), cs, stream);
     run_phase(n, 1);
-    launch_clear_flags(skeys.p, m, d_rows.p, nq, g.V, stream);
-    CK(cudaMemcpyAsync(h_st, d_st, st_bytes, cudaMemcpyDeviceToHost, stream));
+    launch_clear_flags(B().skeys.p, m, d_rows.p, nq, g.V, cs, stream);
+    CK(cudaMemcpyAsync(B().h_st, B().d_st, B().st_bytes, cudaMemcpyDeviceToHost, stream));
     CK(cudaEventRecord(ev[5], stream));
     ++pend.reruns;
     sync();
-    if (h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
+    if (B().h_st->overflow) throw std::runtime_error("positive phase could not be scheduled");
+  }
+
+  // ------------------------------------------------------------- stream --
+  // Pipelined stream (run_pipeline's stage overlap, src/bench.cpp:495-545,
+  // taken onto the device).  The positive phase of batch i and the negative
+  // phase of batch i+1 both read the graph after batch i's merge, so they run
+  // as ONE launch of the matching kernel (k_wbm with two phases): the idle
+  // warps of one phase's long tail take the other's items.  Batch buffers
+  // alternate between two slots; each batch's BatchState points at its
+  // predecessor's, so a batch that has to be rerun (pool or work-item
+  // regrowth) or is rejected stops every later batch of the stream on the
+  // device (overflow 6).  Per device order:
+  //   front(0) neg(0) | merge(i) front(i+1) [pos(i) + neg(i+1)] flags(i) D2H(i) | ...
+  // The host then reports the batches before the first abnormal one, handles
+  // that one through the single-batch path (reruns, exact errors) and resumes.
+  struct StreamBatch {
+    const bdsm_update* src = nullptr;  // host or device updates
+    size_t n = 0;
+  };
+  unsigned char* h_stream = nullptr;  // pinned: per batch a template and a result area
+  size_t h_stream_bytes = 0;
+  std::vector<cudaEvent_t> stream_ev;
+  std::vector<cudaEvent_t> stream_kev;  // pairs around each matching launch, then each merge
+  size_t stream_kev_used = 0;
+  cudaEvent_t next_skev() {
+    if (stream_kev_used == stream_kev.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      stream_kev.push_back(e);
+    }
+    return stream_kev[stream_kev_used++];
+  }
+  std::vector<std::pair<size_t, size_t>> seg_match_ev, seg_merge_ev;  // per batch: first/last kev index
+
+  bool stream_ok() const {
+    if (collect_cap || opts.l2_hot_mb) return false;
+    for (const auto& q : queries)
+      if (q->deadline_s > 0) return false;
+    return !queries.empty();
+  }
+
+  // Front part of a batch on slot cs: H2D, state template, K1 prepare, key
+  // sort, post-sort (flags, visibility table), insert prefix, segment heads.
+  void stream_front(const StreamBatch& sb, bool device_input, BatchState* prev, unsigned char* h_tmpl) {
+    const size_t n = sb.n;
+    ensure_batch(n);
+    ensure_tasks(n);
+    ensure_state();
+    const bdsm_update_dev* src = reinterpret_cast<const bdsm_update_dev*>(sb.src);
+    if (!device_input) {
+      CK(cudaMemcpyAsync(B().ups_ext.p, sb.src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+      src = B().ups_ext.p;
+    }
+    std::memset(h_tmpl, 0, B().st_bytes);
+    BatchState t = template_state();
+    t.prev = prev;
+    std::memcpy(h_tmpl, &t, sizeof(t));
+    CK(cudaMemcpyAsync(B().d_st, h_tmpl, B().st_bytes, cudaMemcpyHostToDevice, stream));
+    const uint32_t m = uint32_t(2 * n);
+    const uint32_t nq = uint32_t(queries.size());
+    const uint32_t id_bits = g.V > 1 ? 32u - uint32_t(__builtin_clz(g.V - 1)) : 1u;
+    const bool full_sort = id_bits >= 32;
+    const uint32_t key_bits = full_sort ? 32u : id_bits;
+    const int sort_end_bit = full_sort ? 64 : int(2 * id_bits);
+    launch_prepare(src, uint32_t(n), view(), d_new_of.p, B().ups.p, B().d_st, B().keys.p, B().vals.p, B().dlab.p,
+                   B().ecode.p, full_sort ? 0xffffffffu : (1u << id_bits), key_bits, stream);
+    cub::DoubleBuffer<uint64_t> kb(B().keys.p, B().keys2.p);
+    cub::DoubleBuffer<uint32_t> vb(B().vals.p, B().vals2.p);
+    size_t tmp = cub_tmp.n;
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
+    CK(cudaMemsetAsync(B().hkeys.p, 0xff, sizeof(unsigned long long) * B().hkeys.n, stream));
+    launch_post_sort(kb.Current(), vb.Current(), key_bits, B().skeys.p, B().svals.p, m, B().d_st, B().head.p,
+                     B().insflag.p, d_rows.p, nq, g.V, B().hkeys.p, B().hvals.p, uint32_t(B().hkeys.n - 1), cs, stream);
+    tmp = cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, B().insflag.p, B().ins_prefix.p, int(m + 1), stream));
+    tmp = cub_tmp.n;
+    CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), B().head.p, B().heads.p,
+                                  &B().d_st->n_touched, int(m), stream));
+    launches += 2;
+    cub_calls += 3;
+  }
+
+  // K3 + K4 of the batch on slot cs.
+  void stream_merge(size_t n) {
+    const uint32_t m = uint32_t(2 * n);
+    const bool small_ok = m >= tune_small_min;
+    launch_alloc(B().heads.p, B().skeys.p, B().ins_prefix.p, m, view(), opts.slack, B().d_st, B().new_off.p,
+                 B().new_cap.p, B().big_list.p, B().small_list.p, B().mid_list.p, small_ok, stream);
+    launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p,
+                         B().new_cap.p, B().ipos.p, d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st,
+                         memo.p, uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p,
+                         small_ok, num_sms, stream);
+    launches += small_ok ? 5 : 4;
+  }
+
+  // Anchors (K5), work queues and memo prefill of (phase, query) for the
+  // batch on slot cs; the launch itself is left to the caller.
+  PhaseArgs stream_phase(uint32_t n, uint32_t phase, int qi) {
+    QueryState& qs = *queries[size_t(qi)];
+    PhaseArgs a = phase_args(n, phase, qi);
+    launch_anchor_count(a, stream);
+    a.self_scan = n <= tune_self_scan;
+    if (!a.self_scan) {
+      size_t tmp = cub_tmp.n;
+      CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, B().upd_cnt.p, B().upd_off.p, AnchorCountSum(),
+                                        AnchorCount{0, 0, 0}, int(n + 1), stream));
+      cub_calls += 1;
+    }
+    launch_anchor_emit(a, stream);
+    launches += 2;
+    if (qs.q.n > 2 && qs.has_leaf) {
+      if (!memo_persistent) {
+        CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+        qs.memo_cold = true;
+      }
+      if (qs.memo_cold) {
+        refresh_hubs();
+        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
+        qs.memo_cold = false;
+        ++launches;
+      } else if (phase == 1) {
+        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, stream);
+        ++launches;
+      }
+    }
+    if (qs.q.n > 2 && qs.natail && !tune_no_tasktail) {
+      B().task_tail.ensure_grow(B().tasks.n * qs.natail);
+      CK(cudaMemsetAsync(B().task_tail.p, 0xff, sizeof(unsigned long long) * B().tasks.n * qs.natail, stream));
+      a.task_tail = B().task_tail.p;
+    }
+    return a;
+  }
+
+  // One launch of the matching kernel for up to two phases of one query.
+  void stream_launch(const PhaseArgs* a, const PhaseArgs* b, int qi) {
+    QueryState& qs = *queries[size_t(qi)];
+    if (qs.q.n <= 2) return;  // 2-vertex matches were counted by the anchors
+    CK(cudaMemsetAsync(qstate.p, 0, sizeof(QueueState), stream));
+    const PhaseArgs& first = a ? *a : *b;
+    PhaseArgs x = first;
+    x.epoch = ++epoch;
+    const uint32_t items = std::max(qs.prev_items[0], qs.prev_items[1]);
+    const int variant = tune_variant ? int(tune_variant) : items > tune_throughput_items ? 4 : 2;
+    x.backoff_max = tune_backoff ? tune_backoff : variant == 2 ? 256u : 1024u;
+    CK(cudaEventRecord(next_skev(), stream));
+    launch_wbm(x, a && b ? b : nullptr, num_sms, variant, stream);
+    CK(cudaEventRecord(next_skev(), stream));
+    ++launches;
+  }
+
+  // Enqueues batches [i0, k) and waits; returns the first batch whose state is
+  // abnormal (k if none).  Results of the batches before it are in h_res(i).
+  size_t stream_segment(const StreamBatch* bs, size_t i0, size_t k, bool device_input) {
+    const size_t nq = queries.size();
+    const size_t sb = st_size();
+    const size_t need = 2 * sb * (k - i0);
+    if (h_stream_bytes < need) {
+      if (h_stream) cudaFreeHost(h_stream);
+      h_stream = nullptr;
+      CK(cudaMallocHost(&h_stream, need));
+      h_stream_bytes = need;
+    }
+    while (stream_ev.size() < k - i0 + 1) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      stream_ev.push_back(e);
+    }
+    auto h_tmpl = [&](size_t i) { return h_stream + 2 * sb * (i - i0); };
+    auto h_res = [&](size_t i) { return h_stream + 2 * sb * (i - i0) + sb; };
+    launches = 0;
+    cub_calls = 0;
+    stream_kev_used = 0;
+    seg_match_ev.assign(k - i0, {0, 0});
+    seg_merge_ev.assign(k - i0, {0, 0});
+    CK(cudaEventRecord(stream_ev[0], stream));
+    cs = 0;
+    stream_front(bs[i0], device_input, nullptr, h_tmpl(i0));
+    seg_match_ev[0].first = stream_kev_used;
+    for (size_t qi = 0; qi < nq; ++qi) {
+      if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
+      PhaseArgs an = stream_phase(uint32_t(bs[i0].n), 0, int(qi));
+      stream_launch(nullptr, &an, int(qi));
+    }
+    for (size_t i = i0; i < k; ++i) {
+      const uint32_t s = uint32_t((i - i0) & 1), t = s ^ 1u;
+      cs = s;
+      seg_merge_ev[i - i0].first = stream_kev_used;
+      CK(cudaEventRecord(next_skev(), stream));
+      stream_merge(bs[i].n);
+      CK(cudaEventRecord(next_skev(), stream));
+      seg_merge_ev[i - i0].second = stream_kev_used;
+      BatchState* st_i = slot_[s].d_st;
+      if (i + 1 < k) {
+        cs = t;
+        stream_front(bs[i + 1], device_input, st_i, h_tmpl(i + 1));
+      }
+      if (i > i0) seg_match_ev[i - i0].first = stream_kev_used;
+      for (size_t qi = 0; qi < nq; ++qi) {
+        if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
+        cs = s;
+        PhaseArgs ap = stream_phase(uint32_t(bs[i].n), 1, int(qi));
+        if (i + 1 < k) {
+          cs = t;
+          PhaseArgs an = stream_phase(uint32_t(bs[i + 1].n), 0, int(qi));
+          stream_launch(&ap, &an, int(qi));
+        } else {
+          stream_launch(&ap, nullptr, int(qi));
+        }
+      }
+      seg_match_ev[i - i0].second = stream_kev_used;
+      cs = s;
+      launch_clear_flags(B().skeys.p, uint32_t(2 * bs[i].n), d_rows.p, uint32_t(nq), g.V, s, stream);
+      ++launches;
+      CK(cudaMemcpyAsync(h_res(i), B().d_st, sb, cudaMemcpyDeviceToHost, stream));
+      CK(cudaEventRecord(stream_ev[i - i0 + 1], stream));
+    }
+    if (memo.p) {
+      if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));
+      CK(cudaMemcpyAsync(h_memo_fill, memo_fill.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+    }
+    sync();
+    cs = 0;
+    for (size_t i = i0; i < k; ++i) {
+      const BatchState& b = *reinterpret_cast<const BatchState*>(h_res(i));
+      if (b.err_count || b.selfloop_min != kNone || b.conflict_min != kNone || b.overflow) return i;
+    }
+    return k;
+  }
+
+  // Counts and stats of a batch from its result area (as wait() reports them).
+  double kev_span(const std::pair<size_t, size_t>& r) {
+    double t = 0;
+    for (size_t e = r.first; e + 1 < r.second; e += 2) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, stream_kev[e], stream_kev[e + 1]);
+      t += ms;
+    }
+    return t;
+  }
+
+  void stream_report(const unsigned char* res, size_t n, double ms, uint64_t* pos, uint64_t* neg,
+                     bdsm_batch_stats* stats, double ms_match = 0, double ms_merge = 0) {
+    const BatchState& b = *reinterpret_cast<const BatchState*>(res);
+    const size_t nq = queries.size();
+    const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(&b + 1);
+    const uint32_t* tmo = reinterpret_cast<const uint32_t*>(cnt + 2 * nq);
+    last_timed.assign(nq, 0);
+    for (size_t qi = 0; qi < nq; ++qi) {
+      last_timed[qi] = tmo[qi] != 0;
+      if (neg) neg[qi] = tmo[qi] ? 0 : cnt[qi];
+      if (pos) pos[qi] = tmo[qi] ? 0 : cnt[nq + qi];
+    }
+    pool_top = b.pool_top;
+    ++batches_done;
+    for (auto& q : queries) {
+      q->prev_items[0] = b.n_items[0];
+      q->prev_items[1] = b.n_items[1];
+    }
+    if (stats) {
+      bdsm_batch_stats s{};
+      s.ms_device = ms;
+      s.dfs_visits = b.visits;
+      s.tasks = b.tasks_total;
+      s.work_items = uint64_t(b.n_items[0]) + b.n_items[1];
+      s.gen_calls = b.gen_calls;
+      s.bytes_phase = b.bytes_phase;
+      s.bytes_kernel = b.bytes_kernel;
+      s.bytes_update = b.bytes_update + 16ull * n;
+      s.touched = b.n_touched;
+      s.relocations = b.relocations;
+      s.attempts = 1;
+      s.d2h_bytes = st_size();
+      s.kernel_launches = launches;
+      s.cub_launches = cub_calls;
+      // the matching launches after this batch's merge (its positive phase,
+      // fused with the next batch's negative phase) and its merge kernels
+      s.ms_match_kernel = ms_match;
+      s.ms_merge_kernel = ms_merge;
+      *stats = s;
+    }
+  }
+
+  bdsm_status apply_stream(const StreamBatch* bs, size_t k, bool device_input, uint64_t* pos, uint64_t* neg,
+                           bdsm_batch_stats* stats, size_t* done) {
+    if (pend.active) throw std::invalid_argument("a batch is already in flight on this engine (wait for it first)");
+    const size_t nq = queries.size();
+    *done = 0;
+    size_t i0 = 0;
+    while (i0 < k) {
+      if (!stream_ok() || k - i0 == 1) {  // one batch, or a mode the stream does not cover
+        bdsm_batch_stats st{};
+        apply(bs[i0].src, bs[i0].n, device_input, pos ? pos + i0 * nq : nullptr, neg ? neg + i0 * nq : nullptr,
+              &st);
+        if (stats) stats[i0] = st;
+        *done = ++i0;
+        continue;
+      }
+      for (size_t i = i0; i < k; ++i)
+        if (bs[i].n == 0 || bs[i].n >= (size_t(1) << 31)) throw std::invalid_argument("stream batches must be non-empty");
+      const auto t0 = std::chrono::steady_clock::now();
+      const size_t j = stream_segment(bs, i0, k, device_input);
+      const size_t sb = st_size();
+      for (size_t i = i0; i < j; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, stream_ev[i - i0], stream_ev[i - i0 + 1]);
+        stream_report(h_stream + 2 * sb * (i - i0) + sb, bs[i].n, ms, pos ? pos + i * nq : nullptr,
+                      neg ? neg + i * nq : nullptr, stats ? stats + i : nullptr, kev_span(seg_match_ev[i - i0]),
+                      kev_span(seg_merge_ev[i - i0]));
+        if (stats) stats[i].ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        *done = i + 1;
+      }
+      if (memo.p && h_memo_fill && *h_memo_fill > memo.n * 2 / 5) reset_memo();
+      if (j == k) break;
+      // batch j needs the single-batch path: a positive-phase regrowth on the
+      // merged graph, or a full rerun / exact error report on the graph before it
+      const BatchState& b = *reinterpret_cast<const BatchState*>(h_stream + 2 * sb * (j - i0) + sb);
+      if (b.overflow == 3 && !b.err_count && b.selfloop_min == kNone && b.conflict_min == kNone) {
+        cs = uint32_t((j - i0) & 1);
+        pend = Pending{};
+        pend.n = bs[j].n;
+        std::memcpy(static_cast<void*>(B().h_st), &b, sb);
+        B().h_st->prev = nullptr;  // its predecessor is final; the slot behind it was reused
+        max_items = std::max<size_t>(max_items * 2, size_t(b.n_items[1]) + 1024);
+        B().items.ensure(max_items);
+        rerun_positive(uint32_t(bs[j].n));
+        stream_report(reinterpret_cast<const unsigned char*>(B().h_st), bs[j].n, 0.0, pos ? pos + j * nq : nullptr,
+                      neg ? neg + j * nq : nullptr, stats ? stats + j : nullptr);
+        if (stats) stats[j].reruns = pend.reruns;
+        cs = 0;
+      } else {
+        // nothing of batch j was merged: rerun it alone (throws its error)
+        bdsm_batch_stats st{};
+        apply(bs[j].src, bs[j].n, device_input, pos ? pos + j * nq : nullptr, neg ? neg + j * nq : nullptr, &st);
+        if (stats) stats[j] = st;
+      }
+      *done = j + 1;
+      i0 = j + 1;
+    }
+    return BDSM_OK;
   }
 
   void fetch_update(const bdsm_update_dev* src, bool device_input, uint32_t idx, bdsm_update* out) {
@@ -1546,6 +1900,26 @@ bdsm_status bdsm_engine_apply_batch_device(bdsm_engine* engine, const bdsm_updat
   });
 }
 
+bdsm_status bdsm_engine_apply_stream(bdsm_engine* engine, const bdsm_update* const* batches, const size_t* sizes,
+                                     size_t k, int device_input, uint64_t* pos, uint64_t* neg,
+                                     bdsm_batch_stats* stats, size_t* done) {
+  size_t dummy = 0;
+  if (!done) done = &dummy;
+  *done = 0;
+  if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
+  if (k && (!batches || !sizes)) return fail(BDSM_INVALID_ARGUMENT, "null batches");
+  return guarded([&]() -> bdsm_status {
+    CK(cudaSetDevice(engine->device));
+    std::vector<bdsm_engine::StreamBatch> bs(k);
+    for (size_t i = 0; i < k; ++i) {
+      if (sizes[i] && !batches[i]) throw std::invalid_argument("null updates");
+      bs[i].src = batches[i];
+      bs[i].n = sizes[i];
+    }
+    return engine->apply_stream(bs.data(), k, device_input != 0, pos, neg, stats, done);
+  });
+}
+
 bdsm_status bdsm_engine_submit_batch(bdsm_engine* engine, const bdsm_update* updates, size_t n) {
   if (!engine) return fail(BDSM_INVALID_ARGUMENT, "null engine");
   if (n && !updates) return fail(BDSM_INVALID_ARGUMENT, "null updates");
@@ -1598,10 +1972,10 @@ size_t bdsm_last_batch_errors(bdsm_engine* engine, bdsm_update_error* out, size_
 }
 
 size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size_t cap) {
-  if (!engine || !engine->h_st) return 0;
-  const size_t n = (sizeof(engine->h_st->trace) + sizeof(engine->h_st->trace_chunks) +
-                    sizeof(engine->h_st->trace_setups)) / sizeof(uint64_t);
-  const uint64_t* t = &engine->h_st->trace[0][0];
+  if (!engine || !engine->slot_[0].h_st) return 0;
+  const BatchState* hs = engine->slot_[0].h_st;
+  const size_t n = (sizeof(hs->trace) + sizeof(hs->trace_chunks) + sizeof(hs->trace_setups)) / sizeof(uint64_t);
+  const uint64_t* t = &hs->trace[0][0];
   for (size_t i = 0; i < n && i < cap; ++i) out[i] = t[i];
   return n;
 }

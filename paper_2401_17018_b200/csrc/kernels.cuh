@@ -61,9 +61,9 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const ui
 void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t key_bits, uint64_t* out_keys,
                       uint32_t* out_vals, uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
                       uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys, uint32_t* hvals,
-                      uint32_t hmask, cudaStream_t s);
+                      uint32_t hmask, uint32_t slot, cudaStream_t s);
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                        cudaStream_t s);
+                        uint32_t slot, cudaStream_t s);
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
                   uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, uint32_t* mid_list,
@@ -112,6 +112,7 @@ struct PhaseArgs {
   const uint32_t* hvals;
   uint32_t hmask;
   uint32_t phase;                // 0 negative (deletes), 1 positive (inserts)
+  uint32_t flag;                 // candidate-row flag of this phase's batch endpoints (row_del/ins_flag(slot))
   uint32_t query;
   uint32_t qn;                   // query vertex count
   uint32_t chunk;
@@ -146,8 +147,15 @@ struct PhaseArgs {
 
 void launch_anchor_count(const PhaseArgs& a, cudaStream_t s);
 void launch_anchor_emit(const PhaseArgs& a, cudaStream_t s);
-// ctas_per_sm: 2 (104 registers, launches bound by their longest subtree), 3 (80), 4 (64, many work items)
-void launch_wbm(const PhaseArgs& a, int num_sms, int ctas_per_sm, cudaStream_t s);
+// Two phases of one launch (k_wbm): the pipelined stream's positive phase of
+// batch i and negative phase of batch i+1, on the same graph.
+struct PhasePair {
+  PhaseArgs p[2];
+  uint32_t n;  // phases in use (1 or 2)
+};
+// ctas_per_sm: 2 (104 registers, launches bound by their longest subtree), 3 (80), 4 (64, many work items).
+// second: a phase of the next batch on the same graph, run in the same launch (nullptr: one phase).
+void launch_wbm(const PhaseArgs& a, const PhaseArgs* second, int num_sms, int ctas_per_sm, cudaStream_t s);
 void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig, const uint32_t* hubs,
                          const uint32_t* n_hubs, int num_sms, cudaStream_t s);
 void launch_select_hubs(const uint32_t* deg, uint32_t V, uint32_t min_deg, uint32_t* hubs, uint32_t* n_hubs,

@@ -48,9 +48,6 @@ __device__ __forceinline__ uint32_t lb_u64(const uint64_t* __restrict__ a, uint3
   return lo;
 }
 
-__device__ __forceinline__ bool batch_aborted(const BatchState* st) {
-  return st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow;
-}
 
 // Level-2 driver of an anchor: the lower-degree backward neighbour of
 // order[2] among the two anchor positions (ties: position 0).  Shared with
@@ -675,7 +672,7 @@ __global__ void __launch_bounds__(256) k_leaf_prefill(PhaseArgs a, const LeafSig
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
+  const uint32_t flag = a.flag;
   // hubs == nullptr: the batch's touched vertices (their weights were
   // invalidated by the merge) instead of the engine's hub list
   const uint32_t nh = hubs ? *n_hubs : a.st->n_touched;
@@ -815,8 +812,10 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
 // src/matcher.cpp:169-217, for --dump-matches): the whole order is
 // enumerated (no counted tail) and every complete match is written in query
 // vertex order to a.match_out.
-template <bool kEmit, int kMinBlocks>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseArgs a) {
+// kPairs: 1 for a single phase (the phase arguments are compile-time uniform),
+// 2 for the pipelined stream's fused launch.
+template <bool kEmit, int kMinBlocks, int kPairs>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const __grid_constant__ PhasePair pp) {
   __shared__ uint32_t s_cand[kWarpsPerBlock][kMaxQ][32];
   __shared__ uint32_t s_M[kWarpsPerBlock][kMaxQ];
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
@@ -829,17 +828,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
   s_dbg = s_dbg_;
 #endif
   // per-warp counters (lane 0 updates them; kept out of the register budget)
-  __shared__ unsigned long long s_stat[kWarpsPerBlock][5];  // count, visits, bytes, calls, kernel bytes
+  __shared__ unsigned long long s_stat[kWarpsPerBlock][10];  // per phase: count, visits, bytes, calls, kernel bytes
   __shared__ unsigned long long s_lacc[kWarpsPerBlock][32][4];  // per-lane count/visits/bytes/calls (leaf levels)
-  if (batch_aborted(a.st)) return;
-  BatchState* st = a.st;
+  // One launch runs up to two phases (the pipelined stream's positive phase
+  // of batch i and negative phase of batch i+1, both on the same graph): the
+  // static items of pp.p[0] come first in the shared queue, then pp.p[1]'s;
+  // a donated item records its phase.  Queue, donation slots, memo and graph
+  // are shared; a phase whose batch was aborted contributes no items.
+  const PhaseArgs& a0 = pp.p[0];
+  const uint32_t n0 = batch_aborted(a0.st) ? 0u : a0.st->n_items[a0.phase];
+  const uint32_t n1 = kPairs < 2 || batch_aborted(pp.p[kPairs - 1].st) ? 0u
+                                                                      : pp.p[kPairs - 1].st->n_items[pp.p[kPairs - 1].phase];
+  const uint32_t n_items = n0 + n1;
+  if (n_items == 0) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
-  const uint32_t n_items = st->n_items[a.phase];
-  const DevGraph& g = a.g;
-  unsigned long long* stat = s_stat[threadIdx.x >> 5];
-  if ((threadIdx.x & 31) < 5) stat[threadIdx.x & 31] = 0;
-  for (int k = 0; k < 4; ++k) s_lacc[threadIdx.x >> 5][threadIdx.x & 31][k] = 0;
+  if (lane < 10) s_stat[w][lane] = 0;
+  for (int k = 0; k < 4; ++k) s_lacc[w][lane][k] = 0;
   __syncwarp();
   uint32_t dtick = 0;
   unsigned long long tt_pref = 0;  // prefetched donation-demand poll
@@ -855,19 +860,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
   uint32_t r_mask = 0;  // unexplored candidates of the current chunk
   uint32_t r_drv = 0;   // index of the driver in the level's backward list
   uint32_t r_tmask = 0; // current chunk: which candidates are same-kind batch endpoints
-  const uint32_t flag = a.phase == 0 ? kRowDelFlag : kRowInsFlag;
 
   while (true) {
     // ---- acquire work ----------------------------------------------------
     uint32_t kind = 0, ref = 0;  // 1 static item, 2 donated item, 3 exit, 4 deadline
-    QueueState* Q = a.q;
+    QueueState* Q = a0.q;
     if (lane == 0) {
       // Static items first (counted as held before the index is taken, so a
       // waiter never sees holders == 0 while a static item is in flight).
       // the deadline is checked before every work item, as the reference's
       // workers check it before every task (Shared::stopping,
       // src/scheduler.cpp:101-110): an expired budget stops the phase
-      if (a.deadline_ns && globaltimer() > a.deadline_ns) {
+      if (a0.deadline_ns && globaltimer() > a0.deadline_ns) {
         kind = 4;
         static_done = true;
       }
@@ -882,12 +886,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
           atomicSub(&Q->holders.v, 1u);
         }
       }
-      if (!kind && !(a.deadline_ns && globaltimer() > a.deadline_ns)) {
+      if (!kind && !(a0.deadline_ns && globaltimer() > a0.deadline_ns)) {
         // Donated work: one ticket per idle period, then wait on that slot.
         if (ticket == kNone) ticket = atomicAdd(&Q->tt.tickets, 1u);
         uint32_t backoff = 128, spins = 0;
         while (true) {
-          if (ticket < a.dyn_cap && ld_volatile(a.dyn_ready + ticket) == a.epoch) {
+          if (ticket < a0.dyn_cap && ld_volatile(a0.dyn_ready + ticket) == a0.epoch) {
             kind = 2;
             ref = ticket;
             ticket = kNone;
@@ -898,13 +902,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
               kind = 3;
               break;
             }
-            if (a.deadline_ns && globaltimer() > a.deadline_ns) {
+            if (a0.deadline_ns && globaltimer() > a0.deadline_ns) {
               kind = 4;
               break;
             }
           }
           __nanosleep(backoff);
-          if (backoff < a.backoff_max) backoff *= 2;
+          if (backoff < a0.backoff_max) backoff *= 2;
         }
       }
     }
@@ -915,6 +919,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
       break;
     }
     if (kind == 3) break;
+    // the phase this item belongs to
+    uint32_t sel = 0;
+    if (kPairs > 1) {
+      if (kind == 1 && ref >= n0) {
+        sel = 1;
+        ref -= n0;
+      } else if (kind == 2) {
+        __threadfence();
+        sel = __ldcg(&a0.dyn[ref].pad[0]);
+      }
+    }
+    const PhaseArgs& a = pp.p[sel];
+    BatchState* st = a.st;
+    const DevGraph& g = a.g;
+    const uint32_t flag = a.flag;
+    unsigned long long* stat = s_stat[w] + 5 * sel;
 #ifdef BDSM_TRACE
     const uint64_t t_item = globaltimer();
     uint32_t it_chunks = 0, it_don = 0;
@@ -932,7 +952,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
       __syncwarp();
       __threadfence();
       // L2-coherent loads (.cg): the slot was written by another SM in this launch
-      const DynItem* it = a.dyn + ref;
+      const DynItem* it = a0.dyn + ref;
       task_id = __ldcg(&it->task);
       lstart = __ldcg(&it->level);
       rbegin = __ldcg(&it->begin);
@@ -1017,7 +1037,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
           // poll is issued one chunk fetch ahead so its L2 round trip overlaps
           // the chunk's filtering.
           const unsigned long long tt = tt_pref;
-          tt_pref = *reinterpret_cast<const volatile unsigned long long*>(&a.q->tt.tickets);
+          tt_pref = *reinterpret_cast<const volatile unsigned long long*>(&a0.q->tt.tickets);
           if (int32_t(uint32_t(tt) - uint32_t(tt >> 32)) > 0) {
             if (lane == l) {  // park the current level: the stack now covers [lstart, l]
               r_cur = c_cur;
@@ -1034,10 +1054,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
               cy0 = clock64();
 #endif
               uint32_t slot = 0;
-              if (lane == 0) slot = dyn_reserve(a.q, a.dyn_cap);
+              if (lane == 0) slot = dyn_reserve(a0.q, a0.dyn_cap);
               slot = __shfl_sync(kFull, slot, 0);
               if (slot != kNone) {
-                DynItem* it = a.dyn + slot;
+                DynItem* it = a0.dyn + slot;
                 if (lane < j) it->M[lane] = s_M[w][lane];
                 if (by_range) {
                   uint32_t cj = __shfl_sync(kFull, r_cur, j), ej = __shfl_sync(kFull, r_end, j);
@@ -1070,11 +1090,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
                 if (lane == 0) {
                   it->task = task_id;
                   it->level = j;
+                  it->pad[0] = sel;
                 }
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) {
-                  atomicExch(a.dyn_ready + slot, a.epoch);
+                  atomicExch(a0.dyn_ready + slot, a0.epoch);
                   atomicAdd(&st->donations, 1u);
                 }
 #ifdef BDSM_TRACE
@@ -1225,7 +1246,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
 #endif
       }
     }
-    if (lane == 0) atomicSub(&a.q->holders.v, 1u);
+    if (lane == 0) atomicSub(&a0.q->holders.v, 1u);
+    {  // fold the per-lane leaf-level accumulators into this phase's counters
+      unsigned long long v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = warp_sum_u64(s_lacc[w][lane][k]);
+        s_lacc[w][lane][k] = 0;
+      }
+      if (lane == 0)
+        for (int k = 0; k < 4; ++k) stat[k] += v[k];
+      __syncwarp();
+    }
 #ifdef BDSM_TRACE
     if (lane == 0) {
       const uint64_t t1 = globaltimer(), dt = t1 - t_item;
@@ -1252,21 +1284,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(PhaseAr
     if (timed_out) break;
   }
   __syncwarp();
-  {  // fold the per-lane leaf-level accumulators into the warp's counters
-    unsigned long long v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = warp_sum_u64(s_lacc[w][lane][k]);
-    if (lane == 0)
-      for (int k = 0; k < 4; ++k) stat[k] += v[k];
-  }
-  __syncwarp();
   if (lane == 0) {
-    if (stat[0]) atomicAdd(a.count_out, stat[0]);
-    if (stat[1]) atomicAdd((unsigned long long*)&st->visits, stat[1]);
-    if (stat[2]) atomicAdd((unsigned long long*)&st->bytes_phase, stat[2]);
-    if (stat[3]) atomicAdd((unsigned long long*)&st->gen_calls, stat[3]);
-    if (stat[4]) atomicAdd((unsigned long long*)&st->bytes_kernel, stat[4]);
-    if (timed_out) atomicExch(a.timed_out, 1u);
+    for (uint32_t sel = 0; sel < uint32_t(kPairs); ++sel) {
+      const PhaseArgs& a = pp.p[sel];
+      const unsigned long long* stat = s_stat[w] + 5 * sel;
+      if (stat[0]) atomicAdd(a.count_out, stat[0]);
+      if (stat[1]) atomicAdd((unsigned long long*)&a.st->visits, stat[1]);
+      if (stat[2]) atomicAdd((unsigned long long*)&a.st->bytes_phase, stat[2]);
+      if (stat[3]) atomicAdd((unsigned long long*)&a.st->gen_calls, stat[3]);
+      if (stat[4]) atomicAdd((unsigned long long*)&a.st->bytes_kernel, stat[4]);
+    }
+    // a deadline stops the launch: the counts of its queries are dropped
+    if (timed_out)
+      for (uint32_t sel = 0; sel < uint32_t(kPairs); ++sel) atomicExch(pp.p[sel].timed_out, 1u);
   }
 }
 
@@ -1288,22 +1318,28 @@ void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig,
   if (nsig) k_leaf_prefill<<<unsigned(num_sms * 8), 256, 0, s>>>(a, sigs, nsig, hubs, n_hubs);
 }
 
-template <bool kEmit, int kMinBlocks>
-void launch_wbm_variant(const PhaseArgs& a, int num_sms, cudaStream_t s) {
+template <bool kEmit, int kMinBlocks, int kPairs>
+void launch_wbm_variant(const PhasePair& pp, int num_sms, cudaStream_t s) {
   // persistent: as many resident CTAs as the SMs hold
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<kEmit, kMinBlocks>, kWarpsPerBlock * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<kEmit, kMinBlocks, kPairs>, kWarpsPerBlock * 32, 0);
     if (per_sm <= 0) per_sm = 1;
   }
-  k_wbm<kEmit, kMinBlocks><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(a);
+  k_wbm<kEmit, kMinBlocks, kPairs><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(pp);
 }
 
-void launch_wbm(const PhaseArgs& a, int num_sms, int ctas_per_sm, cudaStream_t s) {
-  if (a.match_out) launch_wbm_variant<true, 2>(a, num_sms, s);
-  else if (ctas_per_sm >= 4) launch_wbm_variant<false, 4>(a, num_sms, s);
-  else if (ctas_per_sm == 3) launch_wbm_variant<false, 3>(a, num_sms, s);
-  else launch_wbm_variant<false, 2>(a, num_sms, s);
+void launch_wbm(const PhaseArgs& a, const PhaseArgs* second, int num_sms, int ctas_per_sm, cudaStream_t s) {
+  PhasePair pp;
+  pp.p[0] = a;
+  pp.p[1] = second ? *second : a;
+  pp.n = second ? 2u : 1u;
+  if (a.match_out) launch_wbm_variant<true, 2, 1>(pp, num_sms, s);
+  else if (second && ctas_per_sm >= 4) launch_wbm_variant<false, 4, 2>(pp, num_sms, s);
+  else if (second) launch_wbm_variant<false, 2, 2>(pp, num_sms, s);
+  else if (ctas_per_sm >= 4) launch_wbm_variant<false, 4, 1>(pp, num_sms, s);
+  else if (ctas_per_sm == 3) launch_wbm_variant<false, 3, 1>(pp, num_sms, s);
+  else launch_wbm_variant<false, 2, 1>(pp, num_sms, s);
 }
 
 }  // namespace bdsm_b200

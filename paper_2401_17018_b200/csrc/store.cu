@@ -163,6 +163,9 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
                           const uint32_t* __restrict__ new_of, bdsm_update_dev* iups, BatchState* st,
                           uint64_t* keys, uint32_t* vals, uint32_t* dlab, uint8_t* ecode, uint32_t id_limit,
                           uint32_t key_bits) {
+  // pipelined stream: this batch allocates from where its predecessor's merge
+  // left the pool's bump pointer (k_prepare runs after that merge)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) st->pool_top = st->prev->pool_top;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
     if (up.u < g.V) up.u = new_of[up.u];
@@ -214,7 +217,7 @@ __global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t
                             uint32_t key_bits, uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
                             uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
                             uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys,
-                            uint32_t* hvals, uint32_t hmask) {
+                            uint32_t* hvals, uint32_t hmask, uint32_t flag_ins, uint32_t flag_del) {
   const uint64_t dmask = key_bits >= 32 ? 0xffffffffull : (1ull << key_bits) - 1;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= m; j += gridDim.x * blockDim.x) {
     if (j == m) {
@@ -238,7 +241,7 @@ __global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t
     head[j] = h ? 1 : 0;
     insflag[j] = is_del ? 0u : 1u;
     if (src < V)
-      for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? kRowDelFlag : kRowInsFlag);
+      for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? flag_del : flag_ins);
     // visibility table: linear probing (duplicates only in rejected batches);
     // segment heads also map (src, kNone) -> the segment's first index
     for (int pass = 0; pass < (h ? 2 : 1); ++pass) {
@@ -259,11 +262,11 @@ __global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t
 // End of batch (also after a rejected one): clear the per-batch row flags of
 // every touched vertex.
 __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, uint32_t* const* rows,
-                              uint32_t nq, uint32_t V) {
+                              uint32_t nq, uint32_t V, uint32_t flags) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
     uint32_t src = uint32_t(skeys[j] >> 32);
     if (src < V && (j == 0 || uint32_t(skeys[j - 1] >> 32) != src))
-      for (uint32_t q = 0; q < nq; ++q) rows[q][src] &= ~kRowFlags;
+      for (uint32_t q = 0; q < nq; ++q) rows[q][src] &= ~flags;
   }
 }
 
@@ -292,7 +295,7 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
                         const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
                         BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
                         uint32_t* small_list, uint32_t* mid_list, bool small_ok) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted(st)) return;
   const uint32_t nt = st->n_touched;
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
   // warp-uniform loop: list appends and pool allocations are aggregated per
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
     uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
     uint32_t memo_mask, const uint32_t* __restrict__ mid_list) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) {
     if (threadIdx.x == 0 && blockIdx.x == 0) st->overflow = 1;
     return;
@@ -638,7 +641,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
     const uint32_t* __restrict__ new_cap, const DevQueryEnc* __restrict__ qenc, uint32_t nq,
     uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
     uint32_t memo_mask, const uint32_t* __restrict__ small_list) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   const uint32_t nt = st->n_touched, nsmall = st->n_small;
   uint64_t bytes = 0;
@@ -822,7 +825,7 @@ __global__ void __launch_bounds__(256) k_merge_big(
     const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc,
     uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
     uint32_t memo_mask, const uint32_t* __restrict__ big_list) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   __shared__ uint32_t s_start;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -932,7 +935,7 @@ __global__ void __launch_bounds__(256) k_finish_big(
     const uint32_t* __restrict__ svals, uint32_t m, DevGraphMut g, const DevQueryEnc* __restrict__ qenc,
     uint32_t nq, uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
     uint32_t memo_mask, const uint32_t* __restrict__ big_list) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -989,7 +992,7 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
 __global__ void k_hot_walks(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
                             const BatchState* st, DevGraph g, uint32_t* heat, uint32_t walks, uint32_t depth,
                             uint32_t seed) {
-  if (st->err_count || st->selfloop_min != kNone || st->conflict_min != kNone || st->overflow) return;
+  if (batch_aborted_own(st)) return;
   const uint64_t total = uint64_t(st->n_touched) * walks;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -1134,13 +1137,14 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const ui
 void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t key_bits, uint64_t* out_keys,
                       uint32_t* out_vals, uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
                       uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys, uint32_t* hvals,
-                      uint32_t hmask, cudaStream_t s) {
+                      uint32_t hmask, uint32_t slot, cudaStream_t s) {
   k_post_sort<<<blocks_for(uint64_t(m) + 1), kThreads, 0, s>>>(in_keys, in_vals, key_bits, out_keys, out_vals, m,
-                                                              st, head, insflag, rows, nq, V, hkeys, hvals, hmask);
+                                                              st, head, insflag, rows, nq, V, hkeys, hvals, hmask,
+                                                              row_ins_flag(slot), row_del_flag(slot));
 }
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                        cudaStream_t s) {
-  k_clear_flags<<<blocks_for(m), kThreads, 0, s>>>(skeys, m, rows, nq, V);
+                        uint32_t slot, cudaStream_t s) {
+  k_clear_flags<<<blocks_for(m), kThreads, 0, s>>>(skeys, m, rows, nq, V, row_ins_flag(slot) | row_del_flag(slot));
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,

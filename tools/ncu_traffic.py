@@ -6,8 +6,10 @@
     python tools/ncu_traffic.py traffic.csv --steps S --build <sha> [--out profiles/x.json]
 
 Only this library's kernels (k_*) and CUB's are kept.  The launches of one
-bench step are found from the per-step k_wbm count (2 per step for one query:
-negative and positive phase); the summary is per step of the last S steps,
+bench step are found from the per-step k_wbm count (one query: 2 per step one
+batch at a time, 1 in the pipelined stream where the positive phase of batch i
+and the negative phase of batch i+1 share a launch); the summary is per step of
+the last S steps,
 so bench.py can put physical bytes beside its live per-step kernel time.
 """
 import argparse
@@ -57,12 +59,9 @@ def main():
     need = args.steps * args.wbm_per_step
     if len(wbm_idx) < need:
         sys.exit(f"only {len(wbm_idx)} k_wbm launches, need {need}")
-    # the timed steps: from the launch after the k_wbm that closes the step before them
-    first_wbm = wbm_idx[-need]
+    # the timed steps: every launch after the k_wbm that closes the step before them
     prev_end = wbm_idx[-need - 1] if len(wbm_idx) > need else -1
-    # the step starts at the first k_prepare after the previous step's last k_wbm
-    start = next(i for i in range(prev_end + 1, first_wbm + 1) if seq[i]["kernel"] == "k_prepare")
-    timed = seq[start:]
+    timed = seq[prev_end + 1:]
     per = collections.defaultdict(lambda: collections.Counter())
     for d in timed:
         c = per[d["kernel"]]
