@@ -256,8 +256,10 @@ __device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32
 // results follow it in the same allocation (one D2H): u64 counts[2][nq]
 // ([phase][query] matches) and u32 timed_out[nq] (deadline fired).
 struct BatchState {
-  const BatchState* prev;        // the preceding batch of a pipelined stream (nullptr: none); a batch
-                                 // whose predecessor aborted aborts too (overflow 6)
+  BatchState* prev;              // the preceding batch of a pipelined stream (nullptr: none); a batch
+                                 // whose predecessor aborted aborts too (overflow 6).  Cleared by the
+                                 // next batch's K1: by then the merge has folded the predecessor's abort
+                                 // into this batch's own flags, and the predecessor's slot is reused
   uint32_t err_count;            // validate_batch failures
   uint32_t selfloop_min;         // first self-loop update index (kNone: none)
   uint32_t conflict_min;         // first conflicting update index (kNone: none)

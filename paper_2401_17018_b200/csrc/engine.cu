@@ -1563,7 +1563,7 @@ struct bdsm_engine {
   size_t stream_segment(const StreamBatch* bs, size_t i0, size_t k, bool device_input) {
     const size_t nq = queries.size();
     const size_t sb = st_size();
-    const size_t need = 2 * sb * (k - i0);
+    const size_t need = 2 * sb * std::max<size_t>(k - i0, 64);  // room for 64 batches up front
     if (h_stream_bytes < need) {
       if (h_stream) cudaFreeHost(h_stream);
       h_stream = nullptr;

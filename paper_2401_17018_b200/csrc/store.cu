@@ -165,7 +165,13 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
                           uint32_t key_bits) {
   // pipelined stream: this batch allocates from where its predecessor's merge
   // left the pool's bump pointer (k_prepare runs after that merge)
-  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) st->pool_top = st->prev->pool_top;
+  // The batch before that is complete (its abort, if any, was folded into
+  // st->prev's own flags by st->prev's merge) and its slot now holds this
+  // batch's state, so st->prev stops looking back.
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) {
+    st->pool_top = st->prev->pool_top;
+    st->prev->prev = nullptr;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
     if (up.u < g.V) up.u = new_of[up.u];
