@@ -334,6 +334,8 @@ struct bdsm_engine {
     if (h_stream) cudaFreeHost(h_stream);
     for (auto& x : stream_ev) cudaEventDestroy(x);
     for (auto& x : stream_kev) cudaEventDestroy(x);
+    for (auto& x : front_ev)
+      if (x) cudaEventDestroy(x);
     if (h_ups) cudaFreeHost(h_ups);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
@@ -1441,6 +1443,7 @@ struct bdsm_engine {
     return stream_kev[stream_kev_used++];
   }
   std::vector<std::pair<size_t, size_t>> seg_match_ev, seg_merge_ev;  // per batch: first/last kev index
+  cudaEvent_t front_ev[2] = {nullptr, nullptr};  // front A of the batch in slot s done (side stream)
 
   bool stream_ok() const {
     if (collect_cap || opts.l2_hot_mb) return false;
@@ -1449,45 +1452,59 @@ struct bdsm_engine {
     return !queries.empty();
   }
 
-  // Front part of a batch on slot cs: H2D, state template, K1 prepare, key
-  // sort, post-sort (flags, visibility table), insert prefix, segment heads.
-  void stream_front(const StreamBatch& sb, bool device_input, BatchState* prev, unsigned char* h_tmpl) {
+  // Front part A of a batch on slot cs, on stream `st` (the side stream while
+  // the previous batch merges): H2D, state template, the graph-independent
+  // half of K1, key sort, post-sort (conflicts, heads, visibility table),
+  // insert prefix, segment heads.  Part B (stream_validate) follows the
+  // previous batch's merge on the main stream.
+  void stream_front(const StreamBatch& sb, bool device_input, BatchState* prev, unsigned char* h_tmpl,
+                    cudaStream_t st, DBuf<uint8_t>& tmp_buf) {
     const size_t n = sb.n;
     ensure_batch(n);
     ensure_tasks(n);
     ensure_state();
     const bdsm_update_dev* src = reinterpret_cast<const bdsm_update_dev*>(sb.src);
     if (!device_input) {
-      CK(cudaMemcpyAsync(B().ups_ext.p, sb.src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(B().ups_ext.p, sb.src, n * sizeof(bdsm_update), cudaMemcpyHostToDevice, st));
       src = B().ups_ext.p;
     }
     std::memset(h_tmpl, 0, B().st_bytes);
     BatchState t = template_state();
     t.prev = prev;
     std::memcpy(h_tmpl, &t, sizeof(t));
-    CK(cudaMemcpyAsync(B().d_st, h_tmpl, B().st_bytes, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(B().d_st, h_tmpl, B().st_bytes, cudaMemcpyHostToDevice, st));
     const uint32_t m = uint32_t(2 * n);
-    const uint32_t nq = uint32_t(queries.size());
     const uint32_t id_bits = g.V > 1 ? 32u - uint32_t(__builtin_clz(g.V - 1)) : 1u;
     const bool full_sort = id_bits >= 32;
     const uint32_t key_bits = full_sort ? 32u : id_bits;
     const int sort_end_bit = full_sort ? 64 : int(2 * id_bits);
-    launch_prepare(src, uint32_t(n), view(), d_new_of.p, B().ups.p, B().d_st, B().keys.p, B().vals.p, B().dlab.p,
-                   B().ecode.p, full_sort ? 0xffffffffu : (1u << id_bits), key_bits, stream);
+    launch_translate(src, uint32_t(n), g.V, has_elab, d_new_of.p, B().ups.p, B().d_st, B().keys.p, B().vals.p,
+                     B().ecode.p, full_sort ? 0xffffffffu : (1u << id_bits), key_bits, st);
     cub::DoubleBuffer<uint64_t> kb(B().keys.p, B().keys2.p);
     cub::DoubleBuffer<uint32_t> vb(B().vals.p, B().vals2.p);
-    size_t tmp = cub_tmp.n;
-    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp, kb, vb, int(m), 0, sort_end_bit, stream));
-    CK(cudaMemsetAsync(B().hkeys.p, 0xff, sizeof(unsigned long long) * B().hkeys.n, stream));
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, int(m), 0, sort_end_bit, st));
+    tmp_buf.ensure(std::max(tmp, cub_bytes_for(n)));
+    tmp = tmp_buf.n;
+    CK(cub::DeviceRadixSort::SortPairs(tmp_buf.p, tmp, kb, vb, int(m), 0, sort_end_bit, st));
+    CK(cudaMemsetAsync(B().hkeys.p, 0xff, sizeof(unsigned long long) * B().hkeys.n, st));
     launch_post_sort(kb.Current(), vb.Current(), key_bits, B().skeys.p, B().svals.p, m, B().d_st, B().head.p,
-                     B().insflag.p, d_rows.p, nq, g.V, B().hkeys.p, B().hvals.p, uint32_t(B().hkeys.n - 1), cs, stream);
-    tmp = cub_tmp.n;
-    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, tmp, B().insflag.p, B().ins_prefix.p, int(m + 1), stream));
-    tmp = cub_tmp.n;
-    CK(cub::DeviceSelect::Flagged(cub_tmp.p, tmp, cub::CountingInputIterator<uint32_t>(0), B().head.p, B().heads.p,
-                                  &B().d_st->n_touched, int(m), stream));
+                     B().insflag.p, nullptr, 0, g.V, B().hkeys.p, B().hvals.p, uint32_t(B().hkeys.n - 1), cs, st);
+    tmp = tmp_buf.n;
+    CK(cub::DeviceScan::ExclusiveSum(tmp_buf.p, tmp, B().insflag.p, B().ins_prefix.p, int(m + 1), st));
+    tmp = tmp_buf.n;
+    CK(cub::DeviceSelect::Flagged(tmp_buf.p, tmp, cub::CountingInputIterator<uint32_t>(0), B().head.p, B().heads.p,
+                                  &B().d_st->n_touched, int(m), st));
     launches += 2;
     cub_calls += 3;
+  }
+
+  // Front part B (main stream, after the previous batch's merge): presence in
+  // G, pre-batch labels of deletes, batch-endpoint row flags, pool pointer.
+  void stream_validate(size_t n) {
+    launch_validate(B().ups.p, uint32_t(n), view(), B().d_st, B().dlab.p, B().ecode.p, d_rows.p,
+                    uint32_t(queries.size()), cs, stream);
+    ++launches;
   }
 
   // K3 + K4 of the batch on slot cs.
@@ -1570,6 +1587,8 @@ struct bdsm_engine {
       CK(cudaMallocHost(&h_stream, need));
       h_stream_bytes = need;
     }
+    for (auto& fe : front_ev)
+      if (!fe) CK(cudaEventCreateWithFlags(&fe, cudaEventDisableTiming));
     while (stream_ev.size() < k - i0 + 1) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -1584,7 +1603,17 @@ struct bdsm_engine {
     seg_merge_ev.assign(k - i0, {0, 0});
     CK(cudaEventRecord(stream_ev[0], stream));
     cs = 0;
-    stream_front(bs[i0], device_input, nullptr, h_tmpl(i0));
+    stream_front(bs[i0], device_input, nullptr, h_tmpl(i0), stream, cub_tmp);
+    stream_validate(bs[i0].n);
+    // front A of the second batch on the side stream (its slot is free)
+    if (i0 + 1 < k) {
+      CK(cudaEventRecord(fork_ev, stream));
+      CK(cudaStreamWaitEvent(side, fork_ev, 0));
+      cs = 1;
+      stream_front(bs[i0 + 1], device_input, slot_[0].d_st, h_tmpl(i0 + 1), side, cub_tmp_side);
+      CK(cudaEventRecord(front_ev[1], side));
+      cs = 0;
+    }
     seg_match_ev[0].first = stream_kev_used;
     for (size_t qi = 0; qi < nq; ++qi) {
       if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
@@ -1599,10 +1628,10 @@ struct bdsm_engine {
       stream_merge(bs[i].n);
       CK(cudaEventRecord(next_skev(), stream));
       seg_merge_ev[i - i0].second = stream_kev_used;
-      BatchState* st_i = slot_[s].d_st;
-      if (i + 1 < k) {
+      if (i + 1 < k) {  // front B of batch i+1 (its front A ran on the side stream)
         cs = t;
-        stream_front(bs[i + 1], device_input, st_i, h_tmpl(i + 1));
+        CK(cudaStreamWaitEvent(stream, front_ev[t], 0));
+        stream_validate(bs[i + 1].n);
       }
       if (i > i0) seg_match_ev[i - i0].first = stream_kev_used;
       for (size_t qi = 0; qi < nq; ++qi) {
@@ -1623,6 +1652,14 @@ struct bdsm_engine {
       ++launches;
       CK(cudaMemcpyAsync(h_res(i), B().d_st, sb, cudaMemcpyDeviceToHost, stream));
       CK(cudaEventRecord(stream_ev[i - i0 + 1], stream));
+      // slot s is free again: front A of batch i+2 on the side stream, beside
+      // batch i+1's merge
+      if (i + 2 < k) {
+        CK(cudaStreamWaitEvent(side, stream_ev[i - i0 + 1], 0));
+        cs = s;
+        stream_front(bs[i + 2], device_input, slot_[t].d_st, h_tmpl(i + 2), side, cub_tmp_side);
+        CK(cudaEventRecord(front_ev[s], side));
+      }
     }
     if (memo.p) {
       if (!h_memo_fill) CK(cudaMallocHost(&h_memo_fill, sizeof(unsigned long long)));

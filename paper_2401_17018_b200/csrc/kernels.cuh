@@ -58,6 +58,12 @@ void launch_compact(DevGraphMut g_old, const uint64_t* new_off, const uint32_t* 
 void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const uint32_t* new_of,
                     bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint32_t* dlab,
                     uint8_t* ecode, uint32_t id_limit, uint32_t key_bits, cudaStream_t s);
+// pipelined stream: K1 split around the previous batch's merge (store.cu)
+void launch_translate(const bdsm_update_dev* ups, uint32_t n, uint32_t V, bool has_elab, const uint32_t* new_of,
+                      bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint8_t* ecode,
+                      uint32_t id_limit, uint32_t key_bits, cudaStream_t s);
+void launch_validate(const bdsm_update_dev* iups, uint32_t n, DevGraph g, BatchState* st, uint32_t* dlab,
+                     uint8_t* ecode, uint32_t* const* rows, uint32_t nq, uint32_t slot, cudaStream_t s);
 void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t key_bits, uint64_t* out_keys,
                       uint32_t* out_vals, uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
                       uint32_t* const* rows, uint32_t nq, uint32_t V, unsigned long long* hkeys, uint32_t* hvals,

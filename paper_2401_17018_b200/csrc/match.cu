@@ -140,10 +140,20 @@ __device__ void anchor_self_scan(const PhaseArgs& a, AnchorCount& off, AnchorCou
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t first = blockIdx.x * blockDim.x;
   AnchorCount pre{0, 0, 0}, all{0, 0, 0};
-  for (uint32_t j = threadIdx.x; j < a.n_ups; j += blockDim.x) {
-    const AnchorCount v = a.upd_cnt[j];
-    all = ac_add(all, v);
-    if (j < first) pre = ac_add(pre, v);
+  // 8 independent loads in flight per thread (the sums do not wait on each other)
+  constexpr uint32_t U = 8;
+  for (uint32_t j0 = threadIdx.x; j0 < a.n_ups; j0 += blockDim.x * U) {
+    AnchorCount v[U];
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      const uint32_t j = j0 + k * blockDim.x;
+      v[k] = j < a.n_ups ? a.upd_cnt[j] : AnchorCount{0, 0, 0};
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < U; ++k) {
+      all = ac_add(all, v[k]);
+      if (j0 + k * blockDim.x < first) pre = ac_add(pre, v[k]);
+    }
   }
 #pragma unroll
   for (uint32_t o = 16; o; o >>= 1) {

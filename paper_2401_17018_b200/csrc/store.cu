@@ -211,6 +211,72 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
   }
 }
 
+// Pipelined stream, K1 in two parts.  k_translate is the graph-independent
+// part of k_prepare (ids, sort keys, self-loops, unknown vertices, labelled
+// inserts into an unlabelled graph), so the next batch's key sort can run on a
+// side stream while the current batch merges; k_validate is the rest, after
+// that merge: presence of every update in G (insert of an existing / delete of
+// a missing edge, src/graph.cpp:117-135), the pre-batch labels of deleted
+// edges, the batch-endpoint flags in the candidate rows, and the pool's bump
+// pointer taken over from the predecessor's merge.
+__global__ void k_translate(const bdsm_update_dev* __restrict__ ups, uint32_t n, uint32_t V, bool has_elab,
+                            const uint32_t* __restrict__ new_of, bdsm_update_dev* iups, BatchState* st,
+                            uint64_t* keys, uint32_t* vals, uint8_t* ecode, uint32_t id_limit, uint32_t key_bits) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    bdsm_update_dev up = ups[i];
+    if (up.u < V) up.u = new_of[up.u];
+    if (up.v < V) up.v = new_of[up.v];
+    iups[i] = up;
+    if (up.u >= id_limit || up.v >= id_limit) st->overflow = 5;
+    const uint32_t del = up.op != 0 ? 1u : 0u;
+    keys[2 * i] = (uint64_t(up.u) << key_bits) | up.v;
+    keys[2 * i + 1] = (uint64_t(up.v) << key_bits) | up.u;
+    vals[2 * i] = i | (del << 31);
+    vals[2 * i + 1] = i | (del << 31);
+    uint8_t code = 0;
+    if (up.u == up.v) atomicMin(&st->selfloop_min, i);
+    else if (up.u >= V || up.v >= V) code = 1;  // unknown vertex
+    if (code) atomicAdd(&st->err_count, 1u);
+    if (!del && up.elab != kNone && !has_elab) st->overflow = 4;
+    ecode[i] = code;
+  }
+}
+
+__global__ void k_validate(const bdsm_update_dev* __restrict__ iups, uint32_t n, DevGraph g, BatchState* st,
+                           uint32_t* dlab, uint8_t* ecode, uint32_t* const* rows, uint32_t nq, uint32_t flag_ins,
+                           uint32_t flag_del) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) {  // see k_prepare
+    st->pool_top = st->prev->pool_top;
+    st->prev->prev = nullptr;
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bdsm_update_dev up = iups[i];
+    const bool del = up.op != 0;
+    uint32_t lab = kNone;
+    if (up.u != up.v && up.u < g.V && up.v < g.V) {
+      const uint32_t du = g.deg[up.u], dv = g.deg[up.v];
+      const uint32_t x = du <= dv ? up.u : up.v, y = du <= dv ? up.v : up.u;
+      const uint32_t dx = du <= dv ? du : dv;
+      const uint32_t* lst = g.adj + g.off[x];
+      const uint32_t p = lower_bound_u32(lst, dx, y);
+      const bool present = p < dx && lst[p] == y;
+      uint8_t code = 0;
+      if (present && !del) code = 2;  // insert of existing edge
+      if (!present && del) code = 3;  // delete of missing edge
+      if (present && g.elab) lab = g.elab[g.off[x] + p];
+      if (code) {
+        ecode[i] = code;
+        atomicAdd(&st->err_count, 1u);
+      }
+      for (uint32_t q = 0; q < nq; ++q) {
+        atomicOr(rows[q] + up.u, del ? flag_del : flag_ins);
+        atomicOr(rows[q] + up.v, del ? flag_del : flag_ins);
+      }
+    }
+    dlab[i] = lab;
+  }
+}
+
 // After the radix sort of the 2n directed keys: conflicting pairs, segment
 // heads (distinct sources = touched vertices), insert flags for the merge
 // prefix, and the per-phase same-kind endpoint flags in the candidate rows
@@ -247,7 +313,7 @@ __global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t
     head[j] = h ? 1 : 0;
     insflag[j] = is_del ? 0u : 1u;
     if (src < V)
-      for (uint32_t q = 0; q < nq; ++q) atomicOr(rows[q] + src, is_del ? flag_del : flag_ins);
+      for (uint32_t q = 0; rows && q < nq; ++q) atomicOr(rows[q] + src, is_del ? flag_del : flag_ins);
     // visibility table: linear probing (duplicates only in rejected batches);
     // segment heads also map (src, kNone) -> the segment's first index
     for (int pass = 0; pass < (h ? 2 : 1); ++pass) {
@@ -1139,6 +1205,17 @@ void launch_prepare(const bdsm_update_dev* ups, uint32_t n, DevGraph g, const ui
                     uint8_t* ecode, uint32_t id_limit, uint32_t key_bits, cudaStream_t s) {
   k_prepare<<<blocks_for(n), kThreads, 0, s>>>(ups, n, g, new_of, iups, st, keys, vals, dlab, ecode, id_limit,
                                                key_bits);
+}
+void launch_translate(const bdsm_update_dev* ups, uint32_t n, uint32_t V, bool has_elab, const uint32_t* new_of,
+                      bdsm_update_dev* iups, BatchState* st, uint64_t* keys, uint32_t* vals, uint8_t* ecode,
+                      uint32_t id_limit, uint32_t key_bits, cudaStream_t s) {
+  k_translate<<<blocks_for(n), kThreads, 0, s>>>(ups, n, V, has_elab, new_of, iups, st, keys, vals, ecode, id_limit,
+                                                 key_bits);
+}
+void launch_validate(const bdsm_update_dev* iups, uint32_t n, DevGraph g, BatchState* st, uint32_t* dlab,
+                     uint8_t* ecode, uint32_t* const* rows, uint32_t nq, uint32_t slot, cudaStream_t s) {
+  k_validate<<<blocks_for(n), kThreads, 0, s>>>(iups, n, g, st, dlab, ecode, rows, nq, row_ins_flag(slot),
+                                                row_del_flag(slot));
 }
 void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t key_bits, uint64_t* out_keys,
                       uint32_t* out_vals, uint32_t m, BatchState* st, uint8_t* head, uint32_t* insflag,
