@@ -257,9 +257,10 @@ __device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32
 // ([phase][query] matches) and u32 timed_out[nq] (deadline fired).
 struct BatchState {
   BatchState* prev;              // the preceding batch of a pipelined stream (nullptr: none); a batch
-                                 // whose predecessor aborted aborts too (overflow 6).  Cleared by the
-                                 // next batch's K1: by then the merge has folded the predecessor's abort
-                                 // into this batch's own flags, and the predecessor's slot is reused
+                                 // whose predecessor aborted aborts too (overflow 6).  When the
+                                 // predecessor completes (its k_clear_flags, after the launch that ran
+                                 // its positive phase) its abort is folded into this batch's flags and
+                                 // the pointer cleared, before the predecessor's slot is reused
   uint32_t err_count;            // validate_batch failures
   uint32_t selfloop_min;         // first self-loop update index (kNone: none)
   uint32_t conflict_min;         // first conflicting update index (kNone: none)

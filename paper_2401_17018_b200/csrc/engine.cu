@@ -127,7 +127,22 @@ struct bdsm_engine {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   bool early_anchors = false;  // this attempt's negative-phase anchors were issued on `side`
   cudaEvent_t fork2_ev = nullptr, join2_ev = nullptr;  // the insert-prefix scan on `side`
+  // the long lists' merge (k_merge_big + k_finish_big) runs on its own stream
+  // beside the warp- and thread-per-list merges (disjoint lists, atomics on
+  // the shared structures)
+  cudaStream_t side_big = nullptr;
+  cudaEvent_t big_fork_ev = nullptr, big_join_ev = nullptr;
+  cudaStream_t fork_big() {
+    CK(cudaEventRecord(big_fork_ev, stream));
+    CK(cudaStreamWaitEvent(side_big, big_fork_ev, 0));
+    return side_big;
+  }
+  void join_big() {
+    CK(cudaEventRecord(big_join_ev, side_big));
+    CK(cudaStreamWaitEvent(stream, big_join_ev, 0));
+  }
   DBuf<uint8_t> cub_tmp_side;
+  DBuf<uint8_t> cub_tmp_big;  // CUB scratch of side_big (the stream's next-batch anchors)
   int num_sms = 148;
   bdsm_options opts{};
   DevGraphMut g{};
@@ -342,6 +357,9 @@ struct bdsm_engine {
     if (fork2_ev) cudaEventDestroy(fork2_ev);
     if (join2_ev) cudaEventDestroy(join2_ev);
     if (side) cudaStreamDestroy(side);
+    if (side_big) cudaStreamDestroy(side_big);
+    if (big_fork_ev) cudaEventDestroy(big_fork_ev);
+    if (big_join_ev) cudaEventDestroy(big_join_ev);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1176,7 +1194,8 @@ struct bdsm_engine {
     launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p, B().new_cap.p, B().ipos.p,
                          d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st, memo.p,
                          uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p, small_ok,
-                         num_sms, stream);
+                         num_sms, stream, fork_big());
+    join_big();
     CK(cudaEventRecord(m1, stream));
     launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
     cub_calls += 3; // sort, select, scan
@@ -1501,9 +1520,9 @@ struct bdsm_engine {
 
   // Front part B (main stream, after the previous batch's merge): presence in
   // G, pre-batch labels of deletes, batch-endpoint row flags, pool pointer.
-  void stream_validate(size_t n) {
+  void stream_validate(size_t n, cudaStream_t st) {
     launch_validate(B().ups.p, uint32_t(n), view(), B().d_st, B().dlab.p, B().ecode.p, d_rows.p,
-                    uint32_t(queries.size()), cs, stream);
+                    uint32_t(queries.size()), cs, st);
     ++launches;
   }
 
@@ -1516,43 +1535,50 @@ struct bdsm_engine {
     launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p,
                          B().new_cap.p, B().ipos.p, d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st,
                          memo.p, uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p,
-                         small_ok, num_sms, stream);
+                         small_ok, num_sms, stream, fork_big());
+    join_big();
     launches += small_ok ? 5 : 4;
   }
 
   // Anchors (K5), work queues and memo prefill of (phase, query) for the
   // batch on slot cs; the launch itself is left to the caller.
-  PhaseArgs stream_phase(uint32_t n, uint32_t phase, int qi) {
+  // st / tmp: the stream and CUB scratch to use (the next batch's negative
+  // anchors run on side_big beside this batch's positive anchors)
+  PhaseArgs stream_phase(uint32_t n, uint32_t phase, int qi, cudaStream_t st, DBuf<uint8_t>& tmp_buf) {
     QueryState& qs = *queries[size_t(qi)];
     PhaseArgs a = phase_args(n, phase, qi);
-    launch_anchor_count(a, stream);
+    launch_anchor_count(a, st);
     a.self_scan = n <= tune_self_scan;
     if (!a.self_scan) {
-      size_t tmp = cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveScan(cub_tmp.p, tmp, B().upd_cnt.p, B().upd_off.p, AnchorCountSum(),
-                                        AnchorCount{0, 0, 0}, int(n + 1), stream));
+      size_t tmp = 0;
+      CK(cub::DeviceScan::ExclusiveScan(nullptr, tmp, B().upd_cnt.p, B().upd_off.p, AnchorCountSum(),
+                                        AnchorCount{0, 0, 0}, int(n + 1), st));
+      tmp_buf.ensure(tmp);
+      tmp = tmp_buf.n;
+      CK(cub::DeviceScan::ExclusiveScan(tmp_buf.p, tmp, B().upd_cnt.p, B().upd_off.p, AnchorCountSum(),
+                                        AnchorCount{0, 0, 0}, int(n + 1), st));
       cub_calls += 1;
     }
-    launch_anchor_emit(a, stream);
+    launch_anchor_emit(a, st);
     launches += 2;
     if (qs.q.n > 2 && qs.has_leaf) {
       if (!memo_persistent) {
-        CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+        CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, st));
         qs.memo_cold = true;
       }
       if (qs.memo_cold) {
         refresh_hubs();
-        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, stream);
+        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, hub_ids.p, n_hubs.p, num_sms, st);
         qs.memo_cold = false;
         ++launches;
       } else if (phase == 1) {
-        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, stream);
+        launch_leaf_prefill(a, qs.leafsigs.p, qs.n_leafsig, nullptr, nullptr, num_sms, st);
         ++launches;
       }
     }
     if (qs.q.n > 2 && qs.natail && !tune_no_tasktail) {
       B().task_tail.ensure_grow(B().tasks.n * qs.natail);
-      CK(cudaMemsetAsync(B().task_tail.p, 0xff, sizeof(unsigned long long) * B().tasks.n * qs.natail, stream));
+      CK(cudaMemsetAsync(B().task_tail.p, 0xff, sizeof(unsigned long long) * B().tasks.n * qs.natail, st));
       a.task_tail = B().task_tail.p;
     }
     return a;
@@ -1604,7 +1630,7 @@ struct bdsm_engine {
     CK(cudaEventRecord(stream_ev[0], stream));
     cs = 0;
     stream_front(bs[i0], device_input, nullptr, h_tmpl(i0), stream, cub_tmp);
-    stream_validate(bs[i0].n);
+    stream_validate(bs[i0].n, stream);
     // front A of the second batch on the side stream (its slot is free)
     if (i0 + 1 < k) {
       CK(cudaEventRecord(fork_ev, stream));
@@ -1617,7 +1643,7 @@ struct bdsm_engine {
     seg_match_ev[0].first = stream_kev_used;
     for (size_t qi = 0; qi < nq; ++qi) {
       if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
-      PhaseArgs an = stream_phase(uint32_t(bs[i0].n), 0, int(qi));
+      PhaseArgs an = stream_phase(uint32_t(bs[i0].n), 0, int(qi), stream, cub_tmp);
       stream_launch(nullptr, &an, int(qi));
     }
     for (size_t i = i0; i < k; ++i) {
@@ -1628,27 +1654,43 @@ struct bdsm_engine {
       stream_merge(bs[i].n);
       CK(cudaEventRecord(next_skev(), stream));
       seg_merge_ev[i - i0].second = stream_kev_used;
+      // batch i+1's validation and negative anchors on side_big, beside batch
+      // i's positive anchors and prefill on the main stream (both read the
+      // merged graph; the memo's cold start stays on the main stream)
+      bool cold = !memo_persistent;
+      for (const auto& q : queries) cold = cold || q->memo_cold;
+      cudaStream_t nst = cold ? stream : side_big;
+      std::vector<PhaseArgs> an(nq);
       if (i + 1 < k) {  // front B of batch i+1 (its front A ran on the side stream)
         cs = t;
-        CK(cudaStreamWaitEvent(stream, front_ev[t], 0));
-        stream_validate(bs[i + 1].n);
+        if (nst != stream) {
+          CK(cudaEventRecord(big_fork_ev, stream));
+          CK(cudaStreamWaitEvent(nst, big_fork_ev, 0));
+        }
+        CK(cudaStreamWaitEvent(nst, front_ev[t], 0));
+        stream_validate(bs[i + 1].n, nst);
+        for (size_t qi = 0; qi < nq; ++qi)
+          if (queries[qi]->active && !queries[qi]->q.edges.empty())
+            an[qi] = stream_phase(uint32_t(bs[i + 1].n), 0, int(qi), nst, nst == stream ? cub_tmp : cub_tmp_big);
+        if (nst != stream) {
+          CK(cudaEventRecord(big_join_ev, nst));
+        }
       }
+      std::vector<PhaseArgs> ap(nq);
+      cs = s;
+      for (size_t qi = 0; qi < nq; ++qi)
+        if (queries[qi]->active && !queries[qi]->q.edges.empty())
+          ap[qi] = stream_phase(uint32_t(bs[i].n), 1, int(qi), stream, cub_tmp);
+      if (i + 1 < k && nst != stream) CK(cudaStreamWaitEvent(stream, big_join_ev, 0));
       if (i > i0) seg_match_ev[i - i0].first = stream_kev_used;
       for (size_t qi = 0; qi < nq; ++qi) {
         if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
-        cs = s;
-        PhaseArgs ap = stream_phase(uint32_t(bs[i].n), 1, int(qi));
-        if (i + 1 < k) {
-          cs = t;
-          PhaseArgs an = stream_phase(uint32_t(bs[i + 1].n), 0, int(qi));
-          stream_launch(&ap, &an, int(qi));
-        } else {
-          stream_launch(&ap, nullptr, int(qi));
-        }
+        stream_launch(&ap[qi], i + 1 < k ? &an[qi] : nullptr, int(qi));
       }
       seg_match_ev[i - i0].second = stream_kev_used;
       cs = s;
-      launch_clear_flags(B().skeys.p, uint32_t(2 * bs[i].n), d_rows.p, uint32_t(nq), g.V, s, stream);
+      launch_clear_flags(B().skeys.p, uint32_t(2 * bs[i].n), d_rows.p, uint32_t(nq), g.V, s, stream,
+                         i + 1 < k ? slot_[t].d_st : nullptr);
       ++launches;
       CK(cudaMemcpyAsync(h_res(i), B().d_st, sb, cudaMemcpyDeviceToHost, stream));
       CK(cudaEventRecord(stream_ev[i - i0 + 1], stream));
@@ -1893,6 +1935,9 @@ bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options*
     CK(cudaSetDevice(e->device));
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->side_big, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e->big_fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->big_join_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->join_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->fork2_ev, cudaEventDisableTiming));

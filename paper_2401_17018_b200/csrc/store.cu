@@ -165,13 +165,7 @@ __global__ void k_prepare(const bdsm_update_dev* __restrict__ ups, uint32_t n, D
                           uint32_t key_bits) {
   // pipelined stream: this batch allocates from where its predecessor's merge
   // left the pool's bump pointer (k_prepare runs after that merge)
-  // The batch before that is complete (its abort, if any, was folded into
-  // st->prev's own flags by st->prev's merge) and its slot now holds this
-  // batch's state, so st->prev stops looking back.
-  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) {
-    st->pool_top = st->prev->pool_top;
-    st->prev->prev = nullptr;
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) st->pool_top = st->prev->pool_top;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     bdsm_update_dev up = ups[i];
     if (up.u < g.V) up.u = new_of[up.u];
@@ -245,10 +239,7 @@ __global__ void k_translate(const bdsm_update_dev* __restrict__ ups, uint32_t n,
 __global__ void k_validate(const bdsm_update_dev* __restrict__ iups, uint32_t n, DevGraph g, BatchState* st,
                            uint32_t* dlab, uint8_t* ecode, uint32_t* const* rows, uint32_t nq, uint32_t flag_ins,
                            uint32_t flag_del) {
-  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) {  // see k_prepare
-    st->pool_top = st->prev->pool_top;
-    st->prev->prev = nullptr;
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && st->prev) st->pool_top = st->prev->pool_top;  // see k_prepare
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const bdsm_update_dev up = iups[i];
     const bool del = up.op != 0;
@@ -333,8 +324,16 @@ __global__ void k_post_sort(const uint64_t* __restrict__ in_keys, const uint32_t
 
 // End of batch (also after a rejected one): clear the per-batch row flags of
 // every touched vertex.
+// Pipelined stream: `next` is the following batch's state.  This batch is
+// complete now, so `next` folds this batch's abort into its own flags and
+// stops looking back — before this batch's slot is handed to the batch after
+// `next` (whose state overwrites it).
 __global__ void k_clear_flags(const uint64_t* __restrict__ skeys, uint32_t m, uint32_t* const* rows,
-                              uint32_t nq, uint32_t V, uint32_t flags) {
+                              uint32_t nq, uint32_t V, uint32_t flags, BatchState* next) {
+  if (next && blockIdx.x == 0 && threadIdx.x == 0 && next->prev) {
+    if (batch_aborted_own(next->prev)) next->overflow = 6;
+    next->prev = nullptr;
+  }
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
     uint32_t src = uint32_t(skeys[j] >> 32);
     if (src < V && (j == 0 || uint32_t(skeys[j - 1] >> 32) != src))
@@ -1226,8 +1225,9 @@ void launch_post_sort(const uint64_t* in_keys, const uint32_t* in_vals, uint32_t
                                                               row_ins_flag(slot), row_del_flag(slot));
 }
 void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows, uint32_t nq, uint32_t V,
-                        uint32_t slot, cudaStream_t s) {
-  k_clear_flags<<<blocks_for(m), kThreads, 0, s>>>(skeys, m, rows, nq, V, row_ins_flag(slot) | row_del_flag(slot));
+                        uint32_t slot, cudaStream_t s, BatchState* next) {
+  k_clear_flags<<<blocks_for(m), kThreads, 0, s>>>(skeys, m, rows, nq, V, row_ins_flag(slot) | row_del_flag(slot),
+                                                   next);
 }
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
@@ -1242,7 +1242,8 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
                           uint32_t memo_mask, const uint32_t* big_list, const uint32_t* small_list,
-                          const uint32_t* mid_list, bool small_ok, int num_sms, cudaStream_t s) {
+                          const uint32_t* mid_list, bool small_ok, int num_sms, cudaStream_t s,
+                          cudaStream_t s_big) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
@@ -1256,10 +1257,12 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                     0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
                             st, memo, memo_mask, small_list);
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
-  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), BDSM_BIG_THREADS, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+  // long lists (disjoint from the others; shared structures are updated with
+  // atomics) on s_big, which the caller may run beside s
+  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), BDSM_BIG_THREADS, 0, s_big>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, big_list);
   k_finish_big<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * 32 + 255) / 256, uint64_t(num_sms) * 8)), 256, 0,
-                 s>>>(heads, skeys, svals, m, g, qenc, nq, rows, colsize, st, memo, memo_mask, big_list);
+                 s_big>>>(heads, skeys, svals, m, g, qenc, nq, rows, colsize, st, memo, memo_mask, big_list);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
   k_encode_all<<<unsigned(num_sms * 16), 256, 0, s>>>(g, qenc, rows);

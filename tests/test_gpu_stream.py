@@ -114,33 +114,46 @@ def test_stream_device_input():
     e.close()
 
 
-def test_stream_rejected_batch_stops_there():
+@pytest.mark.parametrize("kind", ["missing_delete", "self_loop", "conflict"])
+@pytest.mark.parametrize("at", [1, 2, 3])
+def test_stream_rejected_batch_stops_there(kind, at):
+    """A rejected batch (validation error found after the previous batch's
+    merge, or a self-loop / conflicting pair found before it) stops the stream
+    there: the batches before it are applied and reported, nothing of it."""
     import paper_2401_17018_b200 as bd
     vl, eu, ev, batches = _random_workload(7)
     present = {(int(a), int(b)) for a, b in zip(eu, ev)}
-    for b in batches[:2]:
+    for b in batches[:at]:
         for op, x, y in b:
             (present.add if op == 0 else present.discard)((min(x, y), max(x, y)))
-    # batch 2 starts with a delete of a missing edge -> BatchError, nothing of it applied
-    used = {(min(x, y), max(x, y)) for _, x, y in batches[2]}
-    missing = next((a, b) for a in range(len(vl)) for b in range(a + 1, len(vl))
-                   if (a, b) not in present and (a, b) not in used)
-    bad = [(1, missing[0], missing[1])] + list(batches[2])
-    stream = [batches[0], batches[1], bad, batches[3]]
+    used = {(min(x, y), max(x, y)) for _, x, y in batches[at]}
+    if kind == "missing_delete":  # found by the validation after the previous merge
+        missing = next((a, b) for a in range(len(vl)) for b in range(a + 1, len(vl))
+                       if (a, b) not in present and (a, b) not in used)
+        bad = [(1, missing[0], missing[1])] + list(batches[at])
+        err = bd.BatchError
+    elif kind == "self_loop":  # found before the sort
+        bad = list(batches[at]) + [(0, 5, 5)]
+        err = ValueError
+    else:  # the same pair twice: found after the sort
+        bad = list(batches[at]) + [(batches[at][0][0], batches[at][0][2], batches[at][0][1])]
+        err = ValueError
+    stream = batches[:at] + [bad] + batches[at + 1:]
     e = bd.Engine(vl, eu, ev)
     o = Oracle(vl, eu, ev)
     for ql, qe in QUERIES:
         e.add_query(ql, qe)
         o.add_query(ql, qe)
-    with pytest.raises(bd.BatchError) as ei:
+    with pytest.raises(err) as ei:
         e.match_stream(stream)
-    assert ei.value.done == 2 and len(ei.value.results) == 2
-    for b, r in zip(stream[:2], ei.value.results):
+    assert ei.value.done == at and len(ei.value.results) == at
+    for b, r in zip(stream[:at], ei.value.results):
         pos, neg, _ = o.apply_batch(b)
         assert (r.positive, r.negative) == (pos, neg)
-    assert ei.value.failures and ei.value.failures[0][0] == 0
-    # the engine holds exactly the first two batches: the rest of the stream matches the oracle
-    for b in batches[2:]:
+    if kind == "missing_delete":
+        assert ei.value.failures and ei.value.failures[0][0] == 0
+    # the engine holds exactly the batches before the bad one: the rest matches the oracle
+    for b in batches[at:]:
         r = e.match_batch(b)
         pos, neg, _ = o.apply_batch(b)
         assert (r.positive, r.negative) == (pos, neg)
