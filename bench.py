@@ -374,13 +374,13 @@ def ours(args, world, rank, local):
     engB = bd.Engine(wl.labels, wl.src, wl.dst, device=local, shard_rank=rank, shard_world=world,
                      chunk=args.chunk, l2_hot_mb=args.l2_hot_mb, coalesce=args.coalesce)
     engB.add_query(wl.qlabels, wl.qedges)
-    # pipelined stream (1 GPU): A and B run the timed batches as one stream,
-    # C replays them one batch at a time for the per-batch latency
-    # (graphs whose adjacency fits L2 are timed one flushed batch at a time)
-    pipelined = world == 1 and not args.no_stream and 8 * wl.meta["E"] >= (256 << 20)
+    # pipelined stream: A and B run the timed batches as one stream, L (one
+    # GPU) replays them one batch at a time for the per-batch latency (graphs
+    # whose adjacency fits L2 are timed one flushed batch at a time)
+    pipelined = not args.no_stream and 8 * wl.meta["E"] >= (256 << 20)
     args.no_stream = not pipelined
     engL = None
-    if pipelined:
+    if pipelined and world == 1:
         engL = bd.Engine(wl.labels, wl.src, wl.dst, device=local, chunk=args.chunk, l2_hot_mb=args.l2_hot_mb,
                          coalesce=args.coalesce)
         engL.add_query(wl.qlabels, wl.qedges)
@@ -440,7 +440,7 @@ def ours(args, world, rank, local):
     with ClockSampler(local if not os.environ.get("CUDA_VISIBLE_DEVICES") else 0) as clk:
         if pipelined:
             # per-batch latency: one apply per batch, L2 flushed before each
-            for i in range(args.warmup, nb):
+            for i in range(args.warmup, nb) if engL else []:
                 flush.zero_()
                 torch.cuda.synchronize()
                 r = engL.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
@@ -449,17 +449,37 @@ def ours(args, world, rank, local):
             # value: the timed batches as one pipelined stream from HBM
             # (bdsm_engine_apply_stream); the graph (> 1 GB) exceeds L2
             flush.zero_()
-            torch.cuda.synchronize()
+            barrier()
+            if use_nccl:
+                # multi-GPU stream: NCCL broadcast of the
+                # timed batches from rank 0, every rank streams them through its
+                # replica counting its share of the work units, NCCL all-reduce
+                # of the counts; CUDA events around all of it, max over ranks
+                import torch.distributed as dist
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                for i in range(args.warmup, nb):
+                    dist.broadcast(dev_batches[i].view(torch.int32), src=0)
+                torch.cuda.current_stream().synchronize()
             rs = engA.match_stream_device([dev_batches[i].data_ptr() for i in range(args.warmup, nb)],
                                           [len(wl.batches[i]) for i in range(args.warmup, nb)])
             for r in rs:
                 dev_ms.append(r.stats["ms_device"])
                 statsA.append(r.stats)
                 countsA.append((r.positive[0], r.negative[0]))
+            if use_nccl:
+                cnt = torch.tensor([c for r in rs for c in (r.positive[0], r.negative[0])], dtype=torch.int64,
+                                   device=dev)
+                dist.all_reduce(cnt)
+                ev1.record()
+                ev1.synchronize()
+                total = ev0.elapsed_time(ev1)
+                dev_ms = [total / args.steps] * args.steps
+                nccl_totals.extend(tuple(x) for x in cnt.view(-1, 2).tolist())
             # e2e: the same stream through the C ABI with page-locked host
             # batches: every batch's H2D and its counts' D2H in the timed region
             flush.zero_()
-            torch.cuda.synchronize()
+            barrier()
             t1 = time.perf_counter()
             rs = engB.match_stream([pinned_batches[i] for i in range(args.warmup, nb)])
             e2e_total = (time.perf_counter() - t1) * 1e3

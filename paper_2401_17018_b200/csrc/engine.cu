@@ -1656,12 +1656,13 @@ struct bdsm_engine {
       seg_merge_ev[i - i0].second = stream_kev_used;
       // batch i+1's validation and negative anchors on side_big, beside batch
       // i's positive anchors and prefill on the main stream (both read the
-      // merged graph; the memo's cold start stays on the main stream)
+      // merged graph; the memo's cold start stays on the main stream).  Per
+      // query, as the slots' task and item buffers are shared by the queries.
       bool cold = !memo_persistent;
       for (const auto& q : queries) cold = cold || q->memo_cold;
       cudaStream_t nst = cold ? stream : side_big;
-      std::vector<PhaseArgs> an(nq);
-      if (i + 1 < k) {  // front B of batch i+1 (its front A ran on the side stream)
+      const bool next = i + 1 < k;
+      if (next) {  // front B of batch i+1 (its front A ran on the side stream)
         cs = t;
         if (nst != stream) {
           CK(cudaEventRecord(big_fork_ev, stream));
@@ -1669,23 +1670,26 @@ struct bdsm_engine {
         }
         CK(cudaStreamWaitEvent(nst, front_ev[t], 0));
         stream_validate(bs[i + 1].n, nst);
-        for (size_t qi = 0; qi < nq; ++qi)
-          if (queries[qi]->active && !queries[qi]->q.edges.empty())
-            an[qi] = stream_phase(uint32_t(bs[i + 1].n), 0, int(qi), nst, nst == stream ? cub_tmp : cub_tmp_big);
-        if (nst != stream) {
-          CK(cudaEventRecord(big_join_ev, nst));
-        }
       }
-      std::vector<PhaseArgs> ap(nq);
-      cs = s;
-      for (size_t qi = 0; qi < nq; ++qi)
-        if (queries[qi]->active && !queries[qi]->q.edges.empty())
-          ap[qi] = stream_phase(uint32_t(bs[i].n), 1, int(qi), stream, cub_tmp);
-      if (i + 1 < k && nst != stream) CK(cudaStreamWaitEvent(stream, big_join_ev, 0));
       if (i > i0) seg_match_ev[i - i0].first = stream_kev_used;
+      bool first_q = true;
       for (size_t qi = 0; qi < nq; ++qi) {
         if (!queries[qi]->active || queries[qi]->q.edges.empty()) continue;
-        stream_launch(&ap[qi], i + 1 < k ? &an[qi] : nullptr, int(qi));
+        PhaseArgs an{};
+        if (next) {
+          cs = t;
+          if (nst != stream && !first_q) {  // the previous query's launch has read the buffers
+            CK(cudaEventRecord(big_fork_ev, stream));
+            CK(cudaStreamWaitEvent(nst, big_fork_ev, 0));
+          }
+          an = stream_phase(uint32_t(bs[i + 1].n), 0, int(qi), nst, nst == stream ? cub_tmp : cub_tmp_big);
+          if (nst != stream) CK(cudaEventRecord(big_join_ev, nst));
+        }
+        cs = s;
+        PhaseArgs ap = stream_phase(uint32_t(bs[i].n), 1, int(qi), stream, cub_tmp);
+        if (next && nst != stream) CK(cudaStreamWaitEvent(stream, big_join_ev, 0));
+        stream_launch(&ap, next ? &an : nullptr, int(qi));
+        first_q = false;
       }
       seg_match_ev[i - i0].second = stream_kev_used;
       cs = s;

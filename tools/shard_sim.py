@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-stream", dest="stream", action="store_false",
+                    help="one apply per batch instead of the pipelined stream")
     args = ap.parse_args()
     worlds = [int(w) for w in args.worlds.split(",")]
     dev = torch.device("cuda", 0)
@@ -54,6 +56,7 @@ def main():
     bcast_ms = 16 * wl.meta["batch"] / (NVLINK_GBPS * 1e9) * 1e3 + COLL_LATENCY_MS
     reduce_ms = COLL_LATENCY_MS
     res = {"config": args.config, "V": wl.meta["V"], "E": wl.meta["E"], "batch": wl.meta["batch"],
+           "mode": "pipelined stream per rank" if args.stream else "one apply per batch per rank",
            "steps": args.steps, "warmup": args.warmup, "gen_s": gen_s,
            "collectives_ms": {"broadcast": bcast_ms, "allreduce": reduce_ms,
                               "model": f"16 B/update at {NVLINK_GBPS} GB/s + {COLL_LATENCY_MS} ms per collective"},
@@ -66,7 +69,19 @@ def main():
             eng = bd.Engine(wl.labels, wl.src, wl.dst, device=0, shard_rank=r, shard_world=Wd)
             eng.add_query(wl.qlabels, wl.qedges)
             per, cnt = [], []
-            for i in range(nb):
+            if args.stream:  # warm-up and timed batches each as one pipelined stream
+                for lo, hi, keep in ((0, args.warmup, False), (args.warmup, nb, True)):
+                    flush.zero_()
+                    torch.cuda.synchronize()
+                    rs = eng.match_stream_device([dev_batches[i].data_ptr() for i in range(lo, hi)],
+                                                 [len(wl.batches[i]) for i in range(lo, hi)])
+                    for rr in rs:
+                        cnt.append((rr.positive[0], rr.negative[0]))
+                        if keep:
+                            s = rr.stats
+                            per.append({k: s[k] for k in ("ms_device", "ms_match_kernel", "ms_merge_kernel",
+                                                          "work_items")})
+            for i in range(nb) if not args.stream else []:
                 flush.zero_()
                 torch.cuda.synchronize()
                 rr = eng.match_batch_device(dev_batches[i].data_ptr(), len(wl.batches[i]))
@@ -81,10 +96,18 @@ def main():
             ranks.append(per)
         if base_counts is None:
             base_counts = counts_sum
-        step_max = [max(ranks[r][k]["ms_device"] for r in range(Wd)) for k in range(args.steps)]
+        # the stream's per-batch times are pipeline steps: compare the ranks'
+        # total time over the timed batches
+        if args.stream:
+            tot = [sum(p["ms_device"] for p in ranks[r]) for r in range(Wd)]
+            step_max = [max(tot) / args.steps] * args.steps
+        else:
+            step_max = [max(ranks[r][k]["ms_device"] for r in range(Wd)) for k in range(args.steps)]
         kmax = [max(ranks[r][k]["ms_match_kernel"] for r in range(Wd)) for k in range(args.steps)]
         repl = [statistics.mean(ranks[r][k]["ms_device"] - ranks[r][k]["ms_match_kernel"] for r in range(Wd))
                 for k in range(args.steps)]
+        # one broadcast of the batch and one count reduction per step (a stream
+        # needs only one reduction at its end; counted per step to stay safe)
         pred = [s + (bcast_ms + reduce_ms if Wd > 1 else 0.0) for s in step_max]
         res["worlds"][str(Wd)] = {
             "predicted_ms_per_step": statistics.mean(pred),
