@@ -36,6 +36,9 @@ struct DevGraph {
   const uint32_t* hub_slot;
   const uint32_t* bitmaps;
   uint64_t bm_words;       // words per bitmap ((V + 31) / 32)
+  // bit v set: the weight memo may hold entries of vertex v (set by memo_put,
+  // cleared with the memo); the merge's invalidations skip the others
+  uint32_t* memo_bits;
 };
 
 constexpr uint32_t kMaxLabelIndex = 64;
@@ -236,6 +239,16 @@ __device__ __forceinline__ bool memo_put(unsigned long long* memo, uint32_t mask
   return false;
 }
 
+__device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
+                                                uint32_t sig);
+// The merge's invalidation of x's entries: a probe only when x ever had one
+// (most touched vertices of a large batch never did: one bit load instead of a
+// random probe of the memo per signature).
+__device__ __forceinline__ void memo_invalidate_v(const uint32_t* memo_bits, unsigned long long* memo,
+                                                  uint32_t mask, uint32_t x, uint32_t q, uint32_t sig) {
+  if (memo_bits && !((__ldcg(memo_bits + (x >> 5)) >> (x & 31)) & 1u)) return;
+  memo_invalidate(memo, mask, x, q, sig);
+}
 __device__ __forceinline__ void memo_invalidate(unsigned long long* memo, uint32_t mask, uint32_t x, uint32_t q,
                                                 uint32_t sig) {
   const unsigned long long tag = memo_tag(x, q, sig);

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/bdsm_gpu.h"
 #include "kernels.cuh"
@@ -27,6 +28,13 @@ using namespace bdsm_b200;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range over a host scope (the enqueue of a batch stage; nsys / ncu
+// --nvtx show them beside the kernels)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 struct CudaFailure : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -200,9 +208,11 @@ struct bdsm_engine {
   uint32_t qs_natail(int qi) const { return queries.at(size_t(qi))->natail; }
   bool memo_persistent = true;     // false when a query has too many signatures to invalidate
   unsigned long long* h_memo_fill = nullptr;  // pinned copy of memo_fill, refreshed every batch
+  DBuf<uint32_t> memo_bits;  // DevGraph::memo_bits
   void reset_memo() {
     if (!memo.p) return;
     CK(cudaMemsetAsync(memo.p, 0xff, sizeof(unsigned long long) * memo.n, stream));
+    if (memo_bits.p) CK(cudaMemsetAsync(memo_bits.p, 0, 4 * memo_bits.n, stream));
     CK(cudaMemsetAsync(memo_fill.p, 0, sizeof(unsigned long long), stream));
     for (auto& q : queries) q->memo_cold = true;
   }
@@ -377,6 +387,7 @@ struct bdsm_engine {
     v.hub_slot = g.hub_slot;
     v.bitmaps = g.bitmaps;
     v.bm_words = g.bm_words;
+    v.memo_bits = g.memo_bits;
     return v;
   }
 
@@ -614,6 +625,7 @@ struct bdsm_engine {
     g.hub_slot = hub_slot.n ? hub_slot.p : nullptr;
     g.bitmaps = bitmaps.p;
     g.bm_words = bm_words;
+    g.memo_bits = memo_bits.p;
   }
 
   [[noreturn]] void throw_build_error(const bdsm_graph_desc* d, uint32_t bad) {
@@ -773,6 +785,8 @@ struct bdsm_engine {
       while (words < g.V && words < (size_t(1) << 25)) words <<= 1;
       memo.ensure(words);
       memo_fill.ensure(1);
+      memo_bits.ensure(std::max<size_t>((size_t(g.V) + 31) / 32, 1));
+      refresh_graph_view();
       reset_memo();
     }
     std::vector<EdgeProg> progs;
@@ -996,6 +1010,7 @@ struct bdsm_engine {
   }
 
   void run_phase(uint32_t n, uint32_t phase) {
+    Nvtx range(phase == 0 ? "bdsm negative phase" : "bdsm positive phase");
     for (size_t qi = 0; qi < queries.size(); ++qi) {
       QueryState& qs = *queries[qi];
       if (!qs.active || qs.q.edges.empty()) continue;
@@ -1113,6 +1128,7 @@ struct bdsm_engine {
   Pending pend;
 
   void launch_attempt() {
+    Nvtx range("bdsm batch");
     const size_t n = pend.n;
     const bool device_input = pend.device_input;
     const bdsm_update_dev* src = pend.src;
@@ -1478,6 +1494,7 @@ struct bdsm_engine {
   // previous batch's merge on the main stream.
   void stream_front(const StreamBatch& sb, bool device_input, BatchState* prev, unsigned char* h_tmpl,
                     cudaStream_t st, DBuf<uint8_t>& tmp_buf) {
+    Nvtx range("bdsm front");
     const size_t n = sb.n;
     ensure_batch(n);
     ensure_tasks(n);
@@ -1528,6 +1545,7 @@ struct bdsm_engine {
 
   // K3 + K4 of the batch on slot cs.
   void stream_merge(size_t n) {
+    Nvtx range("bdsm merge");
     const uint32_t m = uint32_t(2 * n);
     const bool small_ok = m >= tune_small_min;
     launch_alloc(B().heads.p, B().skeys.p, B().ins_prefix.p, m, view(), opts.slack, B().d_st, B().new_off.p,
@@ -1604,6 +1622,7 @@ struct bdsm_engine {
   // Enqueues batches [i0, k) and waits; returns the first batch whose state is
   // abnormal (k if none).  Results of the batches before it are in h_res(i).
   size_t stream_segment(const StreamBatch* bs, size_t i0, size_t k, bool device_input) {
+    Nvtx range("bdsm stream segment");
     const size_t nq = queries.size();
     const size_t sb = st_size();
     const size_t need = 2 * sb * std::max<size_t>(k - i0, 64);  // room for 64 batches up front

@@ -39,6 +39,7 @@ struct DevGraphMut {
   const uint32_t* hub_slot;      // membership bitmaps (see DevGraph), or nullptr
   uint32_t* bitmaps;
   uint64_t bm_words;
+  uint32_t* memo_bits;           // see DevGraph
 };
 
 // ---- store.cu: build ------------------------------------------------------

@@ -612,7 +612,11 @@ __device__ __forceinline__ bool memo_get(const PhaseArgs& a, uint32_t x, uint32_
 }
 
 __device__ __forceinline__ void memo_put(const PhaseArgs& a, uint32_t x, uint32_t sig, unsigned long long w) {
-  if (::bdsm_b200::memo_put(a.memo, a.memo_mask, x, a.query, sig, w)) atomicAdd(a.memo_fill, 1ull);
+  if (::bdsm_b200::memo_put(a.memo, a.memo_mask, x, a.query, sig, w)) {
+    atomicAdd(a.memo_fill, 1ull);
+    if (a.g.memo_bits && !((__ldcg(a.g.memo_bits + (x >> 5)) >> (x & 31)) & 1u))
+      atomicOr(a.g.memo_bits + (x >> 5), 1u << (x & 31));
+  }
 }
 
 // Per-lane leaf weight of level t for the lane's level-T candidate c (lanes

@@ -482,7 +482,7 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
                                               unsigned long long* memo, uint32_t memo_mask, uint32_t lane) {
   // the memoised weights of x (its list changed) are stale in every query
   for (uint32_t q = 0; q < nq; ++q)
-    for (uint32_t k = lane; k < qenc[q].nsig; k += 32) memo_invalidate(memo, memo_mask, x, q, qenc[q].sig[k]);
+    for (uint32_t k = lane; k < qenc[q].nsig; k += 32) memo_invalidate_v(g.memo_bits, memo, memo_mask, x, q, qenc[q].sig[k]);
     // membership bitmap of a hub: set inserted, clear deleted neighbours
     if (g.hub_slot) {
       const uint32_t hs = g.hub_slot[x];
@@ -550,7 +550,7 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
         for (uint32_t k = 0; k < qe.nsig; ++k) {
           const uint32_t sg = qe.sig[k];
           if (!((diff >> (sg & 15)) & 1u)) continue;
-          for (uint32_t i = lane; i < dnew; i += 32) memo_invalidate(memo, memo_mask, dst[i], q, sg);
+          for (uint32_t i = lane; i < dnew; i += 32) memo_invalidate_v(g.memo_bits, memo, memo_mask, dst[i], q, sg);
         }
       }
     }
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
       }
     }
     for (uint32_t q = 0; q < nq; ++q)
-      for (uint32_t k = 0; k < qenc[q].nsig; ++k) memo_invalidate(memo, memo_mask, x, q, qenc[q].sig[k]);
+      for (uint32_t k = 0; k < qenc[q].nsig; ++k) memo_invalidate_v(g.memo_bits, memo, memo_mask, x, q, qenc[q].sig[k]);
     // label index of the new list from the old one: class k's first
     // position moves by the inserts minus the deletes below class_lo[k]
     uint32_t lpos[kMaxLabelIndex + 1];
@@ -876,7 +876,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
         for (uint32_t k = 0; k < qe.nsig; ++k) {  // neighbours' weights that count a flipped bit
           const uint32_t sg = qe.sig[k];
           if ((diff >> (sg & 15)) & 1u)
-            for (uint32_t i = 0; i < dnew; ++i) memo_invalidate(memo, memo_mask, dst[i], q, sg);
+            for (uint32_t i = 0; i < dnew; ++i) memo_invalidate_v(g.memo_bits, memo, memo_mask, dst[i], q, sg);
         }
       }
     }
