@@ -472,6 +472,31 @@ __device__ __forceinline__ uint32_t row_of(const DevQueryEnc& qe, uint32_t vl, u
   return row;
 }
 
+// Column-size deltas (CandidateTable column |C(u)|, read by the planner) of
+// the first kColAggQ queries are summed per block in shared memory and added
+// to the global counters once per block: a large batch flips thousands of
+// rows, and per-list atomics on the same few counters serialise in L2.
+constexpr uint32_t kColAggQ = 2;
+struct ColAgg {
+  int (*s)[kMaxQ];  // [kColAggQ][kMaxQ] shared accumulators
+  __device__ __forceinline__ void init() {
+    for (uint32_t i = threadIdx.x; i < kColAggQ * kMaxQ; i += blockDim.x) s[i / kMaxQ][i % kMaxQ] = 0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void add(uint64_t* const* colsize, uint32_t q, uint32_t u, bool up) {
+    if (q < kColAggQ) atomicAdd(&s[q][u], up ? 1 : -1);
+    else atomicAdd((unsigned long long*)(colsize[q] + u), up ? 1ull : (unsigned long long)(-1ll));
+  }
+  __device__ __forceinline__ void flush(uint64_t* const* colsize, uint32_t nq) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kColAggQ * kMaxQ; i += blockDim.x) {
+      const uint32_t q = i / kMaxQ, u = i % kMaxQ;
+      const int v = s[q][u];
+      if (q < nq && v) atomicAdd((unsigned long long*)(colsize[q] + u), (unsigned long long)(long long)v);
+    }
+  }
+};
+
 // After a list's merge (warp-collective): keep its membership bitmap in step,
 // rewrite its label index, and recompute every query's candidate row from the
 // label-range counts of the new list (K4).
@@ -479,7 +504,8 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
                                               const uint64_t* seg, uint32_t segn, const uint32_t* segvals,
                                               const DevQueryEnc* __restrict__ qenc, uint32_t nq,
                                               uint32_t* const* rows, uint64_t* const* colsize,
-                                              unsigned long long* memo, uint32_t memo_mask, uint32_t lane) {
+                                              unsigned long long* memo, uint32_t memo_mask, uint32_t lane,
+                                              ColAgg agg) {
   // the memoised weights of x (its list changed) are stale in every query
   for (uint32_t q = 0; q < nq; ++q)
     for (uint32_t k = lane; k < qenc[q].nsig; k += 32) memo_invalidate_v(g.memo_bits, memo, memo_mask, x, q, qenc[q].sig[k]);
@@ -540,8 +566,7 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
           while (d) {
             uint32_t u = __ffs(d) - 1;
             d &= d - 1;
-            atomicAdd((unsigned long long*)(colsize[q] + u),
-                      (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
+            agg.add(colsize, q, u, (row >> u) & 1u);
           }
         }
         // x's candidate bits changed: the memoised weights of its neighbours
@@ -585,6 +610,9 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     if (threadIdx.x == 0 && blockIdx.x == 0) st->overflow = 1;
     return;
   }
+  __shared__ int s_colagg[kColAggQ][kMaxQ];
+  ColAgg agg{s_colagg};
+  agg.init();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -690,9 +718,10 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
       }
     }
     bytes += 4ull * (uint64_t(dold) + dnew);
-    finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, memo, memo_mask, lane);
+    finish_vertex(g, x, dst, dnew, seg, segn, svals + s, qenc, nq, rows, colsize, memo, memo_mask, lane, agg);
   }
   if (lane == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+  agg.flush(colsize, nq);
 }
 
 // Short lists (<= kSmallList entries before and after the batch; most touched
@@ -714,6 +743,9 @@ __global__ void __launch_bounds__(256) k_merge_small(
     uint32_t memo_mask, const uint32_t* __restrict__ small_list) {
   if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
+  __shared__ int s_colagg[kColAggQ][kMaxQ];
+  ColAgg agg{s_colagg};
+  agg.init();
   const uint32_t nt = st->n_touched, nsmall = st->n_small;
   uint64_t bytes = 0;
   for (uint32_t si = blockIdx.x * blockDim.x + threadIdx.x; si < nsmall; si += gridDim.x * blockDim.x) {
@@ -871,7 +903,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
         while (d) {
           const uint32_t u = __ffs(d) - 1;
           d &= d - 1;
-          atomicAdd((unsigned long long*)(colsize[q] + u), (row >> u) & 1u ? 1ull : (unsigned long long)(-1ll));
+          agg.add(colsize, q, u, (row >> u) & 1u);
         }
         for (uint32_t k = 0; k < qe.nsig; ++k) {  // neighbours' weights that count a flipped bit
           const uint32_t sg = qe.sig[k];
@@ -883,6 +915,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
   }
   for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
   if ((threadIdx.x & 31) == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+  agg.flush(colsize, nq);
 }
 
 // The same merge for lists of >= kBigList entries, one CTA per list: each
@@ -1008,6 +1041,9 @@ __global__ void __launch_bounds__(256) k_finish_big(
     uint32_t memo_mask, const uint32_t* __restrict__ big_list) {
   if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;
+  __shared__ int s_colagg[kColAggQ][kMaxQ];
+  ColAgg agg{s_colagg};
+  agg.init();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1018,8 +1054,9 @@ __global__ void __launch_bounds__(256) k_finish_big(
     const uint64_t* seg = skeys + s;
     const uint32_t x = uint32_t(seg[0] >> 32);
     finish_vertex(g, x, g.adj + g.off[x], g.deg[x], seg, e - s, svals + s, qenc, nq, rows, colsize, memo,
-                  memo_mask, lane);
+                  memo_mask, lane, agg);
   }
+  agg.flush(colsize, nq);
 }
 
 // Full encode (QueryEncodingState::initialize, src/matcher.cpp:10-18):
