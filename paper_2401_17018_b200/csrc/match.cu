@@ -515,6 +515,7 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
       if (mp > fl) fl = mp;
     }
     if (b < kFloorB && lane == 0) floor_l[b] = min(fl, ce);
+    __syncwarp();  // the floor is shared memory read by every lane of the next chunk (racecheck)
     if (ok && g.elab && hit) hit = __ldg(g.elab + xo + p) == lp.elab[b];
     ok = ok && hit;
   }
@@ -1294,6 +1295,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
         c_mask &= c_mask - 1;
         pf_pos = kNone;
         const uint32_t c = s_cand[w][l][k];
+        __syncwarp();  // every lane's reads of M[] for the previous candidate are done (racecheck)
         if (lane == 0) s_M[w][l] = c;
         tvalid &= ~P.inval[l];
         touched |= ((c_tmask >> k) & 1u) << l;
