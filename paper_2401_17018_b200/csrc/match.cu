@@ -900,7 +900,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
   __shared__ TailFactor s_tail[kWarpsPerBlock];
   // short backward lists staged per (warp, level) (setup_level); not in the
   // 4-CTA variants, whose shared memory budget is taken by occupancy
+#ifdef BDSM_NO_STAGE
+  constexpr bool kStage = false;
+#else
   constexpr bool kStage = kMinBlocks <= 3;
+#endif
   __shared__ uint32_t s_stage[kWarpsPerBlock][kStage ? kStageLevels : 1][kStage ? kStageMax : 1];
   __shared__ uint32_t s_stage_meta[kWarpsPerBlock][kStage ? kStageLevels : 1][4];
   __shared__ unsigned long long s_tcnt[kWarpsPerBlock][kMaxQ];  // cached tail-level counts
