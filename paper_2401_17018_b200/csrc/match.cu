@@ -345,29 +345,9 @@ struct LevelSetup {
   uint32_t drv_b, lo, hi, deg_sum;
 };
 
-// Shared-memory staging of one short "other" backward list per (warp, level):
-// the label sub-range of a non-hub backward list that is not the driver,
-// when it has at most kStageMax entries, is copied to shared memory at the
-// level's setup, and the candidates' membership tests in it become shared-
-// memory binary searches instead of chains of dependent global loads.  The
-// list's vertex usually sits at a shallower level than the driver's, so the
-// copy is reused by every setup of the level until that vertex changes (the
-// stage is keyed by vertex, start and length; the graph is immutable during a
-// launch).  Levels 2 .. 2 + kStageLevels - 1; not with edge labels.
-constexpr uint32_t kStageMax = 64;
-constexpr uint32_t kStageLevels = 4;
-struct Stage {
-  uint32_t* buf;   // kStageMax entries
-  uint32_t* meta;  // [0] vertex, [1] start, [2] length, [3] staged backward index (kNone: none this setup)
-};
-__device__ __forceinline__ Stage stage_at(uint32_t* base, uint32_t* meta, uint32_t l) {
-  if (!base || l < 2 || l >= 2 + kStageLevels) return Stage{nullptr, nullptr};
-  return Stage{base + (l - 2) * kStageMax, meta + (l - 2) * 4};
-}
 
 __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const DevGraph& g, const uint32_t* M,
-                                                  uint32_t lane, uint32_t* floor_l, uint32_t* ceil_l,
-                                                  Stage stg = Stage{nullptr, nullptr}) {
+                                                  uint32_t lane, uint32_t* floor_l, uint32_t* ceil_l) {
   const uint32_t nb = lp.nback;
   uint32_t myd = 0xffffffffu;
   uint64_t myo = 0;
@@ -377,12 +357,10 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   uint32_t ibnd = 0;
   if (g.loff && lp.lcls != kNone && lane < 2 * nb)
     ibnd = __ldg(g.loff + uint64_t(M[lp.back[lb_list]]) * (g.nlab + 1) + lp.lcls + (lane & 1));
-  bool hubx = false;
   if (lane < nb) {
     const uint32_t x = M[lp.back[lane]];
     myd = __ldg(g.deg + x);
     myo = __ldg(g.off + x);
-    if (stg.buf && g.hub_slot) hubx = __ldg(g.hub_slot + x) != kNone;
   }
   const uint32_t mn = __reduce_min_sync(kFull, myd);
   LevelSetup s;
@@ -405,29 +383,6 @@ __device__ __forceinline__ LevelSetup setup_level(const LevelProg& lp, const Dev
   s.lo = __shfl_sync(kFull, bnd, 2 * s.drv_b);
   s.hi = __shfl_sync(kFull, bnd, 2 * s.drv_b + 1);
   s.drv_off = __shfl_sync(kFull, myo, s.drv_b);
-  if (stg.buf) {
-    const bool cand = lane < nb && lane != s.drv_b && !hubx && c > f && c - f <= kStageMax;
-    const uint32_t cm = __ballot_sync(kFull, cand);
-    uint32_t sb = kNone;
-    if (cm) {
-      sb = __ffs(cm) - 1;
-      const uint32_t xs = M[lp.back[sb]];
-      const uint32_t fs = __shfl_sync(kFull, f, sb);
-      const uint32_t ns = __shfl_sync(kFull, c - f, sb);
-      const uint64_t os = __shfl_sync(kFull, myo, sb);
-      if (stg.meta[0] != xs || stg.meta[1] != fs || stg.meta[2] != ns) {
-        for (uint32_t i = lane; i < ns; i += 32) stg.buf[i] = __ldg(g.adj + os + fs + i);
-        __syncwarp();
-        if (lane == 0) {
-          stg.meta[0] = xs;
-          stg.meta[1] = fs;
-          stg.meta[2] = ns;
-        }
-      }
-    }
-    if (lane == 0) stg.meta[3] = sb;
-    __syncwarp();
-  }
   return s;
 }
 
@@ -442,7 +397,7 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
                                                  uint32_t cur, uint32_t end2, uint32_t dpos, uint32_t touched,
                                                  uint32_t anchor, uint32_t flag, uint32_t lane, uint32_t& c_out,
                                                  bool& tc_out, bool have_pf = false, uint32_t pf_c = 0,
-                                                 uint32_t pf_rw = 0, Stage stg = Stage{nullptr, nullptr}) {
+                                                 uint32_t pf_rw = 0) {
   const DevGraph& g = a.g;
   const uint32_t idx = cur + lane;
   bool ok = idx < end2;
@@ -469,23 +424,9 @@ __device__ __forceinline__ uint32_t filter_chunk(const PhaseArgs& a, const Level
     }
   }
   const uint32_t remain = end2 - cur;  // driver entries left in this range
-  const uint32_t staged = stg.meta ? stg.meta[3] : kNone;
   for (uint32_t b = 0; b < lp.nback; ++b) {  // other backward lists
     if (b == dpos) continue;
     if (!__any_sync(kFull, ok)) break;
-    if (b == staged) {  // shared-memory copy of this list's label sub-range
-      if (ok) {
-        const uint32_t n = stg.meta[2];
-        uint32_t lo = 0, hi = n;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (stg.buf[mid] < c) lo = mid + 1;
-          else hi = mid;
-        }
-        ok = lo < n && stg.buf[lo] == c;
-      }
-      continue;
-    }
     const uint32_t x = M[lp.back[b]];
     if (g.hub_slot && !g.elab) {  // hub list: one bitmap load instead of a search
       const uint32_t hs = __ldg(g.hub_slot + x);
@@ -785,8 +726,7 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
                                             uint32_t (*s_ceil)[kMaxQ][kFloorB], uint32_t touched, uint32_t anchor,
                                             uint32_t flag, uint32_t lane, TailFactor* out,
                                             unsigned long long* stat, unsigned long long* tcnt, uint32_t* tdeg,
-                                            uint32_t& tvalid, uint32_t task_id, uint32_t* stage_base = nullptr,
-                                            uint32_t* stage_meta = nullptr) {
+                                            uint32_t& tvalid, uint32_t task_id) {
   unsigned long long prod = 1, v = 1, b = 0, c = 0;
   for (uint32_t t = T + 1; t < P.n; ++t) {
     if ((P.leafmask >> t) & 1u) continue;  // leaves of T: weighted per level-T candidate
@@ -840,8 +780,7 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
       tvalid |= 1u << t;
     } else {
       const LevelProg& lp = P.lv[t];
-      const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t],
-                                        stage_at(stage_base, stage_meta, t));
+      const LevelSetup su = setup_level(lp, a.g, M, lane, s_floor[w][t], s_ceil[w][t]);
       __syncwarp();
 #ifdef BDSM_TRACE
       if (lane == 0) {
@@ -856,7 +795,7 @@ __device__ __forceinline__ void tail_factor(const PhaseArgs& a, const EdgeProg& 
         uint32_t cc;
         bool tc;
         cnt += __popc(filter_chunk(a, lp, M, s_floor[w][t], s_ceil[w][t], su.drv_off, cur, su.hi, su.drv_b, touched,
-                                   anchor, flag, lane, cc, tc, false, 0, 0, stage_at(stage_base, stage_meta, t)));
+                                   anchor, flag, lane, cc, tc));
 #ifdef BDSM_TRACE
         if (lane == 0) ++s_dbg[w][0];
 #endif
@@ -898,15 +837,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
   __shared__ uint32_t s_floor[kWarpsPerBlock][kMaxQ][kFloorB];
   __shared__ uint32_t s_ceil[kWarpsPerBlock][kMaxQ][kFloorB];
   __shared__ TailFactor s_tail[kWarpsPerBlock];
-  // short backward lists staged per (warp, level) (setup_level); not in the
-  // 4-CTA variants, whose shared memory budget is taken by occupancy
-#ifdef BDSM_NO_STAGE
-  constexpr bool kStage = false;
-#else
-  constexpr bool kStage = kMinBlocks <= 3;
-#endif
-  __shared__ uint32_t s_stage[kWarpsPerBlock][kStage ? kStageLevels : 1][kStage ? kStageMax : 1];
-  __shared__ uint32_t s_stage_meta[kWarpsPerBlock][kStage ? kStageLevels : 1][4];
   __shared__ unsigned long long s_tcnt[kWarpsPerBlock][kMaxQ];  // cached tail-level counts
   __shared__ uint32_t s_tdeg[kWarpsPerBlock][kMaxQ];
 #ifdef BDSM_TRACE
@@ -930,11 +860,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
   if (lane < 10) s_stat[w][lane] = 0;
-  if constexpr (kStage) {
-    if (lane < kStageLevels) s_stage_meta[w][lane][0] = kNone;
-  }
-  uint32_t* const stage_base = kStage && !a0.g.elab ? &s_stage[w][0][0] : nullptr;
-  uint32_t* const stage_meta = kStage ? &s_stage_meta[w][0][0] : nullptr;
   for (int k = 0; k < 4; ++k) s_lacc[w][lane][k] = 0;
   __syncwarp();
   uint32_t dtick = 0;
@@ -1084,8 +1009,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
     uint32_t c_cur, c_end, c_mask, c_drv, c_tmask;
     {
       c_tmask = __ballot_sync(kFull, lane < ncand && (__ldg(a.rows + s_cand[w][lstart][lane]) & flag));
-      const LevelSetup su = setup_level(P.lv[lstart], g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart],
-                                        stage_at(stage_base, stage_meta, lstart));
+      const LevelSetup su = setup_level(P.lv[lstart], g, s_M[w], lane, s_floor[w][lstart], s_ceil[w][lstart]);
       if (lane == 0) stat[4] += 4ull * su.deg_sum;
       c_off = su.drv_off;
       c_drv = su.drv_b;
@@ -1097,7 +1021,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
         c_mask = ncand == 32 ? kFull : ((1u << ncand) - 1);
       }
       if (lstart == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
-                                 s_tcnt[w], s_tdeg[w], tvalid, task_id, stage_base, stage_meta);
+                                 s_tcnt[w], s_tdeg[w], tvalid, task_id);
     }
     uint32_t l = lstart;
     while (true) {
@@ -1213,8 +1137,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
         cy0 = clock64();
 #endif
         const uint32_t m = filter_chunk(a, P.lv[l], s_M[w], s_floor[w][l], s_ceil[w][l], c_off, cur, c_end, c_drv,
-                                        touched, anchor, flag, lane, c, tc, pf_pos == cur, pf_c, pf_rw,
-                                        stage_at(stage_base, stage_meta, l));
+                                        touched, anchor, flag, lane, c, tc, pf_pos == cur, pf_c, pf_rw);
         pf_pos = kNone;
         // last DFS level: the next chunk's driver entries are loaded now, their
         // rows after this chunk's weights, so both round trips overlap the work
@@ -1318,8 +1241,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
 #ifdef BDSM_TRACE
         cy0 = clock64();
 #endif
-        const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l],
-                                          stage_at(stage_base, stage_meta, l));
+        const LevelSetup su = setup_level(P.lv[l], g, s_M[w], lane, s_floor[w][l], s_ceil[w][l]);
         if (lane == 0) {
           stat[2] += 4ull * su.deg_sum;
           stat[3] += 1;
@@ -1335,7 +1257,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
         c_drv = su.drv_b;
         c_tmask = 0;
         if (l == T) tail_factor(a, P, T, w, s_M[w], s_floor, s_ceil, touched, anchor, flag, lane, &s_tail[w], stat,
-                                 s_tcnt[w], s_tdeg[w], tvalid, task_id, stage_base, stage_meta);
+                                 s_tcnt[w], s_tdeg[w], tvalid, task_id);
 #ifdef BDSM_TRACE
         cy_setup += clock64() - cy0;
 #endif
