@@ -20,14 +20,16 @@ PY
 B=paper_2401_17018_b200/bdsm
 for mode in pipe nopipe; do
   extra=""; [ $mode = nopipe ] && extra="--no-pipeline"
-  /usr/bin/time -f "%e s wall" $B run --graph /tmp/cli_g.txt --gen-queries sparse,6,50 --gen-stream 0.01,mixed,10 \
+  t0=$(date +%s.%N)
+  $B run --graph /tmp/cli_g.txt --gen-queries sparse,6,50 --gen-stream 0.01,mixed,10 \
      --seed 7 --timeout 600 --out $O/$mode $extra > $O/$mode.out 2> $O/$mode.err
+  echo "$mode wall_s $(python -c "print(round($(date +%s.%N) - $t0, 2))")"
   python - $O/$mode <<'PY'
 import csv, sys
 rows = list(csv.DictReader(open(sys.argv[1] + "/stages.csv")))
 pre = sum(float(r["preprocess_s"]) for r in rows); mat = sum(float(r["match_s"]) for r in rows)
 print(sys.argv[1], "batches", len(rows), "preprocess_s %.4f match_s %.4f ratio %.3f" % (pre, mat, pre / (pre + mat)))
 PY
-  cat $O/$mode.out; tail -1 $O/$mode.err
+  cat $O/$mode.out; tail -2 $O/$mode.err
 done
 cmp $O/pipe/deltas.csv $O/nopipe/deltas.csv && echo "deltas identical"
