@@ -225,7 +225,7 @@ struct bdsm_engine {
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
   uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 3 / 4: force a matching-kernel variant
   // the variant of launches with many work items (4: 4 CTAs/SM, 64 registers; 3: 3 CTAs/SM, 80 registers)
-  uint32_t tune_variant_tp = env_u32("BDSM_TUNE_VARIANT_THROUGHPUT", 4);
+  uint32_t tune_variant_tp = env_u32("BDSM_TUNE_VARIANT_THROUGHPUT", 3);
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
   // batches of at least this many directed keys merge short lists one per
