@@ -228,9 +228,27 @@ struct bdsm_engine {
   uint32_t tune_variant_tp = env_u32("BDSM_TUNE_VARIANT_THROUGHPUT", 3);
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
-  // batches of at least this many directed keys merge short lists one per
-  // thread (k_merge_small); below it the warp kernel's latency is lower
-  uint32_t tune_small_min = env_u32("BDSM_TUNE_SMALLMIN", kSmallMergeMinKeys);
+  // short lists (<= tune_small_max entries before and after) of batches with at
+  // least tune_small_min directed keys get their own kernel: lanes per list
+  // tune_small_group below kSmallMergeMinKeys keys (latency-bound: a group of 8
+  // lanes per list, k_merge_group; C2 merge 0.085 -> 0.070 ms) and
+  // tune_small_group_large above (throughput-bound: a thread per list,
+  // k_merge_small, 32 lists in flight per warp; C4 merge 1.59 ms vs 1.92 ms
+  // with groups of 8)
+  uint32_t tune_small_min = env_u32("BDSM_TUNE_SMALLMIN", 1);
+  uint32_t tune_small_group = env_u32("BDSM_TUNE_SMALL_GROUP", 8);
+  uint32_t tune_small_group_large = env_u32("BDSM_TUNE_SMALL_GROUP_LARGE", 1);
+  uint32_t tune_small_max = env_u32("BDSM_TUNE_SMALLMAX", 256);
+  // shortest list merged by a whole CTA (k_merge_big), small / large batches
+  uint32_t tune_big_min = env_u32("BDSM_TUNE_BIGLIST", 1024);
+  uint32_t tune_big_min_large = env_u32("BDSM_TUNE_BIGLIST_LARGE", 1024);
+  bool large_batch(uint32_t m) const { return m >= kSmallMergeMinKeys; }
+  uint32_t small_group(uint32_t m) const { return large_batch(m) ? tune_small_group_large : tune_small_group; }
+  uint32_t small_max(uint32_t m) const {
+    if (m < tune_small_min) return 0;
+    return small_group(m) == 1 ? std::min<uint32_t>(tune_small_max, 256) : tune_small_max;
+  }
+  uint32_t big_min(uint32_t m) const { return large_batch(m) ? tune_big_min_large : tune_big_min; }
   uint32_t tune_self_scan = env_u32("BDSM_TUNE_SELFSCAN", kSelfScanUpdates);
   static uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = getenv(name);
@@ -1209,11 +1227,11 @@ struct bdsm_engine {
     CK(cudaEventRecord(m0, stream));
     const bool small_ok = m >= tune_small_min;
     launch_alloc(B().heads.p, B().skeys.p, B().ins_prefix.p, m, view(), opts.slack, B().d_st, B().new_off.p, B().new_cap.p, B().big_list.p,
-                 B().small_list.p, B().mid_list.p, small_ok, stream);
+                 B().small_list.p, B().mid_list.p, small_max(m), big_min(m), stream);
     launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p, B().new_cap.p, B().ipos.p,
                          d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st, memo.p,
-                         uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p, small_ok,
-                         num_sms, stream, fork_big());
+                         uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p,
+                         small_max(m) ? small_group(m) : 0u, num_sms, stream, fork_big());
     join_big();
     CK(cudaEventRecord(m1, stream));
     launches += small_ok ? 7 : 6;  // prepare, post_sort, alloc, merge_refresh, [merge_small,] merge_big, finish_big
@@ -1552,11 +1570,12 @@ struct bdsm_engine {
     const uint32_t m = uint32_t(2 * n);
     const bool small_ok = m >= tune_small_min;
     launch_alloc(B().heads.p, B().skeys.p, B().ins_prefix.p, m, view(), opts.slack, B().d_st, B().new_off.p,
-                 B().new_cap.p, B().big_list.p, B().small_list.p, B().mid_list.p, small_ok, stream);
+                 B().new_cap.p, B().big_list.p, B().small_list.p, B().mid_list.p, small_max(m), big_min(m),
+                 stream);
     launch_merge_refresh(B().heads.p, B().skeys.p, B().svals.p, B().ins_prefix.p, m, B().ups.p, g, B().new_off.p,
                          B().new_cap.p, B().ipos.p, d_qenc.p, uint32_t(queries.size()), d_rows.p, d_colsize.p, B().d_st,
                          memo.p, uint32_t(memo.n ? memo.n - 1 : 0), B().big_list.p, B().small_list.p, B().mid_list.p,
-                         small_ok, num_sms, stream, fork_big());
+                         small_max(m) ? small_group(m) : 0u, num_sms, stream, fork_big());
     join_big();
     launches += small_ok ? 5 : 4;
   }

@@ -74,14 +74,14 @@ void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
                   uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, uint32_t* mid_list,
-                  bool small_ok, cudaStream_t s);
+                  uint32_t small_max, uint32_t big_min, cudaStream_t s);
 void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
                           DevGraphMut g, const uint64_t* new_off, const uint32_t* new_cap,
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
                           uint32_t memo_mask, const uint32_t* big_list, const uint32_t* small_list,
-                          const uint32_t* mid_list, bool small_ok, int num_sms, cudaStream_t s,
+                          const uint32_t* mid_list, uint32_t small_mode, int num_sms, cudaStream_t s,
                           cudaStream_t s_big);
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s);
 void launch_column_sizes(const uint32_t* rows, uint32_t V, uint32_t n, uint64_t* out, cudaStream_t s);

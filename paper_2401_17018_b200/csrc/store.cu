@@ -365,7 +365,7 @@ __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, u
 __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
                         const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
                         BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
-                        uint32_t* small_list, uint32_t* mid_list, bool small_ok) {
+                        uint32_t* small_list, uint32_t* mid_list, uint32_t small_max, uint32_t big_min) {
   if (batch_aborted(st)) return;
   const uint32_t nt = st->n_touched;
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
@@ -382,8 +382,8 @@ __global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __re
       const uint32_t dold = g.deg[x];
       const uint32_t dnew = dold + nins - ndel;
       // the pre-batch list is long (k_merge_big) / both lists are short (k_merge_small)
-      big = dold >= kBigList ? kBigFlag : 0u;
-      small = small_ok && dold <= kSmallList && dnew <= kSmallList ? kSmallFlag : 0u;
+      big = dold >= big_min ? kBigFlag : 0u;
+      small = !big && dold <= small_max && dnew <= small_max ? kSmallFlag : 0u;
       if (dnew > g.cap[x] || (nins && ndel)) c = slack_cap(dnew, slack);  // overflow, or a mixed segment
     }
     const uint32_t bb = __ballot_sync(kFull, big != 0), bs = __ballot_sync(kFull, small != 0);
@@ -918,6 +918,240 @@ __global__ void __launch_bounds__(256) k_merge_small(
   agg.flush(colsize, nq);
 }
 
+// Lower bound of x in the sorted a[0, n) by a group of GS lanes (sub = lane
+// index within the group): each round the GS lanes test the last element of
+// GS equal blocks, so a list of <= GS^3 entries takes three dependent loads.
+template <uint32_t GS>
+__device__ __forceinline__ uint32_t group_lower_bound(const uint32_t* __restrict__ a, uint32_t n, uint32_t x,
+                                                      uint32_t sub, uint32_t gbase, uint32_t gmask) {
+  uint32_t lo = 0, len = n;
+  while (len > GS) {
+    const uint32_t stride = (len + GS - 1) / GS;
+    const uint32_t last = lo + (sub + 1) * stride - 1;
+    const bool lt = last < lo + len && a[last] < x;
+    const uint32_t c = __popc((__ballot_sync(gmask, lt) >> gbase) & ((GS == 32 ? 0u : 1u << GS) - 1u));
+    const uint32_t nlo = lo + c * stride;
+    len = min(stride, lo + len - nlo);
+    lo = nlo;
+  }
+  const bool lt = sub < len && a[lo + sub] < x;
+  return lo + __popc((__ballot_sync(gmask, lt) >> gbase) & ((GS == 32 ? 0u : 1u << GS) - 1u));
+}
+
+constexpr uint32_t kGroupMoveUnroll = 4;  // k_merge_group: old elements per lane in flight per step
+
+// Short lists (<= kSmallList entries before and after the batch; most touched
+// lists of the 1M-update batches) merged by a group of GS lanes each, so a warp
+// merges 32 / GS lists at once and every load and store of the moves is a
+// GS x 4-byte run (one 32-byte sector at GS = 8) instead of a 4-byte access per
+// lane to 32 different lists (k_merge_small: eight L2 sectors written per
+// sector of list data).  The steps are k_merge_refresh's (insert slots against
+// the intact old list, by GS-ary group searches; in place, left-movers ascend
+// and right-movers descend in steps that are read completely before they are
+// written), and the finish is finish_vertex's spread over the group: memo
+// invalidations and hub bits by key, the label index by class (staged in shared
+// memory), candidate rows by query.
+template <uint32_t GS>
+__global__ void __launch_bounds__(256) k_merge_group(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
+    const uint32_t* __restrict__ svals, const uint32_t* __restrict__ ins_prefix, uint32_t m,
+    const bdsm_update_dev* __restrict__ ups, DevGraphMut g, const uint64_t* __restrict__ new_off,
+    const uint32_t* __restrict__ new_cap, uint32_t* ipos, const DevQueryEnc* __restrict__ qenc, uint32_t nq,
+    uint32_t* const* rows, uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
+    uint32_t memo_mask, const uint32_t* __restrict__ small_list) {
+  if (batch_aborted(st)) return;
+  if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
+  __shared__ int s_colagg[kColAggQ][kMaxQ];
+  __shared__ uint32_t s_lpos[256 / GS][kMaxLabelIndex + 1];
+  ColAgg agg{s_colagg};
+  agg.init();
+  const uint32_t lane = threadIdx.x & 31, sub = lane % GS, gbase = lane - sub;
+  const uint32_t gmask = GS == 32 ? kFull : ((1u << GS) - 1u) << gbase;
+  uint32_t* lpos = s_lpos[threadIdx.x / GS];
+  const uint32_t ngroups = gridDim.x * (blockDim.x / GS);
+  const uint32_t nt = st->n_touched, nsmall = st->n_small;
+  uint64_t bytes = 0;
+  for (uint32_t si = (blockIdx.x * blockDim.x + threadIdx.x) / GS; si < nsmall; si += ngroups) {
+    const uint32_t t = small_list[si];
+    const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
+    const uint64_t* seg = skeys + s;
+    const uint32_t segn = e - s;
+    const uint32_t x = uint32_t(seg[0] >> 32);
+    const uint32_t dold = g.deg[x];
+    const uint64_t ooff = g.off[x];
+    const uint32_t nins = ins_prefix[e] - ins_prefix[s];
+    const uint32_t dnew = dold + nins - (segn - nins);
+    const uint32_t ncap = new_cap[t] & kCapMask;
+    const bool reloc = ncap != 0;
+    const uint64_t noff = new_off[t];
+    const uint32_t* src = g.adj + ooff;
+    uint32_t* dst = g.adj + noff;
+    const uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
+    uint32_t* edst = g.elab ? g.elab + noff : nullptr;
+
+    // 1. insert slots against the intact old list, and the first position that
+    // can move in place (entries below the first batch key never move)
+    uint32_t start = 0;
+    if (segn <= GS) {
+      for (uint32_t k = 0; k < segn; ++k) {
+        const bool del = svals[s + k] >> 31;
+        if (del && (k || reloc)) continue;
+        const uint32_t lb = group_lower_bound<GS>(src, dold, uint32_t(seg[k]), sub, gbase, gmask);
+        if (k == 0 && !reloc) start = lb;
+        if (!del && sub == 0) {
+          const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+          ipos[s + k] = ib + (lb - (k - ib));
+        }
+      }
+    } else {
+      if (sub == GS - 1 && !reloc && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
+      for (uint32_t k = sub; k < segn; k += GS) {
+        if (svals[s + k] >> 31) continue;
+        const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+        ipos[s + k] = ib + (lower_bound_u32(src, dold, uint32_t(seg[k])) - (k - ib));
+      }
+      start = __shfl_sync(gmask, start, gbase + GS - 1);
+    }
+    __syncwarp(gmask);
+    // 2. move the old elements
+    const bool ascending = reloc || nins == 0;
+    const uint32_t step = GS * kGroupMoveUnroll;
+    const uint32_t nsteps = dold > start ? (dold - start + step - 1) / step : 0;
+    for (uint32_t sj = 0; sj < nsteps; ++sj) {
+      const uint32_t base = start + (ascending ? sj : nsteps - 1 - sj) * step;
+      uint32_t a[kGroupMoveUnroll], p[kGroupMoveUnroll], el[kGroupMoveUnroll];
+      bool mv[kGroupMoveUnroll];
+#pragma unroll
+      for (uint32_t k = 0; k < kGroupMoveUnroll; ++k) {
+        const uint32_t i = base + k * GS + sub;
+        mv[k] = false;
+        el[k] = kNone;
+        a[k] = 0;
+        if (i < dold) {
+          a[k] = src[i];
+          if (esrc) el[k] = esrc[i];
+        }
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kGroupMoveUnroll; ++k) {
+        const uint32_t i = base + k * GS + sub;
+        p[k] = 0;
+        if (i < dold) {
+          bool dl;
+          merged_pos(seg, segn, ins_prefix, s, a[k], i, p[k], dl);
+          mv[k] = !dl && (reloc || p[k] != i);
+        }
+      }
+      __syncwarp(gmask);
+#pragma unroll
+      for (uint32_t k = 0; k < kGroupMoveUnroll; ++k)
+        if (mv[k]) {
+          dst[p[k]] = a[k];
+          if (edst) edst[p[k]] = el[k];
+        }
+      __syncwarp(gmask);
+    }
+    // 3. inserts
+    for (uint32_t k = sub; k < segn; k += GS) {
+      const uint32_t val = svals[s + k];
+      if (val >> 31) continue;
+      const uint32_t pp = ipos[s + k];
+      dst[pp] = uint32_t(seg[k]);
+      if (edst) edst[pp] = ups[val & 0x7fffffffu].elab;
+    }
+    __syncwarp(gmask);
+    if (sub == 0) {
+      g.deg[x] = dnew;
+      if (reloc) {
+        g.off[x] = noff;
+        g.cap[x] = ncap;
+      }
+      bytes += 4ull * (uint64_t(dold) + dnew);
+    }
+    // 4. finish (finish_vertex over the group)
+    for (uint32_t q = 0; q < nq; ++q)
+      for (uint32_t k = sub; k < qenc[q].nsig; k += GS)
+        memo_invalidate_v(g.memo_bits, memo, memo_mask, x, q, qenc[q].sig[k]);
+    if (g.hub_slot) {
+      const uint32_t hs = g.hub_slot[x];
+      if (hs != kNone) {
+        uint32_t* bm = g.bitmaps + uint64_t(hs) * g.bm_words;
+        for (uint32_t k = sub; k < segn; k += GS) {
+          const uint32_t y = uint32_t(seg[k]);
+          if (svals[s + k] >> 31) atomicAnd(bm + (y >> 5), ~(1u << (y & 31)));
+          else atomicOr(bm + (y >> 5), 1u << (y & 31));
+        }
+      }
+    }
+    // label index: class k's first position moves by the inserts minus the
+    // deletes below class_lo[k] (the segment is sorted)
+    const bool indexed = g.loff != nullptr;
+    if (indexed) {
+      uint32_t* lrow = g.loff + uint64_t(x) * (g.nlab + 1);
+      for (uint32_t k = sub; k <= g.nlab; k += GS) {
+        uint32_t v = dnew;
+        if (k < g.nlab) {
+          const uint32_t lo = g.class_lo[k];
+          int acc = 0;
+          for (uint32_t j = 0; j < segn && uint32_t(seg[j]) < lo; ++j) acc += (svals[s + j] >> 31) ? -1 : 1;
+          v = uint32_t(int(lrow[k]) + acc);
+        }
+        lrow[k] = v;
+        lpos[k] = v;
+      }
+      __syncwarp(gmask);
+    }
+    // candidate rows, one query per lane
+    const uint32_t vl = g.vlabel[x];
+    for (uint32_t q = sub; q < nq; q += GS) {
+      const DevQueryEnc& qe = qenc[q];
+      uint32_t row = 0;
+      bool any = false;
+      for (uint32_t u = 0; u < qe.n; ++u) any |= vl == qe.qlabel[u];
+      if (any) {
+        uint32_t cnt[kMaxQ];
+        for (uint32_t gi = 0; gi < qe.G; ++gi) {
+          uint32_t c = 0;
+          if (indexed) {
+            const uint32_t cls = qe.gcls[gi];
+            c = cls == kNone ? 0u : lpos[cls + 1] - lpos[cls];
+          } else {
+            for (uint32_t i = 0; i < dnew; ++i) c += dst[i] >= qe.glo[gi] && dst[i] < qe.ghi[gi];
+          }
+          cnt[gi] = c > qe.cap ? qe.cap : c;
+        }
+        for (uint32_t u = 0; u < qe.n; ++u) {
+          if (vl != qe.qlabel[u]) continue;
+          bool ok = true;
+          for (uint32_t gi = 0; gi < qe.G && ok; ++gi) ok = cnt[gi] >= qe.qcnt[u][gi];
+          if (ok) row |= 1u << u;
+        }
+      }
+      const uint32_t word = rows[q][x];
+      const uint32_t before = word & ~kRowFlags;
+      if (before != row) {
+        rows[q][x] = row | (word & kRowFlags);
+        const uint32_t diff = before ^ row;
+        uint32_t d = diff;
+        while (d) {
+          const uint32_t u = __ffs(d) - 1;
+          d &= d - 1;
+          agg.add(colsize, q, u, (row >> u) & 1u);
+        }
+        for (uint32_t k = 0; k < qe.nsig; ++k) {  // neighbours' weights that count a flipped bit
+          const uint32_t sg = qe.sig[k];
+          if ((diff >> (sg & 15)) & 1u)
+            for (uint32_t i = 0; i < dnew; ++i) memo_invalidate_v(g.memo_bits, memo, memo_mask, dst[i], q, sg);
+        }
+      }
+    }
+    __syncwarp(gmask);  // lpos is reused by the group's next list
+  }
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(kFull, bytes, o);
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd((unsigned long long*)&st->bytes_update, (unsigned long long)bytes);
+  agg.flush(colsize, nq);
+}
+
 // The same merge for lists of >= kBigList entries, one CTA per list: each
 // sweep step moves 256 threads x kMoveUnroll elements (read completely, then
 // written, with a CTA barrier between), so an 18K-neighbour hub moves in a
@@ -1269,9 +1503,11 @@ void launch_clear_flags(const uint64_t* skeys, uint32_t m, uint32_t* const* rows
 void launch_alloc(const uint32_t* heads, const uint64_t* skeys, const uint32_t* ins_prefix,
                   uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off,
                   uint32_t* new_cap, uint32_t* big_list, uint32_t* small_list, uint32_t* mid_list,
-                  bool small_ok, cudaStream_t s) {
+                  uint32_t small_max, uint32_t big_min, cudaStream_t s) {
+  // small_max: longest list (before and after) of the short-list kernel, 0 =
+  // none; k_merge_small's position array bounds it at kSmallList
   k_alloc<<<blocks_for(m), kThreads, 0, s>>>(heads, skeys, ins_prefix, m, g, slack, st, new_off, new_cap,
-                                             big_list, small_list, mid_list, small_ok);
+                                             big_list, small_list, mid_list, small_max, big_min ? big_min : kBigList);
 }
 void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const uint32_t* svals,
                           const uint32_t* ins_prefix, uint32_t m, const bdsm_update_dev* ups,
@@ -1279,7 +1515,7 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
                           uint32_t* ipos, const DevQueryEnc* qenc, uint32_t nq, uint32_t* const* rows,
                           uint64_t* const* colsize, BatchState* st, unsigned long long* memo,
                           uint32_t memo_mask, const uint32_t* big_list, const uint32_t* small_list,
-                          const uint32_t* mid_list, bool small_ok, int num_sms, cudaStream_t s,
+                          const uint32_t* mid_list, uint32_t small_mode, int num_sms, cudaStream_t s,
                           cudaStream_t s_big) {
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
@@ -1289,10 +1525,23 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask,
                                                   mid_list);
-  if (small_ok)
+  // short lists: small_mode 1 = a thread per list (k_merge_small), 8 / 16 = a
+  // group of that many lanes per list (k_merge_group), 0 = none (k_alloc did
+  // not split them off)
+  if (small_mode == 1)
     k_merge_small<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) + 255) / 256, uint64_t(num_sms) * 8)), 256,
                     0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
                             st, memo, memo_mask, small_list);
+  else if (small_mode == 8 || small_mode == 16) {
+    const unsigned gb = unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * small_mode + 255) / 256,
+                                                    uint64_t(num_sms) * 8));
+    if (small_mode == 8)
+      k_merge_group<8><<<gb, 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+                                          nq, rows, colsize, st, memo, memo_mask, small_list);
+    else
+      k_merge_group<16><<<gb, 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+                                           nq, rows, colsize, st, memo, memo_mask, small_list);
+  }
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
   // long lists (disjoint from the others; shared structures are updated with
   // atomics) on s_big, which the caller may run beside s

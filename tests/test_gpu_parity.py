@@ -259,18 +259,21 @@ def test_anchor_offset_scan_paths(monkeypatch, self_scan):
             e.close()
 
 
+@pytest.mark.parametrize("small_group", ["1", "8", "16"])
 @pytest.mark.parametrize("bitmap_mindeg", [None, "4"])
-def test_thread_merge_matches_reference(monkeypatch, bitmap_mindeg):
-    """Short lists (<= 256 entries) of large batches are merged one per thread
+def test_thread_merge_matches_reference(monkeypatch, bitmap_mindeg, small_group):
+    """Short lists (<= 256 entries) of large batches are merged one per lane
+    group (k_merge_group, 8 or 16 lanes per list) or one per thread
     (k_merge_small); the threshold is lowered so every golden batch takes
     that path: counts equal the reference's, and on a mixed random stream
     every neighbour list equals the expected one after each batch.  With
-    bitmaps forced onto small vertices the thread path's bitmap maintenance
-    is exercised too."""
+    bitmaps forced onto small vertices the short-list path's bitmap
+    maintenance is exercised too."""
     import os
     import sys
     import paper_2401_17018_b200 as bd
     monkeypatch.setenv("BDSM_TUNE_SMALLMIN", "1")
+    monkeypatch.setenv("BDSM_TUNE_SMALL_GROUP", small_group)
     if bitmap_mindeg:
         monkeypatch.setenv("BDSM_BITMAP_MINDEG", bitmap_mindeg)
     for suite in gu.SUITES:
