@@ -241,7 +241,7 @@ struct bdsm_engine {
   uint32_t tune_small_max = env_u32("BDSM_TUNE_SMALLMAX", 256);
   // shortest list merged by a whole CTA (k_merge_big), small / large batches
   uint32_t tune_big_min = env_u32("BDSM_TUNE_BIGLIST", 1024);
-  uint32_t tune_big_min_large = env_u32("BDSM_TUNE_BIGLIST_LARGE", 1024);
+  uint32_t tune_big_min_large = env_u32("BDSM_TUNE_BIGLIST_LARGE", 4096);  // C4: 4096 268.7M, 2048 265.7M, 1024 253.1M
   bool large_batch(uint32_t m) const { return m >= kSmallMergeMinKeys; }
   uint32_t small_group(uint32_t m) const { return large_batch(m) ? tune_small_group_large : tune_small_group; }
   uint32_t small_max(uint32_t m) const {

@@ -354,6 +354,9 @@ constexpr uint32_t kBigList = BDSM_BIG_LIST;  // lists this long are merged by a
 constexpr uint32_t kBigFlag = 0x80000000u;  // new_cap[t]: the list is merged by k_merge_big
 constexpr uint32_t kSmallList = BDSM_SMALL_LIST;  // lists up to this long (before and after): one thread each
 constexpr uint32_t kSmallFlag = 0x40000000u;  // new_cap[t]: the list is merged by k_merge_small
+// batch keys of a short list at most (k_merge_small keeps their positions in a
+// per-thread array; a list with more keys goes to k_merge_refresh)
+constexpr uint32_t kSmallKeys = 32;
 constexpr uint32_t kCapMask = 0x3fffffffu;
 
 __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, uint32_t nt, uint32_t m) {
@@ -361,68 +364,82 @@ __device__ __forceinline__ uint32_t seg_end(const uint32_t* heads, uint32_t t, u
 }
 
 // K3 (part 1): per touched vertex, new degree and relocation when the merged
-// list no longer fits its slack.
-__global__ void k_alloc(const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys,
-                        const uint32_t* __restrict__ ins_prefix, uint32_t m, DevGraph g, float slack,
-                        BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
-                        uint32_t* small_list, uint32_t* mid_list, uint32_t small_max, uint32_t big_min) {
+// list no longer fits its slack; the list goes to the kernel for its length.
+// List appends and pool allocations are aggregated per CTA (warp ballots and
+// scans into shared counters, then one global atomic per counter per CTA): a
+// 1M-update batch touches 2M lists, and per-warp atomics on the same five
+// counters serialise in L2.  In-place lists keep their offset, which the merge
+// kernels read themselves (new_off is only written for relocations).
+__global__ void __launch_bounds__(kThreads) k_alloc(
+    const uint32_t* __restrict__ heads, const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ ins_prefix,
+    uint32_t m, DevGraph g, float slack, BatchState* st, uint64_t* new_off, uint32_t* new_cap, uint32_t* big_list,
+    uint32_t* small_list, uint32_t* mid_list, uint32_t small_max, uint32_t big_min) {
   if (batch_aborted(st)) return;
+  __shared__ uint32_t s_cnt[3];  // mid, big, small lists of this CTA round
+  __shared__ unsigned long long s_pool, s_reloc;
+  __shared__ uint32_t s_base[3];
+  __shared__ unsigned long long s_pbase;
   const uint32_t nt = st->n_touched;
   const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-  // warp-uniform loop: list appends and pool allocations are aggregated per
-  // warp (one atomic each instead of one per list)
-  for (uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x - lane; t0 < nt; t0 += gridDim.x * blockDim.x) {
-    const uint32_t t = t0 + lane;
-    uint32_t big = 0, small = 0, c = 0, x = 0;
+  for (uint32_t c0 = blockIdx.x * blockDim.x; c0 < nt; c0 += gridDim.x * blockDim.x) {  // CTA-uniform
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_pool = s_reloc = 0;
+    __syncthreads();
+    const uint32_t t = c0 + threadIdx.x;
+    uint32_t big = 0, small = 0, c = 0;
     if (t < nt) {
       const uint32_t s = heads[t], e = seg_end(heads, t, nt, m);
-      x = uint32_t(skeys[s] >> 32);
+      const uint32_t x = uint32_t(skeys[s] >> 32);
       const uint32_t nins = ins_prefix[e] - ins_prefix[s];
       const uint32_t ndel = (e - s) - nins;
       const uint32_t dold = g.deg[x];
       const uint32_t dnew = dold + nins - ndel;
       // the pre-batch list is long (k_merge_big) / both lists are short (k_merge_small)
       big = dold >= big_min ? kBigFlag : 0u;
-      small = !big && dold <= small_max && dnew <= small_max ? kSmallFlag : 0u;
+      small = !big && dold <= small_max && dnew <= small_max && e - s <= kSmallKeys ? kSmallFlag : 0u;
       if (dnew > g.cap[x] || (nins && ndel)) c = slack_cap(dnew, slack);  // overflow, or a mixed segment
     }
-    const uint32_t bb = __ballot_sync(kFull, big != 0), bs = __ballot_sync(kFull, small != 0);
     const uint32_t bm = __ballot_sync(kFull, t < nt && !big && !small);
-    uint32_t base = 0;
-    if (bm) {
-      if (lane == 0) base = atomicAdd(&st->n_mid, __popc(bm));
-      base = __shfl_sync(kFull, base, 0);
-      if ((bm >> lane) & 1u) mid_list[base + __popc(bm & lt)] = t;
-    }
-    if (bb) {
-      if (lane == 0) base = atomicAdd(&st->n_big, __popc(bb));
-      base = __shfl_sync(kFull, base, 0);
-      if (big) big_list[base + __popc(bb & lt)] = t;
-    }
-    if (bs) {
-      if (lane == 0) base = atomicAdd(&st->n_small, __popc(bs));
-      base = __shfl_sync(kFull, base, 0);
-      if (small) small_list[base + __popc(bs & lt)] = t;
-    }
+    const uint32_t bb = __ballot_sync(kFull, big != 0), bs = __ballot_sync(kFull, small != 0);
     const uint32_t br = __ballot_sync(kFull, c != 0);
-    uint64_t at = 0;
-    if (br) {  // relocations: one pool allocation for the warp, carved by an inclusive scan
-      uint64_t inc = c;
+    // warp offsets within the CTA
+    uint32_t wo = 0;
+    if (lane < 3) {
+      const uint32_t b = lane == 0 ? bm : lane == 1 ? bb : bs;
+      if (b) wo = atomicAdd(&s_cnt[lane], __popc(b));
+    }
+    const uint32_t wo_mid = __shfl_sync(kFull, wo, 0), wo_big = __shfl_sync(kFull, wo, 1);
+    const uint32_t wo_small = __shfl_sync(kFull, wo, 2);
+    uint64_t inc = c, wpool = 0;
+    if (br) {  // relocations: the warp's slots carved by an inclusive scan
 #pragma unroll
       for (uint32_t o = 1; o < 32; o <<= 1) {
         const uint64_t v = __shfl_up_sync(kFull, inc, o);
         if (lane >= o) inc += v;
       }
       if (lane == 31) {
-        at = atomicAdd((unsigned long long*)&st->pool_top, (unsigned long long)inc);
-        atomicAdd((unsigned long long*)&st->relocations, (unsigned long long)__popc(br));
+        wpool = atomicAdd(&s_pool, (unsigned long long)inc);
+        atomicAdd(&s_reloc, (unsigned long long)__popc(br));
       }
-      at = __shfl_sync(kFull, at, 31) + inc - c;
+      wpool = __shfl_sync(kFull, wpool, 31);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_base[0] = s_cnt[0] ? atomicAdd(&st->n_mid, s_cnt[0]) : 0u;
+      s_base[1] = s_cnt[1] ? atomicAdd(&st->n_big, s_cnt[1]) : 0u;
+      s_base[2] = s_cnt[2] ? atomicAdd(&st->n_small, s_cnt[2]) : 0u;
+      s_pbase = s_pool ? atomicAdd((unsigned long long*)&st->pool_top, s_pool) : 0ull;
+      if (s_reloc) atomicAdd((unsigned long long*)&st->relocations, s_reloc);
+    }
+    __syncthreads();
+    if ((bm >> lane) & 1u) mid_list[s_base[0] + wo_mid + __popc(bm & lt)] = t;
+    if (big) big_list[s_base[1] + wo_big + __popc(bb & lt)] = t;
+    if (small) small_list[s_base[2] + wo_small + __popc(bs & lt)] = t;
     if (t < nt) {
-      new_off[t] = c ? at : g.off[x];
+      if (c) new_off[t] = s_pbase + wpool + inc - c;
       new_cap[t] = c | big | small;  // capacity 0: in place
     }
+    __syncthreads();  // the shared counters are reset for the next round
   }
 }
 
@@ -479,19 +496,29 @@ __device__ __forceinline__ uint32_t row_of(const DevQueryEnc& qe, uint32_t vl, u
 constexpr uint32_t kColAggQ = 2;
 struct ColAgg {
   int (*s)[kMaxQ];  // [kColAggQ][kMaxQ] shared accumulators
+  uint32_t* done;   // shared: warps of the CTA that have finished
   __device__ __forceinline__ void init() {
     for (uint32_t i = threadIdx.x; i < kColAggQ * kMaxQ; i += blockDim.x) s[i / kMaxQ][i % kMaxQ] = 0;
+    if (threadIdx.x == 0) *done = 0;
     __syncthreads();
   }
   __device__ __forceinline__ void add(uint64_t* const* colsize, uint32_t q, uint32_t u, bool up) {
     if (q < kColAggQ) atomicAdd(&s[q][u], up ? 1 : -1);
     else atomicAdd((unsigned long long*)(colsize[q] + u), up ? 1ull : (unsigned long long)(-1ll));
   }
+  // Warp-collective, once per warp at its end: the CTA's last warp to finish
+  // adds the sums, so finished warps exit instead of waiting at a barrier for
+  // the CTA's slowest list.
   __device__ __forceinline__ void flush(uint64_t* const* colsize, uint32_t nq) {
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < kColAggQ * kMaxQ; i += blockDim.x) {
+    __threadfence_block();
+    __syncwarp();
+    uint32_t last = 0;
+    if ((threadIdx.x & 31) == 0) last = atomicAdd(done, 1u) == (blockDim.x >> 5) - 1u;
+    if (!__shfl_sync(kFull, last, 0)) return;
+    __threadfence_block();
+    for (uint32_t i = threadIdx.x & 31; i < kColAggQ * kMaxQ; i += 32) {
       const uint32_t q = i / kMaxQ, u = i % kMaxQ;
-      const int v = s[q][u];
+      const int v = atomicAdd(&s[q][u], 0);
       if (q < nq && v) atomicAdd((unsigned long long*)(colsize[q] + u), (unsigned long long)(long long)v);
     }
   }
@@ -611,7 +638,8 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     return;
   }
   __shared__ int s_colagg[kColAggQ][kMaxQ];
-  ColAgg agg{s_colagg};
+  __shared__ uint32_t s_agg_done;
+  ColAgg agg{s_colagg, &s_agg_done};
   agg.init();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -630,7 +658,7 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     const uint32_t dnew = dold + nins - (segn - nins);
     const uint32_t ncap = new_cap[t] & kCapMask;
     const bool reloc = ncap != 0;
-    const uint64_t noff = new_off[t];
+    const uint64_t noff = reloc ? new_off[t] : ooff;
     uint32_t* src = g.adj + ooff;
     uint32_t* dst = g.adj + noff;
     uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
@@ -724,6 +752,74 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
   agg.flush(colsize, nq);
 }
 
+// k_merge_small's run copies: full blocks of 8 entries without predicates (8
+// loads in flight, then 8 stores), the remainder predicated; kLab: the graph
+// has edge labels, moved alongside.
+template <bool kLab>
+__device__ __forceinline__ void run_up(const uint32_t* src, uint32_t* dst, const uint32_t* esrc, uint32_t* edst,
+                                       uint32_t from, uint32_t to, uint32_t len) {
+  uint32_t b = 0;
+  for (; b + 8 <= len; b += 8) {
+    uint32_t v[8], l[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      v[k] = src[from + b + k];
+      if (kLab) l[k] = esrc[from + b + k];
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      dst[to + b + k] = v[k];
+      if (kLab) edst[to + b + k] = l[k];
+    }
+  }
+  if (b < len) {
+    uint32_t v[8], l[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      v[k] = b + k < len ? src[from + b + k] : 0u;
+      if (kLab) l[k] = b + k < len ? esrc[from + b + k] : 0u;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k)
+      if (b + k < len) {
+        dst[to + b + k] = v[k];
+        if (kLab) edst[to + b + k] = l[k];
+      }
+  }
+}
+template <bool kLab>
+__device__ __forceinline__ void run_down(const uint32_t* src, uint32_t* dst, const uint32_t* esrc, uint32_t* edst,
+                                         uint32_t from, uint32_t to, uint32_t len) {
+  uint32_t b = len;
+  for (; b >= 8; b -= 8) {
+    uint32_t v[8], l[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      v[k] = src[from + b - 8 + k];
+      if (kLab) l[k] = esrc[from + b - 8 + k];
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      dst[to + b - 8 + k] = v[k];
+      if (kLab) edst[to + b - 8 + k] = l[k];
+    }
+  }
+  if (b) {
+    uint32_t v[8], l[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      v[k] = k < b ? src[from + k] : 0u;
+      if (kLab) l[k] = k < b ? esrc[from + k] : 0u;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k)
+      if (k < b) {
+        dst[to + k] = v[k];
+        if (kLab) edst[to + k] = l[k];
+      }
+  }
+}
+
 // Short lists (<= kSmallList entries before and after the batch; most touched
 // lists at the C2-C4 shapes) are merged by ONE thread each, so a warp merges
 // 32 of them at once instead of one.  The batch keys' positions in the old
@@ -744,7 +840,8 @@ __global__ void __launch_bounds__(256) k_merge_small(
   if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   __shared__ int s_colagg[kColAggQ][kMaxQ];
-  ColAgg agg{s_colagg};
+  __shared__ uint32_t s_agg_done;
+  ColAgg agg{s_colagg, &s_agg_done};
   agg.init();
   const uint32_t nt = st->n_touched, nsmall = st->n_small;
   uint64_t bytes = 0;
@@ -760,51 +857,25 @@ __global__ void __launch_bounds__(256) k_merge_small(
     const uint32_t dnew = dold + nins - (segn - nins);
     const uint32_t ncap = new_cap[t] & kCapMask;
     const bool reloc = ncap != 0;
-    const uint64_t noff = new_off[t];
+    const uint64_t noff = reloc ? new_off[t] : ooff;
     const uint32_t* src = g.adj + ooff;
     uint32_t* dst = g.adj + noff;
     const uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
     uint32_t* edst = g.elab ? g.elab + noff : nullptr;
     auto ins_label = [&](uint32_t k) { return ups[svals[s + k] & 0x7fffffffu].elab; };
     // where each batch key falls in the old list (independent searches)
-    uint32_t ypos[2 * kSmallList];
+    uint32_t ypos[kSmallKeys];
     for (uint32_t k = 0; k < segn; ++k) ypos[k] = lower_bound_u32(src, dold, uint32_t(seg[k]));
     // copy a run of old entries, 8 loads in flight; in place the runs move
     // left in ascending order or right in descending order, and a block is
     // read completely before it is written, so overlapping runs are safe
     auto copy_up = [&](uint32_t from, uint32_t to, uint32_t len) {
-      for (uint32_t b = 0; b < len; b += 8) {
-        uint32_t v[8], l[8];
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-          v[k] = b + k < len ? src[from + b + k] : 0u;
-          l[k] = esrc && b + k < len ? esrc[from + b + k] : 0u;
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
-          if (b + k < len) {
-            dst[to + b + k] = v[k];
-            if (edst) edst[to + b + k] = l[k];
-          }
-      }
+      if (esrc) run_up<true>(src, dst, esrc, edst, from, to, len);
+      else run_up<false>(src, dst, nullptr, nullptr, from, to, len);
     };
     auto copy_down = [&](uint32_t from, uint32_t to, uint32_t len) {
-      for (uint32_t b = len; b > 0;) {
-        const uint32_t nb = b < 8 ? b : 8;
-        b -= nb;
-        uint32_t v[8], l[8];
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-          v[k] = k < nb ? src[from + b + k] : 0u;
-          l[k] = esrc && k < nb ? esrc[from + b + k] : 0u;
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
-          if (k < nb) {
-            dst[to + b + k] = v[k];
-            if (edst) edst[to + b + k] = l[k];
-          }
-      }
+      if (esrc) run_down<true>(src, dst, esrc, edst, from, to, len);
+      else run_down<false>(src, dst, nullptr, nullptr, from, to, len);
     };
     if (reloc || nins == 0) {  // ascending: out of place, or delete-only in place (moves left)
       // in place the entries below the first batch key do not move
@@ -962,8 +1033,9 @@ __global__ void __launch_bounds__(256) k_merge_group(
   if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;  // k_merge_refresh flags the overflow
   __shared__ int s_colagg[kColAggQ][kMaxQ];
+  __shared__ uint32_t s_agg_done;
   __shared__ uint32_t s_lpos[256 / GS][kMaxLabelIndex + 1];
-  ColAgg agg{s_colagg};
+  ColAgg agg{s_colagg, &s_agg_done};
   agg.init();
   const uint32_t lane = threadIdx.x & 31, sub = lane % GS, gbase = lane - sub;
   const uint32_t gmask = GS == 32 ? kFull : ((1u << GS) - 1u) << gbase;
@@ -983,7 +1055,7 @@ __global__ void __launch_bounds__(256) k_merge_group(
     const uint32_t dnew = dold + nins - (segn - nins);
     const uint32_t ncap = new_cap[t] & kCapMask;
     const bool reloc = ncap != 0;
-    const uint64_t noff = new_off[t];
+    const uint64_t noff = reloc ? new_off[t] : ooff;
     const uint32_t* src = g.adj + ooff;
     uint32_t* dst = g.adj + noff;
     const uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
@@ -1182,7 +1254,7 @@ __global__ void __launch_bounds__(256) k_merge_big(
     const uint32_t nins = ins_prefix[e] - ins_prefix[s];
     const uint32_t dnew = dold + nins - (segn - nins);
     const bool reloc = ncap != 0;
-    const uint64_t noff = new_off[t];
+    const uint64_t noff = reloc ? new_off[t] : ooff;
     uint32_t* src = g.adj + ooff;
     uint32_t* dst = g.adj + noff;
     uint32_t* esrc = g.elab ? g.elab + ooff : nullptr;
@@ -1276,7 +1348,8 @@ __global__ void __launch_bounds__(256) k_finish_big(
   if (batch_aborted(st)) return;
   if (st->pool_top > g.pool_size) return;
   __shared__ int s_colagg[kColAggQ][kMaxQ];
-  ColAgg agg{s_colagg};
+  __shared__ uint32_t s_agg_done;
+  ColAgg agg{s_colagg, &s_agg_done};
   agg.init();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

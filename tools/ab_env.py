@@ -68,7 +68,7 @@ def main() -> int:
                                            [len(wl.batches[i]) for i in range(args.warmup, nb)])
                 counts = [(r.positive[0], r.negative[0]) for r in list(warm) + list(rs)]
                 ms = sum(r.stats["ms_device"] for r in rs) / len(rs)
-                merge = [r.stats.get("ms_merge") for r in rs]
+                merge = [round(r.stats.get("ms_merge_kernel", 0), 3) for r in rs]
                 e.close()
             finally:
                 for k, old in saved.items():
