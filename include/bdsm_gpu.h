@@ -254,6 +254,40 @@ BDSM_API int64_t bdsm_engine_matches(bdsm_engine* engine, int query, int phase, 
  * of the last batch (zeros otherwise).  Returns the number of words. */
 BDSM_API size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size_t cap);
 
+/* Multi-device engine group (SURVEY.md §8(e) in one process; the devices[]
+ * option of §8(b)).  One engine per listed device (a device may repeat), each
+ * holding a replica of the graph and applying every batch to it, and counting
+ * only its share (shard r of n) of the canonical cost-balanced work-unit order;
+ * a batch's counts are the sums over the engines.  The reference has no
+ * multi-device mode; every call keeps the semantics of the engine call it is
+ * named after (same counts, errors, all-or-nothing contract).  bdsm_options'
+ * device / shard fields are set per engine.  Stats: times of the slowest engine,
+ * work counters summed.  A query whose deadline fires on any device reports 0/0
+ * for that batch.  apply_stream takes host batches only. */
+typedef struct bdsm_group bdsm_group;
+BDSM_API bdsm_status bdsm_group_create(const bdsm_graph_desc* graph, const bdsm_options* opts,
+                                       const int32_t* devices, uint32_t num_devices, bdsm_group** out);
+BDSM_API void bdsm_group_destroy(bdsm_group* group);
+BDSM_API uint32_t bdsm_group_size(bdsm_group* group);
+/* Engine r of the group (introspection: neighbours, rows, column sizes). */
+BDSM_API bdsm_engine* bdsm_group_engine(bdsm_group* group, uint32_t r);
+BDSM_API int bdsm_group_add_query(bdsm_group* group, const bdsm_query_desc* query);
+BDSM_API bdsm_status bdsm_group_apply_batch(bdsm_group* group, const bdsm_update* updates, size_t n,
+                                            uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats);
+BDSM_API bdsm_status bdsm_group_submit_batch(bdsm_group* group, const bdsm_update* updates, size_t n);
+BDSM_API bdsm_status bdsm_group_wait(bdsm_group* group, uint64_t* pos, uint64_t* neg, bdsm_batch_stats* stats);
+BDSM_API bdsm_status bdsm_group_apply_stream(bdsm_group* group, const bdsm_update* const* batches,
+                                             const size_t* sizes, size_t k, uint64_t* pos, uint64_t* neg,
+                                             bdsm_batch_stats* stats, size_t* done);
+BDSM_API size_t bdsm_group_last_batch_errors(bdsm_group* group, bdsm_update_error* out, size_t cap);
+BDSM_API bdsm_status bdsm_group_set_deadline(bdsm_group* group, int query, double seconds_from_now);
+BDSM_API bdsm_status bdsm_group_set_query_active(bdsm_group* group, int query, int active);
+BDSM_API int bdsm_group_query_timed_out(bdsm_group* group, int query);
+BDSM_API bdsm_status bdsm_group_replan(bdsm_group* group, int query);
+/* Matches of the last batch over all engines, merged into one sorted list. */
+BDSM_API bdsm_status bdsm_group_collect_matches(bdsm_group* group, uint64_t cap);
+BDSM_API int64_t bdsm_group_matches(bdsm_group* group, int query, int phase, uint32_t* out, size_t cap);
+
 BDSM_API const char* bdsm_version(void);
 
 #ifdef __cplusplus

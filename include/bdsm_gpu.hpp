@@ -75,7 +75,11 @@ class Engine {
  public:
   // LabeledGraph::build_from_edges semantics: vertex ids dense, 0-based, unique
   // (src/graph.cpp:38-46); edge errors are reported by the engine.
-  Engine(const std::vector<VertexRecord>& vs, const std::vector<EdgeRecord>& es, bdsm_options opts = defaults()) {
+  // devices: more than one entry builds a multi-device group (bdsm_group_*,
+  // a replica per device, work units split over them); the calls below keep
+  // their meaning.
+  Engine(const std::vector<VertexRecord>& vs, const std::vector<EdgeRecord>& es, bdsm_options opts = defaults(),
+         const std::vector<std::int32_t>& devices = {}) {
     std::vector<std::uint32_t> labels(vs.size(), 0xffffffffu);
     std::vector<bool> seen(vs.size(), false);
     for (const auto& r : vs) {
@@ -95,11 +99,20 @@ class Engine {
     }
     bdsm_graph_desc g{std::uint32_t(vs.size()), labels.data(), es.size(), src.data(), dst.data(),
                       any_label ? el.data() : nullptr};
-    check(bdsm_engine_create(&g, &opts, &e_));
+    if (devices.size() > 1) {
+      check(bdsm_group_create(&g, &opts, devices.data(), std::uint32_t(devices.size()), &g_));
+      e_ = bdsm_group_engine(g_, 0);
+    } else {
+      if (devices.size() == 1) opts.device = devices[0];
+      check(bdsm_engine_create(&g, &opts, &e_));
+    }
   }
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
-  ~Engine() { bdsm_engine_destroy(e_); }
+  ~Engine() {
+    if (g_) bdsm_group_destroy(g_);
+    else bdsm_engine_destroy(e_);
+  }
 
   static bdsm_options defaults() {
     bdsm_options o{};
@@ -121,7 +134,7 @@ class Engine {
     }
     bdsm_query_desc d{std::uint32_t(labels.size()), labels.data(), std::uint32_t(edges.size()), a.data(), b.data(),
                       any_label ? l.data() : nullptr};
-    int r = bdsm_engine_add_query(e_, &d);
+    int r = g_ ? bdsm_group_add_query(g_, &d) : bdsm_engine_add_query(e_, &d);
     if (r < 0) check(bdsm_status(-r));
     ++nq_;
     return r;
@@ -131,7 +144,8 @@ class Engine {
   std::vector<Counts> match_batch(const std::vector<EdgeUpdate>& batch, bdsm_batch_stats* stats = nullptr) {
     const std::vector<bdsm_update> ups = pack(batch);
     std::vector<std::uint64_t> pos(nq_), neg(nq_);
-    check(bdsm_engine_apply_batch(e_, ups.data(), ups.size(), pos.data(), neg.data(), stats));
+    check(g_ ? bdsm_group_apply_batch(g_, ups.data(), ups.size(), pos.data(), neg.data(), stats)
+             : bdsm_engine_apply_batch(e_, ups.data(), ups.size(), pos.data(), neg.data(), stats));
     return counts(pos, neg);
   }
 
@@ -141,26 +155,31 @@ class Engine {
   // the same with a batch already packed (so the caller can pack batch i+1
   // while batch i runs)
   void submit_packed(const std::vector<bdsm_update>& ups) {
-    check(bdsm_engine_submit_batch(e_, ups.data(), ups.size()));
+    check(g_ ? bdsm_group_submit_batch(g_, ups.data(), ups.size())
+             : bdsm_engine_submit_batch(e_, ups.data(), ups.size()));
   }
   std::vector<Counts> wait(bdsm_batch_stats* stats = nullptr) {
     std::vector<std::uint64_t> pos(nq_), neg(nq_);
-    check(bdsm_engine_wait(e_, pos.data(), neg.data(), stats));
+    check(g_ ? bdsm_group_wait(g_, pos.data(), neg.data(), stats) : bdsm_engine_wait(e_, pos.data(), neg.data(), stats));
     return counts(pos, neg);
   }
 
   void set_deadline(int query, double seconds_from_now) {
-    check(bdsm_engine_set_deadline(e_, query, seconds_from_now));
+    check(g_ ? bdsm_group_set_deadline(g_, query, seconds_from_now)
+             : bdsm_engine_set_deadline(e_, query, seconds_from_now));
   }
   // run_pipeline drops an unsolved query from later batches (src/bench.cpp:420-432)
-  void set_query_active(int query, bool active) { check(bdsm_engine_set_query_active(e_, query, active ? 1 : 0)); }
+  void set_query_active(int query, bool active) {
+    check(g_ ? bdsm_group_set_query_active(g_, query, active ? 1 : 0)
+             : bdsm_engine_set_query_active(e_, query, active ? 1 : 0));
+  }
   // MatchStats::timed_out of `query` in the last batch (its counts were dropped)
   bool query_timed_out(int query) {
-    const int r = bdsm_engine_query_timed_out(e_, query);
+    const int r = g_ ? bdsm_group_query_timed_out(g_, query) : bdsm_engine_query_timed_out(e_, query);
     if (r < 0) check(bdsm_status(-r));
     return r != 0;
   }
-  void replan(int query) { check(bdsm_engine_replan(e_, query)); }
+  void replan(int query) { check(g_ ? bdsm_group_replan(g_, query) : bdsm_engine_replan(e_, query)); }
   std::vector<std::uint64_t> column_sizes(int query, std::uint32_t n) {
     std::vector<std::uint64_t> out(32);
     check(bdsm_engine_column_sizes(e_, query, out.data()));
@@ -169,20 +188,23 @@ class Engine {
   }
   // Bounded match materialisation for later batches (0: counts only).
   void collect_matches(std::uint64_t cap) {
-    check(bdsm_engine_collect_matches(e_, cap));
+    check(g_ ? bdsm_group_collect_matches(g_, cap) : bdsm_engine_collect_matches(e_, cap));
     collect_cap_ = cap;
   }
   // Matches of the last batch for (query, phase 0 negative / 1 positive),
   // flattened num_vertices words each, sorted; throws std::length_error when
   // more matches exist than the engine collected (raise the cap).
   std::vector<std::uint32_t> matches(int query, int phase, std::uint32_t num_vertices) {
-    std::int64_t total = bdsm_engine_matches(e_, query, phase, nullptr, 0);
+    auto fetch = [&](std::uint32_t* out, std::size_t cap) {
+      return g_ ? bdsm_group_matches(g_, query, phase, out, cap) : bdsm_engine_matches(e_, query, phase, out, cap);
+    };
+    std::int64_t total = fetch(nullptr, 0);
     if (total < 0) check(bdsm_status(-total));
     if (std::uint64_t(total) > collect_cap_)
       throw std::length_error(std::to_string(total) + " matches, only " + std::to_string(collect_cap_) +
                               " collected (raise the collect_matches cap)");
     std::vector<std::uint32_t> out(std::size_t(total) * num_vertices);
-    std::int64_t again = bdsm_engine_matches(e_, query, phase, out.data(), std::size_t(total));
+    std::int64_t again = fetch(out.data(), std::size_t(total));
     if (again < 0) check(bdsm_status(-again));
     return out;
   }
@@ -220,7 +242,8 @@ class Engine {
     if (s == BDSM_OUT_OF_MEMORY) throw std::bad_alloc();
     throw std::runtime_error(msg);
   }
-  bdsm_engine* e_ = nullptr;
+  bdsm_engine* e_ = nullptr;  // the engine, or the group's engine 0 (introspection)
+  bdsm_group* g_ = nullptr;
   std::size_t nq_ = 0;
   std::uint64_t collect_cap_ = 0;
 };

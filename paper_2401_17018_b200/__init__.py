@@ -140,6 +140,34 @@ def _load():
     L.bdsm_plan_edge_orbits.argtypes = [C.c_void_p, C.c_void_p]
     L.bdsm_version.restype = C.c_char_p
     L.bdsm_version.argtypes = []
+    # multi-device engine group (bdsm_group_*)
+    L.bdsm_group_create.restype = C.c_int
+    L.bdsm_group_create.argtypes = [C.POINTER(_GraphDesc), C.POINTER(_Options), C.c_void_p, C.c_uint32,
+                                    C.POINTER(C.c_void_p)]
+    L.bdsm_group_destroy.restype = None
+    L.bdsm_group_destroy.argtypes = [C.c_void_p]
+    L.bdsm_group_size.restype = C.c_uint32
+    L.bdsm_group_size.argtypes = [C.c_void_p]
+    L.bdsm_group_engine.restype = C.c_void_p
+    L.bdsm_group_engine.argtypes = [C.c_void_p, C.c_uint32]
+    L.bdsm_group_add_query.restype = C.c_int
+    L.bdsm_group_add_query.argtypes = [C.c_void_p, C.POINTER(_QueryDesc)]
+    L.bdsm_group_apply_batch.restype = C.c_int
+    L.bdsm_group_apply_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                         C.POINTER(_Stats)]
+    L.bdsm_group_submit_batch.restype = C.c_int
+    L.bdsm_group_submit_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.bdsm_group_wait.restype = C.c_int
+    L.bdsm_group_wait.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
+    L.bdsm_group_apply_stream.restype = C.c_int
+    L.bdsm_group_apply_stream.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
+    L.bdsm_group_set_query_active.restype = C.c_int
+    L.bdsm_group_set_query_active.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.bdsm_group_collect_matches.restype = C.c_int
+    L.bdsm_group_collect_matches.argtypes = [C.c_void_p, C.c_uint64]
+    L.bdsm_group_matches.restype = C.c_int64
+    L.bdsm_group_matches.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]
     _lib = L
     return L
 
@@ -442,6 +470,131 @@ class Engine:
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().bdsm_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class EngineGroup:
+    """One engine per device in `devices` (a device may repeat), each holding a
+    replica of the graph and counting its share of the work units
+    (bdsm_group_*, SURVEY.md §8(e) in one process); counts are the sums over
+    the engines and equal one Engine's."""
+
+    def __init__(self, vertex_labels, src, dst, edge_labels=None, *, devices: Sequence[int] = (0,),
+                 group_bits: int = 2, slack: float = 0.25, pool_reserve: float = 0.5, chunk: int = 32,
+                 coalesce: bool = False):
+        L = lib()
+        self._vl = _u32(vertex_labels)
+        s, d = _u32(src), _u32(dst)
+        el = None if edge_labels is None else _u32(edge_labels)
+        desc = _GraphDesc(len(self._vl), self._vl.ctypes.data, len(s), s.ctypes.data, d.ctypes.data,
+                          None if el is None else el.ctypes.data)
+        opts = _Options(group_bits, 1 if coalesce else 0, 0, 0, 1, slack, pool_reserve, chunk, 0, 0)
+        devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+        h = C.c_void_p()
+        st = L.bdsm_group_create(C.byref(desc), C.byref(opts), devs.ctypes.data, len(devs), C.byref(h))
+        if st != 0:
+            _raise(st)
+        self._h = h
+        self.nq = 0
+        self.query_sizes: List[int] = []
+
+    def _e0(self):
+        return lib().bdsm_group_engine(self._h, 0)
+
+    @property
+    def size(self) -> int:
+        return int(lib().bdsm_group_size(self._h))
+
+    def add_query(self, labels: Sequence[int], edges: Iterable[Tuple]) -> int:
+        ql = _u32(labels)
+        edges = list(edges)
+        qa = _u32([e[0] for e in edges])
+        qb = _u32([e[1] for e in edges])
+        qlab = _u32([NO_LABEL if (len(e) < 3 or e[2] is None or e[2] < 0) else e[2] for e in edges])
+        desc = _QueryDesc(len(ql), ql.ctypes.data, len(qa), qa.ctypes.data if len(qa) else None,
+                          qb.ctypes.data if len(qb) else None, qlab.ctypes.data if len(qlab) else None)
+        r = lib().bdsm_group_add_query(self._h, C.byref(desc))
+        if r < 0:
+            _raise(-r)
+        self.nq += 1
+        self.query_sizes.append(len(ql))
+        return r
+
+    def match_batch(self, updates) -> BatchResult:
+        ups = make_updates(updates)
+        pos = np.zeros(max(self.nq, 1), np.uint64)
+        neg = np.zeros(max(self.nq, 1), np.uint64)
+        st = _Stats()
+        r = lib().bdsm_group_apply_batch(self._h, _ptr(ups) if len(ups) else None, len(ups), _ptr(pos), _ptr(neg),
+                                         C.byref(st))
+        if r != 0:
+            _raise(r, self._e0())
+        return BatchResult(pos[: self.nq].tolist(), neg[: self.nq].tolist(), _stats_dict(st))
+
+    def match_stream(self, batches) -> List[BatchResult]:
+        ups = [make_updates(b) for b in batches]
+        k, nq = len(ups), max(self.nq, 1)
+        parr = (C.c_void_p * max(k, 1))(*[C.c_void_p(u.ctypes.data) for u in ups])
+        sarr = (C.c_size_t * max(k, 1))(*[len(u) for u in ups])
+        pos = np.zeros(max(k * nq, 1), np.uint64)
+        neg = np.zeros(max(k * nq, 1), np.uint64)
+        stats = (_Stats * max(k, 1))()
+        done = C.c_size_t(0)
+        r = lib().bdsm_group_apply_stream(self._h, parr, sarr, k, _ptr(pos), _ptr(neg), stats, C.byref(done))
+        out = [BatchResult(pos[i * nq:i * nq + self.nq].tolist(), neg[i * nq:i * nq + self.nq].tolist(),
+                           _stats_dict(stats[i])) for i in range(done.value)]
+        if r != 0:
+            try:
+                _raise(r, self._e0())
+            except Exception as e:
+                e.done = done.value
+                e.results = out
+                raise
+        return out
+
+    def set_query_active(self, query: int, active: bool) -> None:
+        r = lib().bdsm_group_set_query_active(self._h, query, 1 if active else 0)
+        if r != 0:
+            _raise(r)
+
+    def collect_matches(self, cap: int) -> None:
+        r = lib().bdsm_group_collect_matches(self._h, cap)
+        if r != 0:
+            _raise(r)
+
+    def matches(self, query: int, positive: bool) -> np.ndarray:
+        n = self.query_sizes[query]
+        total = lib().bdsm_group_matches(self._h, query, 1 if positive else 0, None, 0)
+        if total < 0:
+            _raise(int(-total))
+        out = np.zeros((total, n), np.uint32)
+        got = lib().bdsm_group_matches(self._h, query, 1 if positive else 0, _ptr(out), total)
+        if got < 0:
+            _raise(int(-got))
+        return out
+
+    def neighbors(self, v: int, replica: int = 0) -> List[int]:
+        e = lib().bdsm_group_engine(self._h, replica)
+        d = lib().bdsm_engine_neighbors(e, v, None, 0)
+        out = np.zeros(max(d, 1), np.uint32)
+        lib().bdsm_engine_neighbors(e, v, _ptr(out), d)
+        return out[:d].tolist()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().bdsm_group_destroy(self._h)
             self._h = None
 
     def __del__(self):

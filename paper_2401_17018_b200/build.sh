@@ -16,9 +16,10 @@ for f in store match engine; do
 done
 g++ -std=c++17 -O3 -fPIC -fvisibility=hidden -I"$HERE/../include" -I/usr/local/cuda/include \
     -c "$HERE/csrc/planner.cpp" -o "$OBJ/planner.o"
+g++ -std=c++17 -O3 -fPIC -fvisibility=hidden -I"$HERE/../include" -c "$HERE/csrc/group.cpp" -o "$OBJ/group.o"
 for p in "${pids[@]}"; do wait "$p" || { cat "$OBJ"/*.ptxas.log; exit 1; }; done
 "$NVCC" -shared -gencode arch=compute_100a,code=sm_100a -o "$OUT" \
-    "$OBJ/store.o" "$OBJ/match.o" "$OBJ/engine.o" "$OBJ/planner.o"
+    "$OBJ/store.o" "$OBJ/match.o" "$OBJ/engine.o" "$OBJ/planner.o" "$OBJ/group.o" -lpthread
 echo "built $OUT"
 [ -n "${BDSM_OUT:-}" ] && exit 0
 # `bdsm run` CLI (drop-in for the reference's tools/bdsm.cpp), linked against the C ABI

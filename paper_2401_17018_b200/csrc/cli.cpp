@@ -73,6 +73,7 @@ struct Args {
   unsigned group_bits = 2;
   bool no_pipeline = false, dump_matches = false;
   int device = 0;
+  std::vector<std::int32_t> devices;  // --devices a,b,...: a multi-device group (work units split over them)
   bool generate_only = false;
 };
 
@@ -83,7 +84,7 @@ struct Args {
                "                [--workers N] [--group-size N] [--stealing off|passive|active]\n"
                "                [--coalesce on|off] [--timeout S] [--seed N] [--out DIR]\n"
                "                [--group-bits N] [--dump-plan FILE] [--no-pipeline] [--dump-matches]\n"
-               "                [--device N]\n";
+               "                [--device N] [--devices N,N,...]\n";
   std::exit(msg.empty() ? 0 : 109);  // CLI11 parse errors exit non-zero
 }
 
@@ -127,6 +128,12 @@ Args parse(int argc, char** argv) {
       else if (k == "--seed") a.seed = std::stoull(v);
       else if (k == "--group-bits") a.group_bits = unsigned(std::stoul(v));
       else if (k == "--device") a.device = std::stoi(v);
+      else if (k == "--devices") {
+        std::stringstream ds(v);
+        std::string tok;
+        while (std::getline(ds, tok, ',')) a.devices.push_back(std::stoi(tok));
+        if (a.devices.empty()) throw std::invalid_argument("empty device list");
+      }
       else usage("The following argument was not expected: " + k);
     } catch (const std::logic_error&) {
       usage("bad value for " + k + ": " + v);
@@ -198,7 +205,7 @@ int run(const Args& args) {
   opts.group_bits = args.group_bits;
   opts.device = args.device;
   opts.coalesce = args.coalesce == "on" ? 1u : 0u;
-  Engine engine(g.vertices, g.edges, opts);
+  Engine engine(g.vertices, g.edges, opts, args.devices);
   std::vector<QueryRun> queries;
   if (!args.query.empty()) {
     queries.push_back({bdsm::text::load_query_file(args.query), "file", {}, 0, true});

@@ -1947,6 +1947,9 @@ const char* bdsm_version(void) { return "bdsm_b200 0.1 (sm_100a)"; }
 
 const char* bdsm_last_error(void) { return g_last_error.c_str(); }
 
+// group.cpp's failures (not exported)
+void bdsm_internal_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
 bdsm_status bdsm_engine_create(const bdsm_graph_desc* graph, const bdsm_options* opts, bdsm_engine** out) {
   if (!out) return fail(BDSM_INVALID_ARGUMENT, "null output pointer");
   *out = nullptr;

@@ -127,3 +127,22 @@ def test_cli_exact_coalescing_matches_reference(name, tmp_path):
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == meta["summary"].replace("OUT/", out + "/")
     assert read(os.path.join(out, "deltas.csv")) == read(os.path.join(GOLD, name, "ref", "deltas.csv"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_cli_multi_device_group_matches_reference(name, tmp_path):
+    """`--devices 0,0,0`: a multi-device group (replicas, work units split over
+    three engines sharing the one GPU) writes the reference's deltas and match
+    dumps."""
+    meta = case(name)
+    out = str(tmp_path / "out")
+    dump = ["--dump-matches"] if meta.get("dump_matches") else []
+    r = subprocess.run([CLI, "run"] + cli_args(name, meta, out) + dump + ["--devices", "0,0,0"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == meta["summary"].replace("OUT/", out + "/")
+    ref = os.path.join(GOLD, name, "ref")
+    assert read(os.path.join(out, "deltas.csv")) == read(os.path.join(ref, "deltas.csv"))
+    for f in sorted(f for f in os.listdir(ref) if f.startswith("matches_batch")):
+        assert read(os.path.join(out, f)) == read(os.path.join(ref, f)), f
