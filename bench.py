@@ -180,10 +180,20 @@ def cpu_model():
 
 
 def so_sha():
+    """Build identity of the engine: a hash of its sources and build script
+    (nvcc's fatbinaries embed temporary names, so the .so bytes differ between
+    two builds of the same sources)."""
+    import glob
     import hashlib
-    import paper_2401_17018_b200 as bd
-    with open(bd.lib_path(), "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    h = hashlib.sha256()
+    pkg = os.path.join(REPO, "paper_2401_17018_b200")
+    files = sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [os.path.join(pkg, "build.sh"),
+                                                                   os.path.join(REPO, "include", "bdsm_gpu.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return "src-" + h.hexdigest()[:16]
 
 
 def physical_roofline(config, mk, mg, bker, bphase_ref, bupd, peak, peak_kind, step_ms, batch):
@@ -228,7 +238,8 @@ def physical_roofline(config, mk, mg, bker, bphase_ref, bupd, peak, peak_kind, s
                            "re-read working set is L2-resident, the kernel is bound by dependent L2 round trips"},
         })
         m = tr["kernels"]
-        merge = {k: m[k] for k in ("k_alloc", "k_merge_refresh", "k_merge_small", "k_merge_big", "k_finish_big")
+        merge = {k: m[k] for k in ("k_alloc", "k_merge_refresh", "k_merge_small", "k_merge_group", "k_merge_big",
+                                   "k_finish_big")
                  if k in m}
         if merge:
             md = sum(v["dram_bytes_per_step"] for v in merge.values())
