@@ -11,11 +11,32 @@
 
 #include <cub/cub.cuh>
 
+#include <mutex>
+#include <unordered_map>
+
 namespace bdsm_b200 {
 
 namespace {
 
 constexpr int kThreads = 256;
+
+// CTAs of `kernel` resident on the whole GPU at `threads` per CTA (one wave).
+// The merge kernels stride over their lists statically, so a grid of 1.33
+// waves (1184 CTAs where 888 fit) takes two waves' time.
+template <typename K>
+uint64_t resident_ctas(K kernel, int threads, int num_sms) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> per_sm;  // (kernel) -> CTAs per SM at `threads`
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = per_sm.find(key);
+  if (it == per_sm.end()) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, 0) != cudaSuccess || n < 1) n = 1;
+    it = per_sm.emplace(key, n).first;
+  }
+  return uint64_t(num_sms) * uint64_t(it->second);
+}
 
 inline unsigned blocks_for(uint64_t n, int threads = kThreads) {
   uint64_t b = (n + threads - 1) / threads;
@@ -752,27 +773,32 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
   agg.flush(colsize, nq);
 }
 
-// k_merge_small's run copies: full blocks of 8 entries without predicates (8
-// loads in flight, then 8 stores), the remainder predicated; kLab: the graph
-// has edge labels, moved alongside.
+// k_merge_small's run copies: full blocks of kRunUnroll entries without
+// predicates (kRunUnroll loads in flight, then the stores), the remainder in
+// predicated blocks of 8; kLab: the graph has edge labels, moved alongside.
+#ifndef BDSM_RUN_UNROLL
+#define BDSM_RUN_UNROLL 16
+#endif
+constexpr uint32_t kRunUnroll = BDSM_RUN_UNROLL;
 template <bool kLab>
 __device__ __forceinline__ void run_up(const uint32_t* src, uint32_t* dst, const uint32_t* esrc, uint32_t* edst,
                                        uint32_t from, uint32_t to, uint32_t len) {
+  constexpr uint32_t U = kLab ? 8 : kRunUnroll;
   uint32_t b = 0;
-  for (; b + 8 <= len; b += 8) {
-    uint32_t v[8], l[8];
+  for (; b + U <= len; b += U) {
+    uint32_t v[U], l[U];
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
+    for (uint32_t k = 0; k < U; ++k) {
       v[k] = src[from + b + k];
       if (kLab) l[k] = esrc[from + b + k];
     }
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
+    for (uint32_t k = 0; k < U; ++k) {
       dst[to + b + k] = v[k];
       if (kLab) edst[to + b + k] = l[k];
     }
   }
-  if (b < len) {
+  for (; b < len; b += 8) {
     uint32_t v[8], l[8];
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
@@ -790,32 +816,35 @@ __device__ __forceinline__ void run_up(const uint32_t* src, uint32_t* dst, const
 template <bool kLab>
 __device__ __forceinline__ void run_down(const uint32_t* src, uint32_t* dst, const uint32_t* esrc, uint32_t* edst,
                                          uint32_t from, uint32_t to, uint32_t len) {
+  constexpr uint32_t U = kLab ? 8 : kRunUnroll;
   uint32_t b = len;
-  for (; b >= 8; b -= 8) {
-    uint32_t v[8], l[8];
+  for (; b >= U; b -= U) {
+    uint32_t v[U], l[U];
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
-      v[k] = src[from + b - 8 + k];
-      if (kLab) l[k] = esrc[from + b - 8 + k];
+    for (uint32_t k = 0; k < U; ++k) {
+      v[k] = src[from + b - U + k];
+      if (kLab) l[k] = esrc[from + b - U + k];
     }
 #pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
-      dst[to + b - 8 + k] = v[k];
-      if (kLab) edst[to + b - 8 + k] = l[k];
+    for (uint32_t k = 0; k < U; ++k) {
+      dst[to + b - U + k] = v[k];
+      if (kLab) edst[to + b - U + k] = l[k];
     }
   }
-  if (b) {
+  while (b) {  // the remainder, highest block first (in place the entries move right)
+    const uint32_t nb = b < 8 ? b : 8;
+    b -= nb;
     uint32_t v[8], l[8];
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k) {
-      v[k] = k < b ? src[from + k] : 0u;
-      if (kLab) l[k] = k < b ? esrc[from + k] : 0u;
+      v[k] = k < nb ? src[from + b + k] : 0u;
+      if (kLab) l[k] = k < nb ? esrc[from + b + k] : 0u;
     }
 #pragma unroll
     for (uint32_t k = 0; k < 8; ++k)
-      if (k < b) {
-        dst[to + k] = v[k];
-        if (kLab) edst[to + k] = l[k];
+      if (k < nb) {
+        dst[to + b + k] = v[k];
+        if (kLab) edst[to + b + k] = l[k];
       }
   }
 }
@@ -928,21 +957,19 @@ __global__ void __launch_bounds__(256) k_merge_small(
       for (uint32_t k = 0; k < qenc[q].nsig; ++k) memo_invalidate_v(g.memo_bits, memo, memo_mask, x, q, qenc[q].sig[k]);
     // label index of the new list from the old one: class k's first
     // position moves by the inserts minus the deletes below class_lo[k]
-    uint32_t lpos[kMaxLabelIndex + 1];
+    // (a two-pointer walk over the sorted keys, the row rewritten in place;
+    // no per-thread array, which lived in local memory)
     const bool indexed = g.loff != nullptr;
+    uint32_t* lrow = indexed ? g.loff + uint64_t(x) * (g.nlab + 1) : nullptr;
     if (indexed) {
-      uint32_t* row = g.loff + uint64_t(x) * (g.nlab + 1);
-      for (uint32_t k = 0; k < g.nlab; ++k) lpos[k] = row[k];
       int acc = 0;
-      uint32_t ci = 0;
-      for (uint32_t k = 0; k < segn; ++k) {
-        const uint32_t y = uint32_t(seg[k]);
-        while (ci < g.nlab && g.class_lo[ci] <= y) lpos[ci++] += acc;
-        acc += (svals[s + k] >> 31) ? -1 : 1;
+      uint32_t j = 0;
+      for (uint32_t k = 0; k < g.nlab; ++k) {
+        const uint32_t lo = g.class_lo[k];
+        for (; j < segn && uint32_t(seg[j]) < lo; ++j) acc += (svals[s + j] >> 31) ? -1 : 1;
+        lrow[k] = uint32_t(int(lrow[k]) + acc);
       }
-      while (ci < g.nlab) lpos[ci++] += acc;
-      lpos[g.nlab] = dnew;
-      for (uint32_t k = 0; k <= g.nlab; ++k) row[k] = lpos[k];
+      lrow[g.nlab] = dnew;
     }
     const uint32_t vl = g.vlabel[x];
     for (uint32_t q = 0; q < nq; ++q) {
@@ -952,7 +979,7 @@ __global__ void __launch_bounds__(256) k_merge_small(
         uint32_t c = 0;
         if (indexed) {
           const uint32_t cls = qe.gcls[gi];
-          c = cls == kNone ? 0u : lpos[cls + 1] - lpos[cls];
+          c = cls == kNone ? 0u : lrow[cls + 1] - lrow[cls];
         } else {
           for (uint32_t i = 0; i < dnew; ++i) c += dst[i] >= qe.glo[gi] && dst[i] < qe.ghi[gi];
         }
@@ -1593,7 +1620,7 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   // one warp per touched vertex (<= m), persistent over a bounded grid
   uint64_t warps = m ? m : 1;
   uint64_t blocks = (warps * 32 + 255) / 256;
-  uint64_t cap = uint64_t(num_sms) * 8;
+  const uint64_t cap = resident_ctas(k_merge_refresh, 256, num_sms);
   if (blocks > cap) blocks = cap;
   k_merge_refresh<<<unsigned(blocks), 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off,
                                                   new_cap, ipos, qenc, nq, rows, colsize, st, memo, memo_mask,
@@ -1602,12 +1629,14 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   // group of that many lanes per list (k_merge_group), 0 = none (k_alloc did
   // not split them off)
   if (small_mode == 1)
-    k_merge_small<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) + 255) / 256, uint64_t(num_sms) * 8)), 256,
+    k_merge_small<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) + 255) / 256,
+                                                resident_ctas(k_merge_small, 256, num_sms))), 256,
                     0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, qenc, nq, rows, colsize,
                             st, memo, memo_mask, small_list);
   else if (small_mode == 8 || small_mode == 16) {
-    const unsigned gb = unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * small_mode + 255) / 256,
-                                                    uint64_t(num_sms) * 8));
+    const unsigned gb = unsigned(std::min<uint64_t>(
+        (uint64_t(m ? m : 1) * small_mode + 255) / 256,
+        small_mode == 8 ? resident_ctas(k_merge_group<8>, 256, num_sms) : resident_ctas(k_merge_group<16>, 256, num_sms)));
     if (small_mode == 8)
       k_merge_group<8><<<gb, 256, 0, s>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, small_list);
@@ -1618,9 +1647,11 @@ void launch_merge_refresh(const uint32_t* heads, const uint64_t* skeys, const ui
   // a CTA per long list (k_alloc's list), so long lists merge concurrently
   // long lists (disjoint from the others; shared structures are updated with
   // atomics) on s_big, which the caller may run beside s
-  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, uint64_t(num_sms) * 16)), BDSM_BIG_THREADS, 0, s_big>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
+  k_merge_big<<<unsigned(std::min<uint64_t>(m ? m : 1, resident_ctas(k_merge_big, BDSM_BIG_THREADS, num_sms))),
+                BDSM_BIG_THREADS, 0, s_big>>>(heads, skeys, svals, ins_prefix, m, ups, g, new_off, new_cap, ipos, qenc,
                                           nq, rows, colsize, st, memo, memo_mask, big_list);
-  k_finish_big<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * 32 + 255) / 256, uint64_t(num_sms) * 8)), 256, 0,
+  k_finish_big<<<unsigned(std::min<uint64_t>((uint64_t(m ? m : 1) * 32 + 255) / 256,
+                                             resident_ctas(k_finish_big, 256, num_sms))), 256, 0,
                  s_big>>>(heads, skeys, svals, m, g, qenc, nq, rows, colsize, st, memo, memo_mask, big_list);
 }
 void launch_encode_all(DevGraph g, const DevQueryEnc* qenc, uint32_t* rows, int num_sms, cudaStream_t s) {
