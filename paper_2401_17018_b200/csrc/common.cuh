@@ -283,6 +283,9 @@ struct BatchState {
                                  // the sorted bits, 6 a preceding batch of the stream aborted
   uint32_t n_tasks[2];           // per phase (0 negative, 1 positive), last query
   uint32_t n_items[2];
+  uint32_t item_lo[2], item_hi[2];  // multi-GPU: this rank's work items per phase, a contiguous index range
+                                    // (owners are monotone in the canonical order), so k_wbm never walks
+                                    // the other ranks' items
   uint32_t donations;            // statistics: donated subtrees
   uint32_t n_big;                // long lists this batch (k_alloc -> k_merge_big)
   uint32_t n_small;              // short lists this batch (k_alloc -> k_merge_small)

@@ -97,6 +97,10 @@ __device__ __forceinline__ void for_each_anchor(const PhaseArgs& a, uint32_t i, 
 
 __global__ void k_anchor_count(PhaseArgs a) {
   if (batch_aborted(a.st)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // k_anchor_emit narrows this rank's item range
+    a.st->item_lo[a.phase] = kNone;
+    a.st->item_hi[a.phase] = 0;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= a.n_ups; i += gridDim.x * blockDim.x) {
     uint32_t nt = 0, ni = 0;
     uint64_t cost = 0;
@@ -201,6 +205,7 @@ __global__ void k_anchor_emit(PhaseArgs a) {
   if (total_items > a.max_items) return;
   uint64_t direct = 0;    // 2-vertex queries: every anchor is a match
   uint64_t bytes = 0, calls = 0;
+  uint32_t my_lo = kNone, my_hi = 0;  // this thread's items owned by this rank
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ups; i += gridDim.x * blockDim.x) {
     const AnchorCount off = a.self_scan ? self_off : a.upd_off[i];
     uint32_t t = off.tasks, it = off.items;
@@ -234,6 +239,10 @@ __global__ void k_anchor_emit(PhaseArgs a) {
         uint32_t owner = a.shard_world > 1
                              ? uint32_t((unsigned __int128)(c + b) * a.shard_world / total_cost)
                              : 0;
+        if (owner == a.shard_rank) {
+          my_lo = min(my_lo, it);
+          my_hi = it + 1;
+        }
         a.items[it++] = Item{owner == a.shard_rank ? t : kNone, b};
       }
       ++t;
@@ -241,6 +250,13 @@ __global__ void k_anchor_emit(PhaseArgs a) {
     });
   }
   if (direct) atomicAdd(a.count_out, (unsigned long long)direct);
+  if (a.shard_world > 1) {
+    const uint32_t wlo = __reduce_min_sync(kFull, my_lo), whi = __reduce_max_sync(kFull, my_hi);
+    if ((threadIdx.x & 31) == 0 && wlo != kNone) {
+      atomicMin(&a.st->item_lo[a.phase], wlo);
+      atomicMax(&a.st->item_hi[a.phase], whi);
+    }
+  }
   if (a.shard_rank == 0 && bytes) {
     atomicAdd((unsigned long long*)&a.st->bytes_phase, (unsigned long long)bytes);
     atomicAdd((unsigned long long*)&a.st->gen_calls, (unsigned long long)calls);
@@ -852,9 +868,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
   // a donated item records its phase.  Queue, donation slots, memo and graph
   // are shared; a phase whose batch was aborted contributes no items.
   const PhaseArgs& a0 = pp.p[0];
-  const uint32_t n0 = batch_aborted(a0.st) ? 0u : a0.st->n_items[a0.phase];
-  const uint32_t n1 = kPairs < 2 || batch_aborted(pp.p[kPairs - 1].st) ? 0u
-                                                                      : pp.p[kPairs - 1].st->n_items[pp.p[kPairs - 1].phase];
+  // static items of each phase: all of them, or this rank's contiguous range
+  auto phase_items = [](const PhaseArgs& a, uint32_t& lo) -> uint32_t {
+    lo = 0;
+    if (batch_aborted(a.st)) return 0u;
+    if (a.shard_world <= 1) return a.st->n_items[a.phase];
+    const uint32_t l = a.st->item_lo[a.phase], h = a.st->item_hi[a.phase];
+    lo = l;
+    return h > l ? h - l : 0u;
+  };
+  uint32_t lo0 = 0, lo1 = 0;
+  const uint32_t n0 = phase_items(a0, lo0);
+  const uint32_t n1 = kPairs < 2 ? 0u : phase_items(pp.p[kPairs - 1], lo1);
   const uint32_t n_items = n0 + n1;
   if (n_items == 0) return;
   const uint32_t lane = threadIdx.x & 31;
@@ -959,7 +984,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinBlocks) k_wbm(const _
 #endif
     uint32_t task_id, lstart, rbegin, rend, ncand = 0;
     if (kind == 1) {
-      const Item item = a.items[ref];
+      const Item item = a.items[(sel ? lo1 : lo0) + ref];
       task_id = item.task;
       lstart = 2;
       rbegin = item.begin;
