@@ -632,9 +632,13 @@ __device__ __forceinline__ void finish_vertex(DevGraphMut& g, uint32_t x, const 
 constexpr uint32_t kMoveUnroll = 8;      // old elements per thread in flight per sweep step (k_merge_big)
 constexpr uint32_t kWarpMoveUnroll = 4;  // the same for k_merge_refresh (lists < kBigList)
 constexpr uint32_t kWarpSearchKeys = 4;  // k_merge_refresh: segments up to this many keys use warp searches
-// k_merge_refresh is latency-bound over many short lists: a tighter register
-// budget (6 CTAs = 48 warps per SM) keeps more lists in flight
-constexpr int kMergeWarpBlocks = 6;
+// k_merge_refresh is latency-bound over many lists: its register budget sets
+// how many are in flight per SM.  5 CTAs: 48 registers (C4 279.2M updates/s,
+// C2 12.38M); 6: 40 with 116 B of spills (280.8M, 12.17M); 4: 61 (277.8M)
+#ifndef BDSM_MERGE_WARP_BLOCKS
+#define BDSM_MERGE_WARP_BLOCKS 5
+#endif
+constexpr int kMergeWarpBlocks = BDSM_MERGE_WARP_BLOCKS;
 
 // K3 (part 2) + K4: one warp per touched vertex.  Insert slots are computed
 // first against the intact old list.  In place (merged list fits the slack)
@@ -689,12 +693,24 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
     // that can move (entries below the first batch key never move).  A few
     // keys are searched one after another by the whole warp (two dependent
     // loads each below 1024 entries); many keys by one lane each.
-    uint32_t start = 0;
+    // With <= 32 keys, lane k also keeps key k's position in the old list
+    // (k_lb) and kind (k_del): a moved element's merged position then comes
+    // from ballots over the keys instead of a search per element.
+    uint32_t start = 0, k_lb = 0;
+    bool k_del = false;
+#ifdef BDSM_NO_KEY_LANES
+    const bool keys_in_lanes = false;
+#else
+    const bool keys_in_lanes = segn <= 32;
+#endif
     if (segn <= kWarpSearchKeys) {
       for (uint32_t k = 0; k < segn; ++k) {
         const bool del = svals[s + k] >> 31;
-        if (del && (k || reloc)) continue;
         const uint32_t lb = warp_lower_bound(src, dold, uint32_t(seg[k]), lane);
+        if (lane == k) {
+          k_lb = lb;
+          k_del = del;
+        }
         if (k == 0 && !reloc) start = lb;
         if (!del && lane == 0) {
           const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
@@ -702,15 +718,18 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
         }
       }
     } else {
-      if (lane == 31 && !reloc && dold) start = lower_bound_u32(src, dold, uint32_t(seg[0]));
       for (uint32_t k = lane; k < segn; k += 32) {
-        if (svals[s + k] >> 31) continue;  // delete
-        uint32_t y = uint32_t(seg[k]);
-        uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
-        uint32_t db = k - ib;
-        ipos[s + k] = ib + (lower_bound_u32(src, dold, y) - db);
+        const bool del = svals[s + k] >> 31;
+        const uint32_t lb = lower_bound_u32(src, dold, uint32_t(seg[k]));
+        if (k < 32) {
+          k_lb = lb;
+          k_del = del;
+        }
+        if (del) continue;
+        const uint32_t ib = ins_prefix[s + k] - ins_prefix[s];
+        ipos[s + k] = ib + (lb - (k - ib));
       }
-      start = __shfl_sync(kFull, start, 31);
+      if (!reloc && dold) start = __shfl_sync(kFull, k_lb, 0);
     }
     __syncwarp();
     // 2. move old elements
@@ -731,13 +750,56 @@ __global__ void __launch_bounds__(256, kMergeWarpBlocks) k_merge_refresh(
           if (esrc) el[k] = esrc[i];
         }
       }
+      if (keys_in_lanes) {
+        // old element i: inserts before it = insert keys with position <= i,
+        // deletes before it = delete keys with position < i, deleted if a
+        // delete key sits at i.  Keys before the window by ballot, the few
+        // inside it one by one.
+        const bool live = lane < segn;
+        const uint32_t ins_before = __popc(__ballot_sync(kFull, live && !k_del && k_lb < base));
+        const uint32_t del_before = __popc(__ballot_sync(kFull, live && k_del && k_lb < base));
+        uint32_t win = __ballot_sync(kFull, live && k_lb >= base && k_lb < base + step);
+        uint32_t I[kWarpMoveUnroll], D[kWarpMoveUnroll];
+        bool dl[kWarpMoveUnroll];
 #pragma unroll
-      for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
-        const uint32_t i = base + k * 32 + lane;
-        if (i < dold) {
-          bool dl;
-          merged_pos(seg, segn, ins_prefix, s, a[k], i, p[k], dl);
-          mv[k] = !dl && (reloc || p[k] != i);
+        for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
+          I[k] = ins_before;
+          D[k] = del_before;
+          dl[k] = false;
+        }
+        while (win) {
+          const uint32_t kk = __ffs(win) - 1;
+          win &= win - 1;
+          const uint32_t lb = __shfl_sync(kFull, k_lb, kk);
+          const bool del = __shfl_sync(kFull, k_del ? 1u : 0u, kk);
+#pragma unroll
+          for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
+            const uint32_t i = base + k * 32 + lane;
+            if (del) {
+              D[k] += lb < i;
+              dl[k] |= lb == i;
+            } else {
+              I[k] += lb <= i;
+            }
+          }
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
+          const uint32_t i = base + k * 32 + lane;
+          if (i < dold) {
+            p[k] = i - D[k] + I[k];
+            mv[k] = !dl[k] && (reloc || p[k] != i);
+          }
+        }
+      } else {
+#pragma unroll
+        for (uint32_t k = 0; k < kWarpMoveUnroll; ++k) {
+          const uint32_t i = base + k * 32 + lane;
+          if (i < dold) {
+            bool dl;
+            merged_pos(seg, segn, ins_prefix, s, a[k], i, p[k], dl);
+            mv[k] = !dl && (reloc || p[k] != i);
+          }
         }
       }
       __syncwarp();
