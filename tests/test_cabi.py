@@ -47,3 +47,16 @@ def test_no_gpu_fails_loudly():
     import paper_2401_17018_b200 as bd
     with pytest.raises(bd.EngineError):
         bd.Engine([0, 0], [0], [1])
+
+
+def test_group_without_gpu_fails_loudly():
+    """The multi-device group reports the device failure of its engines (no
+    CPU fallback), and rejects an empty device list."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2401_17018_b200 as bd
+    with pytest.raises(bd.EngineError, match="device 0"):
+        bd.EngineGroup([0, 0], [0], [1], devices=[0, 0])
+    with pytest.raises(ValueError, match="no devices"):
+        bd.EngineGroup([0, 0], [0], [1], devices=[])
