@@ -263,7 +263,9 @@ BDSM_API size_t bdsm_engine_debug_trace(bdsm_engine* engine, uint64_t* out, size
  * named after (same counts, errors, all-or-nothing contract).  bdsm_options'
  * device / shard fields are set per engine.  Stats: times of the slowest engine,
  * work counters summed.  A query whose deadline fires on any device reports 0/0
- * for that batch.  apply_stream takes host batches only. */
+ * for that batch.  apply_stream takes host batches only.  After a device failure
+ * (BDSM_CUDA_ERROR / BDSM_OUT_OF_MEMORY) on any engine the replicas may differ:
+ * destroy the group. */
 typedef struct bdsm_group bdsm_group;
 BDSM_API bdsm_status bdsm_group_create(const bdsm_graph_desc* graph, const bdsm_options* opts,
                                        const int32_t* devices, uint32_t num_devices, bdsm_group** out);

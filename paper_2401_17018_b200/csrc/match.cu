@@ -1362,12 +1362,17 @@ void launch_leaf_prefill(const PhaseArgs& a, const LeafSig* sigs, uint32_t nsig,
 
 template <bool kEmit, int kMinBlocks, int kPairs>
 void launch_wbm_variant(const PhasePair& pp, int num_sms, cudaStream_t s) {
-  // persistent: as many resident CTAs as the SMs hold
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wbm<kEmit, kMinBlocks, kPairs>, kWarpsPerBlock * 32, 0);
-    if (per_sm <= 0) per_sm = 1;
-  }
+  // persistent: as many resident CTAs as the SMs hold (queried once per
+  // variant; a function-local static is initialised once even when engines on
+  // several host threads launch concurrently, e.g. a multi-device group)
+  static const int per_sm = [] {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_wbm<kEmit, kMinBlocks, kPairs>, kWarpsPerBlock * 32, 0) !=
+            cudaSuccess ||
+        n <= 0)
+      n = 1;
+    return n;
+  }();
   k_wbm<kEmit, kMinBlocks, kPairs><<<unsigned(num_sms * per_sm), kWarpsPerBlock * 32, 0, s>>>(pp);
 }
 
