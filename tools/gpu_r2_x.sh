@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # Round 2, final call (x, after the thread-safe occupancy query): traffic captures of this build first (so the bench lines read their own build's
-# physical bytes), GPU tests, smoke, the default bench line and the reference arm, the launch list, C4,
+# physical bytes), GPU tests, smoke, the default bench line, C4 and the launch list.
 O=gpurun_out/x; mkdir -p $O
 SHA=$(python -c "import bench; print(bench.so_sha())" 2>/dev/null)
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum \
