@@ -573,12 +573,17 @@ class EngineGroup:
         r = lib().bdsm_group_collect_matches(self._h, cap)
         if r != 0:
             _raise(r)
+        self._collect_cap = cap
 
     def matches(self, query: int, positive: bool) -> np.ndarray:
+        """The last batch's matches of `query` over every engine, merged and sorted."""
         n = self.query_sizes[query]
         total = lib().bdsm_group_matches(self._h, query, 1 if positive else 0, None, 0)
         if total < 0:
             _raise(int(-total))
+        if total > getattr(self, "_collect_cap", 0):  # as Engine.matches: the cap bounds the total
+            raise EngineError(f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
+                              "(raise the collect_matches cap)")
         out = np.zeros((total, n), np.uint32)
         got = lib().bdsm_group_matches(self._h, query, 1 if positive else 0, _ptr(out), total)
         if got < 0:

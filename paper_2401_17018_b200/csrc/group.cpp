@@ -26,6 +26,7 @@ struct bdsm_group {
   std::vector<bdsm_engine*> engines;
   std::vector<int32_t> devices;
   std::vector<uint32_t> nverts;  // per query: vertices (match rows)
+  uint64_t collect_cap = 0;      // per engine (bdsm_group_collect_matches)
   std::vector<uint8_t> timed;    // per query: timed out in some engine during the last batch
 };
 
@@ -276,24 +277,30 @@ bdsm_status bdsm_group_collect_matches(bdsm_group* g, uint64_t cap) {
     const bdsm_status s = bdsm_engine_collect_matches(e, cap);
     if (s != BDSM_OK) return s;
   }
+  g->collect_cap = cap;
   return BDSM_OK;
 }
 
 int64_t bdsm_group_matches(bdsm_group* g, int query, int phase, uint32_t* out, size_t cap) {
   if (!g || query < 0 || size_t(query) >= g->nverts.size()) return -int64_t(BDSM_INVALID_ARGUMENT);
   const size_t n = g->nverts[size_t(query)];
-  std::vector<uint32_t> all;
   int64_t total = 0;
-  for (bdsm_engine* e : g->engines) {  // each engine holds the matches of its own work units
-    const int64_t c = bdsm_engine_matches(e, query, phase, nullptr, 0);
-    if (c < 0) return c;
-    // rows beyond what the engine collected (its cap) stay ~0 and are dropped
-    std::vector<uint32_t> m(size_t(c) * n, ~0u);
-    const int64_t c2 = bdsm_engine_matches(e, query, phase, m.data(), size_t(c));
+  std::vector<int64_t> per(g->engines.size());
+  for (size_t r = 0; r < g->engines.size(); ++r) {  // counts first: no rows are fetched for a count query
+    per[r] = bdsm_engine_matches(g->engines[r], query, phase, nullptr, 0);
+    if (per[r] < 0) return per[r];
+    total += per[r];
+  }
+  if (!out) return total;
+  std::vector<uint32_t> all;
+  for (size_t r = 0; r < g->engines.size(); ++r) {  // each engine holds the matches of its own work units
+    // at most the engine's cap of rows exists; rows beyond what it collected stay ~0 and are dropped
+    const size_t rows = size_t(std::min<uint64_t>(uint64_t(per[r]), g->collect_cap));
+    std::vector<uint32_t> m(rows * n, ~0u);
+    const int64_t c2 = bdsm_engine_matches(g->engines[r], query, phase, m.data(), rows);
     if (c2 < 0) return c2;
-    for (size_t i = 0; n && i < size_t(c); ++i)
+    for (size_t i = 0; n && i < rows; ++i)
       if (m[i * n] != ~0u) all.insert(all.end(), m.begin() + i * n, m.begin() + (i + 1) * n);
-    total += c;
   }
   // one sorted list, as a single engine reports it (src/matcher.cpp:365-366)
   const size_t have = n ? all.size() / n : 0;

@@ -79,3 +79,20 @@ def test_group_matches_equal_single_engine():
                 assert np.array_equal(g.matches(0, pos), e.matches(0, pos)), inst["name"]
         e.close()
         g.close()
+
+
+def test_group_matches_cap():
+    """More matches than the collect cap: the count is reported and the rows
+    are refused (Engine.matches' contract), without fetching them."""
+    import paper_2401_17018_b200 as bd
+    fig = {i["name"]: i for i in gu.load("fig1")}
+    g, _ = _group(fig["fig1_batch"], [0, 0])
+    g.collect_matches(2)
+    r = g.match_batch([(0, 0, 2), (0, 1, 4), (1, 4, 5)])
+    assert r.positive == [4]
+    with pytest.raises(bd.EngineError, match="4 matches"):
+        g.matches(0, True)
+    g.collect_matches(8)
+    r = g.match_batch([(1, 0, 2)])  # deleting (0, 2) removes the matches through it
+    assert len(g.matches(0, False)) == r.negative[0]
+    g.close()
