@@ -419,7 +419,7 @@ class Engine:
         if total < 0:
             _raise(int(-total), self._h)
         if total > getattr(self, "_collect_cap", 0):
-            raise EngineError(f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
+            raise EngineError(3, f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
                               "(raise the collect_matches cap)")
         out = np.zeros((total, n), np.uint32)
         got = lib().bdsm_engine_matches(self._h, query, 1 if positive else 0, _ptr(out), total)
@@ -582,7 +582,7 @@ class EngineGroup:
         if total < 0:
             _raise(int(-total))
         if total > getattr(self, "_collect_cap", 0):  # as Engine.matches: the cap bounds the total
-            raise EngineError(f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
+            raise EngineError(3, f"{total} matches, only {getattr(self, '_collect_cap', 0)} collected "
                               "(raise the collect_matches cap)")
         out = np.zeros((total, n), np.uint32)
         got = lib().bdsm_group_matches(self._h, query, 1 if positive else 0, _ptr(out), total)

@@ -96,3 +96,17 @@ def test_group_matches_cap():
     r = g.match_batch([(1, 0, 2)])  # deleting (0, 2) removes the matches through it
     assert len(g.matches(0, False)) == r.negative[0]
     g.close()
+
+
+def test_engine_matches_cap():
+    """Engine.matches refuses a truncated match set the same way."""
+    import paper_2401_17018_b200 as bd
+    fig = {i["name"]: i for i in gu.load("fig1")}
+    vl, eu, ev, el, ql, qe, _ = gu.instance_arrays(fig["fig1_batch"])
+    e = bd.Engine(vl, eu, ev, el)
+    e.add_query(ql, qe)
+    e.collect_matches(2)
+    assert e.match_batch([(0, 0, 2), (0, 1, 4), (1, 4, 5)]).positive == [4]
+    with pytest.raises(bd.EngineError, match="4 matches"):
+        e.matches(0, True)
+    e.close()
