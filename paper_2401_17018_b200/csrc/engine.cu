@@ -224,8 +224,17 @@ struct bdsm_engine {
   uint32_t tune_backoff = env_u32("BDSM_TUNE_BACKOFF", 0);
   uint32_t tune_merge_ratio = env_u32("BDSM_TUNE_MERGE", 8);
   uint32_t tune_variant = env_u32("BDSM_TUNE_VARIANT", 0);  // 2 / 3 / 4: force a matching-kernel variant
-  // the variant of launches with many work items (4: 4 CTAs/SM, 64 registers; 3: 3 CTAs/SM, 80 registers)
-  uint32_t tune_variant_tp = env_u32("BDSM_TUNE_VARIANT_THROUGHPUT", 3);
+  // the variant of launches with many work items (4: 4 CTAs/SM, 64 registers; 3: 3 CTAs/SM, 80 registers):
+  // 4 up to tune_many_items items per phase (C3, ~10K: 69.5K vs 66.1K updates/s), 3 above (C4, ~30K: +3 %);
+  // BDSM_TUNE_VARIANT_THROUGHPUT forces one of them
+  uint32_t tune_variant_tp = env_u32("BDSM_TUNE_VARIANT_THROUGHPUT", 0);
+  uint32_t tune_many_items = env_u32("BDSM_TUNE_MANY_ITEMS", 16000);
+  int variant_for(uint32_t items) const {
+    if (tune_variant) return int(tune_variant);
+    if (items <= tune_throughput_items) return 2;
+    if (tune_variant_tp) return int(tune_variant_tp);
+    return items > tune_many_items ? 3 : 4;
+  }
   uint32_t tune_no_tasktail = env_u32("BDSM_TUNE_NO_TASKTAIL", 0);  // 1: recount anchor-only tail levels per item
   uint32_t tune_throughput_items = env_u32("BDSM_TUNE_ITEMS", kThroughputItems);
   // short lists (<= tune_small_max entries before and after) of batches with at
@@ -1106,8 +1115,7 @@ struct bdsm_engine {
           a.task_tail = B().task_tail.p;
         }
         // variant by the previous batch's work items of this (query, phase)
-        const int variant = tune_variant ? int(tune_variant)
-                                         : qs.prev_items[phase] > tune_throughput_items ? int(tune_variant_tp) : 2;
+        const int variant = variant_for(qs.prev_items[phase]);
         a.backoff_max = tune_backoff ? tune_backoff : variant == 2 ? 256u : 1024u;
         launch_wbm(a, nullptr, num_sms, variant, stream);
         CK(cudaEventRecord(next_kev(), stream));
@@ -1633,7 +1641,7 @@ struct bdsm_engine {
     PhaseArgs x = first;
     x.epoch = ++epoch;
     const uint32_t items = std::max(qs.prev_items[0], qs.prev_items[1]);
-    const int variant = tune_variant ? int(tune_variant) : items > tune_throughput_items ? int(tune_variant_tp) : 2;
+    const int variant = variant_for(items);
     x.backoff_max = tune_backoff ? tune_backoff : variant == 2 ? 256u : 1024u;
     CK(cudaEventRecord(next_skev(), stream));
     launch_wbm(x, a && b ? b : nullptr, num_sms, variant, stream);
